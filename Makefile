@@ -1,0 +1,32 @@
+# Builds the in-tree CUDA library (sm_100a only) and the CPU oracle.
+#
+#   make            -> paper_2410_18944_b200/libwostgpu.so + oracle/liboracle.so (+ oracle/_ref)
+#
+# -fmad=false: the walk path keeps the reference's fp64 operation order
+# (no FMA contraction) so geometry and per-walk results are bit-comparable
+# with the reference; kernels that do not need this use explicit fmaf().
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC,-O2 \
+           --expt-relaxed-constexpr -Xptxas -warn-spills
+PKG := paper_2410_18944_b200
+SRC := $(wildcard $(PKG)/csrc/*.cu)
+HDR := $(wildcard $(PKG)/csrc/*.cuh) include/wostgpu.h include/wostgpu_types.h
+OBJ := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))
+
+all: $(PKG)/libwostgpu.so oracle
+
+build/%.o: $(PKG)/csrc/%.cu $(HDR)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(PKG)/libwostgpu.so: $(OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lnccl -lcudart
+
+oracle:
+	$(MAKE) -C oracle all
+
+clean:
+	rm -rf build $(PKG)/libwostgpu.so
+
+.PHONY: all oracle clean

@@ -1,0 +1,318 @@
+"""Benchmark: guided walk-on-stars walks/s on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], "cfg 2"): preset neumann-strip-vlin
+(proj/src/presets.cpp:217-221), 128x128 cell-centre grid per GPU, 256 walks
+per point, learnable-MIS guiding with online training in every round
+(train_until = 256), default FieldConfig / TrainConfig / SolverConfig, seed 1.
+One step = one complete solve of that configuration (256 wpp rounds, each a
+device walk round plus a training round) = 4,194,304 walks per GPU.
+
+  python bench.py [--gpus N --steps K --warmup W]          our CUDA path
+  python bench.py --impl reference [...]                   the reference C++ on host cores
+
+N > 1 (torchrun, one rank per GPU): weak scaling; rank r owns rows
+[128 r, 128 r + 128) of a 128 x 128N grid over the same domain (global point
+index keys every walk's stream), guiding-field gradients are allreduced over
+NVLink with NCCL before every Adam step.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PRESET = "neumann-strip-vlin"
+GRID = 128
+WPP = 256
+TRAIN_UNTIL = 256
+SEED = 1
+# algorithmic HBM bytes per walk step: 52 B SoA walk state read
+# + written = 104 B; training rounds add a 56 B trace record written + read
+BYTES_PER_STEP = 104
+BYTES_PER_TRAIN_STEP = 112
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index, self.samples, self.proc = index, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for n, v in zip(names, s[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def flush_l2(buf):
+    """Write a buffer larger than the 126 MB L2 between timed steps."""
+    if buf is not None:
+        buf.zero_()
+
+
+def cpu_reference_rate(rounds, threads, preset=PRESET, grid=GRID, mode=3):
+    """The reference's own run_solve (oracle/_ref, Release-flag build) on the
+    host cores for a bounded number of wpp rounds of the same workload."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import REF_FAST_SO, REF_SO, Oracle
+    so = REF_FAST_SO if os.path.exists(REF_FAST_SO) else REF_SO
+    kind = "reference"
+    if not os.path.exists(so):
+        return None
+    os.environ["OMP_NUM_THREADS"] = str(threads)
+    os.environ["WOST_THREADS"] = str(threads)
+    ref = Oracle("ref", so)
+    sec, rel, tsec = (np.zeros(1) for _ in range(3))
+    import ctypes as C
+    rc = ref.lib.ref_run_solve(preset.encode(), grid, grid, rounds, mode, TRAIN_UNTIL, SEED, None,
+                               sec.ctypes.data_as(C.POINTER(C.c_double)),
+                               rel.ctypes.data_as(C.POINTER(C.c_double)),
+                               tsec.ctypes.data_as(C.POINTER(C.c_double)))
+    if rc != 0:
+        return None
+    walks = grid * grid * rounds
+    return {"value": walks / float(sec[0]), "seconds": float(sec[0]), "kind": kind,
+            "train_seconds": float(tsec[0]), "walks": walks}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    rounds = args.ref_rounds
+    for _ in range(args.warmup):
+        cpu_reference_rate(rounds, threads)
+    vals, secs = [], []
+    for _ in range(args.steps):
+        r = cpu_reference_rate(rounds, threads)
+        if r is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+            return
+        vals.append(r["value"])
+        secs.append(r["seconds"])
+    value = float(np.mean(vals))
+    sample = (f"{rounds} of {WPP} wpp rounds of cfg 2 ({PRESET} {GRID}x{GRID}, learnable MIS, "
+              f"training every round) through the reference's run_solve")
+    line = {"metric": "guided WoSt walks/sec", "value": value, "unit": "walks/s",
+            "impl": "reference", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": float(np.mean(secs)) * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cfg2 {PRESET} {GRID}x{GRID} learnable_mis wpp sample {rounds}",
+                       "preset": PRESET, "grid": [GRID, GRID], "rounds_per_step": rounds},
+            "cpu_baseline": {"value": value, "unit": "walks/s", "cores": threads,
+                             "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": "walks/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mlp", default="exact", choices=["exact", "tensor"])
+    ap.add_argument("--ref-rounds", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    from paper_2410_18944_b200 import _lib, abi, api
+    from paper_2410_18944_b200.scene import cell_centers, make_preset, relmse, analytic_image
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    _lib.init(local)
+
+    preset = make_preset(PRESET)
+    bb = preset.scene.bbox
+    # weak scaling: rank r owns rows [GRID r, GRID (r+1)) of a GRID x GRID*world grid
+    all_pts = cell_centers(GRID, GRID * world, bb)
+    n_local = GRID * GRID
+    pts = np.ascontiguousarray(all_pts[rank * n_local:(rank + 1) * n_local])
+    offset = rank * n_local
+
+    fcfg = abi.field_config()
+    field = api.GuidingField(fcfg, bb, SEED)
+    p0, m0, v0, s0 = field.state()
+    scfg = abi.solver_config("learnable_mis")
+    solver = api.Solver(api.Accel(preset.scene), field, scfg,
+                        api.MLP_TENSOR if args.mlp == "tensor" else api.MLP_EXACT)
+    if world > 1:
+        uid = [api.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        solver.attach_comm(uid[0], world, rank)
+    tcfg = abi.train_config(seed=SEED)
+    solver.set_points(pts, offset)
+    zero_stats = np.zeros(n_local, dtype=abi.POINT_STATS_DTYPE)
+    l2 = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def one_step():
+        field.set_state(p0, m0, v0, s0)  # every step trains from the same initial field
+        solver.set_stats(zero_stats)
+        flush_l2(l2)
+        torch.cuda.synchronize()
+        _, ms = solver.run(SEED, WPP, TRAIN_UNTIL, tcfg)
+        return ms
+
+    for _ in range(args.warmup):
+        one_step()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.kernel_launches()
+    times, prof = [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            times.append(one_step())
+            prof.append(solver.run_profile())
+    launches = (_lib.kernel_launches() - launches0) // max(1, args.steps)
+    torch.cuda.synchronize()
+    step_ms = float(np.mean(times))
+    total_ms = float(np.sum(times))
+    if dist:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    walks_per_step = n_local * WPP * world
+    value = walks_per_step * args.steps / (total_ms * 1e-3)
+
+    # quality: relMSE of the last step against the analytic solution
+    st = solver.stats()
+    ref_img = np.array([preset.analytic(x, y) for x, y in pts])
+    rel_guided = relmse(st["mean"], ref_img)
+
+    # roofline of the dominant kernel (the walk kernel)
+    pr = prof[-1]
+    peaks, peak_kind = measured_peaks()
+    alg_bytes = pr["steps"] * BYTES_PER_STEP + pr["train_steps"] * BYTES_PER_TRAIN_STEP
+    achieved = alg_bytes / (pr["walk_ms"] * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "walk_kernel", "achieved": achieved,
+                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                "traffic": None, "peak_source": peak_kind,
+                "algorithmic_bytes_per_step": alg_bytes, "walk_ms_per_step": pr["walk_ms"],
+                "train_ms_per_step": pr["train_ms"], "walk_steps_per_step": pr["steps"]}
+
+    # e2e through the public API with host buffers (points in, statistics out)
+    e2e_times = []
+    h2d = pts.nbytes
+    d2h = n_local * abi.POINT_STATS_DTYPE.itemsize
+    for _ in range(max(1, min(2, args.steps))):
+        field.set_state(p0, m0, v0, s0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        solver.set_points(pts, offset)
+        solver.run(SEED, WPP, TRAIN_UNTIL, tcfg)
+        _ = solver.stats()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = float(np.mean(e2e_times))
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    # uniform WoSt at equal samples for the variance-reduction factor
+    usolver = api.Solver(api.Accel(preset.scene), None, abi.solver_config("uniform"))
+    usolver.set_points(pts, offset)
+    _, ums = usolver.run(SEED, WPP, 0, None)
+    rel_uniform = relmse(usolver.stats()["mean"], ref_img)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = cpu_reference_rate(args.ref_rounds, os.cpu_count() or 1)
+        if r:
+            cpu = {"value": r["value"], "unit": "walks/s", "cores": os.cpu_count(),
+                   "kind": r["kind"],
+                   "sample": f"{args.ref_rounds} of {WPP} wpp rounds of the same workload "
+                             f"({r['walks']} walks, {r['seconds']:.2f} s) via the reference's run_solve"}
+    if rank == 0:
+        line = {"metric": "guided WoSt walks/sec", "value": value, "unit": "walks/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"cfg2: {PRESET} {GRID}x{GRID * world} grid, {WPP} wpp, "
+                                       f"learnable_mis, online training every round",
+                           "preset": PRESET, "grid": [GRID, GRID * world], "wpp": WPP,
+                           "train_until": TRAIN_UNTIL, "mlp": args.mlp,
+                           "l2": "flushed (256 MiB write) before every step",
+                           "parallelism": f"dp{world} (points sharded, NCCL grad allreduce)"},
+                "e2e": {"value": walks_per_step / e2e_s, "unit": "walks/s",
+                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "gpu_launches": int(launches),
+                "roofline": roofline,
+                "cpu_baseline": cpu,
+                "clocks": clk.summary(),
+                "quality": {"relmse_guided": rel_guided, "relmse_uniform_equal_wpp": rel_uniform,
+                            "vr_factor": rel_uniform / rel_guided if rel_guided > 0 else None,
+                            "uniform_ms": ums, "escaped": pr["escaped"]}}
+        print(json.dumps(line))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

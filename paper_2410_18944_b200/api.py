@@ -1,0 +1,296 @@
+"""Python mirror of the reference's wost:: API for the guided WoSt hot path,
+running on the B200 through the C-ABI (include/wostgpu.h).
+
+Names, argument meaning and error behaviour follow the reference headers:
+  Accel          proj/include/wost/geom2d.hpp:38-91
+  GuidingField   proj/include/wost/guide_field.hpp:37-96
+  solve_batch    proj/include/wost/wost.hpp:160-163
+  train_batch    proj/include/wost/guide_train.hpp:104-105
+  Engine/run     proj/src/solver.cpp:53-167 (see harness.py)
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import abi
+from ._lib import check, init, load
+from .scene import Scene
+
+MLP_EXACT, MLP_TENSOR = 0, 1
+
+
+def _d(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _xy(xy):
+    return np.ascontiguousarray(np.asarray(xy, dtype=np.float64).reshape(-1, 2))
+
+
+class Accel:
+    """wost::Accel over a Scene: the device scene + BVH (geom2d.hpp:38)."""
+
+    def __init__(self, scene: Scene, device=None):
+        init(device)
+        self.scene = scene
+        h = C.c_void_p()
+        check(load().wostgpu_scene_create(*scene.c_args(), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            load().wostgpu_scene_destroy(self.h)
+            self.h = None
+
+    def _info(self):
+        t = C.c_double()
+        f = C.c_int32()
+        box = (C.c_double * 4)()
+        check(load().wostgpu_scene_info(self.h, C.byref(t), C.byref(f), box))
+        return t.value, bool(f.value), tuple(box)
+
+    @property
+    def t_epsilon(self):
+        return self._info()[0]
+
+    @property
+    def root_box(self):
+        return self._info()[2]
+
+    @property
+    def has_neumann_flux(self):
+        return self._info()[1]
+
+    def closest_point(self, xy, kinds=abi.KIND_ALL):
+        xy = _xy(xy)
+        n = len(xy)
+        pt = np.zeros((n, 2))
+        d = np.zeros(n)
+        seg = np.zeros(n, dtype=np.int32)
+        check(load().wostgpu_closest_point(self.h, n, _d(xy), kinds, _d(pt), _d(d),
+                                            seg.ctypes.data_as(C.POINTER(C.c_int32))))
+        return pt, d, seg
+
+    def closest_silhouette(self, xy):
+        xy = _xy(xy)
+        d = np.zeros(len(xy))
+        check(load().wostgpu_closest_silhouette(self.h, len(xy), _d(xy), _d(d)))
+        return d
+
+    def ray_first_hit(self, origin, direction, t_max, kinds=abi.KIND_ALL, exclude=None):
+        o = _xy(origin)
+        dr = _xy(direction)
+        n = len(o)
+        tm = np.ascontiguousarray(np.broadcast_to(np.asarray(t_max, dtype=np.float64), (n,)))
+        ex = None if exclude is None else np.ascontiguousarray(exclude, dtype=np.int32)
+        t = np.zeros(n)
+        pt = np.zeros((n, 2))
+        nrm = np.zeros((n, 2))
+        seg = np.zeros(n, dtype=np.int32)
+        kind = np.zeros(n, dtype=np.int32)
+        I = C.POINTER(C.c_int32)
+        check(load().wostgpu_ray_first_hit(
+            self.h, n, _d(o), _d(dr), _d(tm), kinds,
+            None if ex is None else ex.ctypes.data_as(I), _d(t), _d(pt), _d(nrm),
+            seg.ctypes.data_as(I), kind.ctypes.data_as(I)))
+        return t, pt, nrm, seg, kind
+
+    def star_radius(self, xy, r_min):
+        xy = _xy(xy)
+        r = np.zeros(len(xy))
+        check(load().wostgpu_star_radius(self.h, len(xy), _d(xy), r_min, _d(r)))
+        return r
+
+
+class GuidingField:
+    """wost::GuidingField (guide_field.hpp:37): grid + MLP on the device."""
+
+    def __init__(self, cfg: abi.FieldConfig, bbox, seed, device=None):
+        init(device)
+        self.cfg = cfg
+        self.bbox = tuple(bbox)
+        h = C.c_void_p()
+        check(load().wostgpu_field_create(C.byref(cfg), (C.c_double * 4)(*bbox), seed, C.byref(h)))
+        self.h = h
+        n = C.c_int64()
+        check(load().wostgpu_field_param_count(self.h, C.byref(n)))
+        self.n_params = n.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            load().wostgpu_field_destroy(self.h)
+            self.h = None
+
+    @property
+    def output_dim(self):
+        return (2 + self.cfg.mixture_dim) * self.cfg.mixture_k + 1
+
+    def params(self):
+        p = np.zeros(self.n_params, dtype=np.float32)
+        check(load().wostgpu_field_get_state(self.h, p.ctypes.data_as(C.POINTER(C.c_float)),
+                                              None, None, None))
+        return p
+
+    def state(self):
+        p = np.zeros(self.n_params, dtype=np.float32)
+        m = np.zeros(self.n_params)
+        v = np.zeros(self.n_params)
+        steps = C.c_int64()
+        check(load().wostgpu_field_get_state(self.h, p.ctypes.data_as(C.POINTER(C.c_float)),
+                                              _d(m), _d(v), C.byref(steps)))
+        return p, m, v, steps.value
+
+    def set_params(self, p):
+        p = np.ascontiguousarray(p, dtype=np.float32)
+        check(load().wostgpu_field_set_state(self.h, p.ctypes.data_as(C.POINTER(C.c_float)),
+                                              None, None, -1))
+
+    def set_state(self, p, m, v, steps):
+        p = np.ascontiguousarray(p, dtype=np.float32)
+        m = np.ascontiguousarray(m, dtype=np.float64)
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        check(load().wostgpu_field_set_state(self.h, p.ctypes.data_as(C.POINTER(C.c_float)),
+                                              _d(m), _d(v), steps))
+
+    def eval_batch(self, xy, mlp=MLP_EXACT):
+        xy = _xy(xy)
+        out = np.zeros((len(xy), self.output_dim))
+        check(load().wostgpu_field_eval_batch(self.h, len(xy), _d(xy), _d(out), mlp))
+        return out
+
+
+def normalize_params(raw, k, dim=2):
+    """normalize_params(unpack_params(raw)) on device (sphdist.cpp:287-310)."""
+    raw = np.ascontiguousarray(raw, dtype=np.float64)
+    out = np.zeros(raw.shape[0], dtype=abi.MIXTURE_DTYPE)
+    check(load().wostgpu_normalize_params(raw.shape[0], _d(raw), k, dim,
+                                           C.c_void_p(out.ctypes.data)))
+    return out
+
+
+class Solver:
+    """StepContext + SolveScratch + the Engine's record/training state
+    (wost.hpp:33-51, solver.cpp:53-105) resident on one GPU."""
+
+    def __init__(self, accel: Accel, field: GuidingField | None, cfg: abi.SolverConfig,
+                 mlp=MLP_EXACT):
+        self.accel, self.field, self.cfg = accel, field, cfg
+        h = C.c_void_p()
+        check(load().wostgpu_solver_create(accel.h, field.h if field else None, C.byref(cfg),
+                                            C.byref(h)))
+        self.h = h
+        self.n_points = 0
+        self.set_mlp(mlp)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            load().wostgpu_solver_destroy(self.h)
+            self.h = None
+
+    def set_mlp(self, mlp):
+        check(load().wostgpu_solver_set_mlp(self.h, mlp))
+
+    def set_points(self, xy, global_offset=0):
+        xy = _xy(xy)
+        self.n_points = len(xy)
+        check(load().wostgpu_solver_set_points(self.h, len(xy), _d(xy), global_offset))
+
+    def stats(self):
+        st = np.zeros(self.n_points, dtype=abi.POINT_STATS_DTYPE)
+        check(load().wostgpu_solver_get_stats(self.h, C.c_void_p(st.ctypes.data)))
+        return st
+
+    def set_stats(self, st):
+        st = np.ascontiguousarray(st, dtype=abi.POINT_STATS_DTYPE)
+        check(load().wostgpu_solver_set_stats(self.h, C.c_void_p(st.ctypes.data)))
+
+    def solve_rounds(self, seed, wpp_first, n_rounds, collect=False):
+        check(load().wostgpu_solve_rounds(self.h, seed, wpp_first, n_rounds, int(collect)))
+
+    def walks(self):
+        """estimate / escaped / steps of every point in the last round."""
+        n = self.n_points
+        est = np.zeros(n)
+        esc = np.zeros(n, dtype=np.int32)
+        steps = np.zeros(n, dtype=np.int32)
+        I = C.POINTER(C.c_int32)
+        check(load().wostgpu_fetch_walks(self.h, _d(est), esc.ctypes.data_as(I),
+                                          steps.ctypes.data_as(I)))
+        return est, esc, steps
+
+    def records(self):
+        n = C.c_int64()
+        check(load().wostgpu_fetch_records(self.h, None, 0, C.byref(n)))
+        out = np.zeros(n.value, dtype=abi.GUIDE_RECORD_DTYPE)
+        check(load().wostgpu_fetch_records(self.h, C.c_void_p(out.ctypes.data), n.value,
+                                            C.byref(n)))
+        return out[: n.value]
+
+    def counters(self):
+        v = [C.c_int64() for _ in range(4)]
+        check(load().wostgpu_solver_counters(self.h, *[C.byref(x) for x in v]))
+        return dict(zip(("walks", "steps", "escaped", "records"), (x.value for x in v)))
+
+    def timing(self):
+        w, t = C.c_double(), C.c_double()
+        check(load().wostgpu_solver_timing(self.h, C.byref(w), C.byref(t)))
+        return w.value, t.value
+
+    def train_round(self, cfg: abi.TrainConfig, rnd):
+        st = abi.TrainStats()
+        check(load().wostgpu_train_round(self.h, C.byref(cfg), rnd, C.byref(st)))
+        return st
+
+    def train_batch(self, records, cfg: abi.TrainConfig, rnd):
+        recs = np.ascontiguousarray(records, dtype=abi.GUIDE_RECORD_DTYPE)
+        st = abi.TrainStats()
+        check(load().wostgpu_train_batch(self.h, C.c_void_p(recs.ctypes.data), len(recs),
+                                          C.byref(cfg), rnd, C.byref(st)))
+        return st
+
+    def field_grad(self, records, cfg: abi.TrainConfig):
+        recs = np.ascontiguousarray(records, dtype=abi.GUIDE_RECORD_DTYPE)
+        g = np.zeros(self.field.n_params)
+        check(load().wostgpu_field_grad(self.h, C.c_void_p(recs.ctypes.data), len(recs),
+                                         C.byref(cfg), _d(g)))
+        return g
+
+    def run(self, seed, wpp, train_until=256, train_cfg: abi.TrainConfig | None = None):
+        """Engine loop natively (wostgpu_run): returns (TrainStats, device ms)."""
+        st = abi.TrainStats()
+        ms = C.c_double()
+        check(load().wostgpu_run(self.h, seed, wpp, train_until,
+                                  C.byref(train_cfg) if train_cfg is not None else None,
+                                  C.byref(st), C.byref(ms)))
+        return st, ms.value
+
+    def run_profile(self):
+        w, t = C.c_double(), C.c_double()
+        v = [C.c_int64() for _ in range(4)]
+        check(load().wostgpu_run_profile(self.h, C.byref(w), C.byref(t), *[C.byref(x) for x in v]))
+        out = dict(zip(("walks", "steps", "escaped", "train_steps"), (x.value for x in v)))
+        out["walk_ms"], out["train_ms"] = w.value, t.value
+        return out
+
+    def attach_comm(self, unique_id: bytes, nranks, rank):
+        check(load().wostgpu_solver_attach_comm(self.h, unique_id, nranks, rank))
+
+
+def comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(load().wostgpu_comm_unique_id(buf))
+    return buf.raw
+
+
+def solve_batch(solver: Solver, points, stats, seed, wpp_index, collect_records=False):
+    """Drop-in solve_batch (wost.hpp:160-163): updates `stats` in place and
+    returns the round's records when collect_records."""
+    xy = _xy(points)
+    st = np.ascontiguousarray(stats, dtype=abi.POINT_STATS_DTYPE)
+    check(load().wostgpu_solve_batch(solver.h, len(xy), _d(xy), C.c_void_p(st.ctypes.data), seed,
+                                      wpp_index, int(collect_records)))
+    solver.n_points = len(xy)
+    stats[...] = st
+    return solver.records() if collect_records else None

@@ -1,0 +1,90 @@
+// Kernel argument blocks and launch wrappers shared by the kernel TUs and the
+// host runtime (wg_runtime.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "wg_device.cuh"
+#include "wg_field.cuh"
+
+namespace wg {
+
+// Guide record as kept in HBM during a collecting round (80 B). One per walk
+// step, appended by the walk kernel, completed by the walk's own backfill at
+// termination (backfill_targets_append, proj/src/guide_train.cpp:58-79).
+struct __align__(16) DevRecord {
+  float x, y;
+  float nux, nuy;
+  float nx, ny;
+  float pdf_mis, pdf_g, pdf_u, c;
+  float target;  // |u(x_{k+1})| after backfill
+  float local;   // <N> - <S> of this step (own throughput frame)
+  float mult;    // p_u / p_mis
+  float rr;      // roulette reweight
+  int32_t prev;  // previous record of the same walk, -1 for the first
+  uint32_t flags;
+  uint64_t key;  // deterministic selection key (seed, round, point, depth)
+};
+static_assert(sizeof(DevRecord) == 80, "record layout");
+enum : uint32_t { REC_ON_NEUMANN = 1u, REC_VALID = 2u };
+
+struct SolverParams {
+  double eps, rmin, fixed_c, grazing_floor;
+  int32_t rr_depth, max_steps, mode, reflect, clamp_grazing;
+};
+
+struct WalkArgs {
+  SceneView scene;         // global-memory view
+  int32_t scene_smem_bytes;  // > 0: stage nodes/segs/silhouettes in smem
+  FieldView field;
+  SolverParams sp;
+  const double* points;  // [n_points][2]
+  int64_t n_points;
+  int64_t point_offset;  // global index of points[0]
+  uint64_t seed;
+  uint64_t wpp_first;
+  int32_t n_rounds;
+  double* est;      // [n_rounds][n_points]
+  int32_t* esc;     // [n_rounds][n_points]
+  int32_t* steps;   // [n_rounds][n_points] (may be null)
+  // records (collecting rounds)
+  DevRecord* recs;
+  unsigned long long* rec_counter;
+  int64_t rec_capacity;
+  uint64_t key_seed;
+  // counters: [0] steps, [1] escaped, [2] walks, [3] record overflow, [4] scene error
+  unsigned long long* counters;
+};
+
+struct QueryArgs {
+  SceneView scene;
+  int64_t n;
+  int32_t op;  // 0 closest_point, 1 silhouette, 2 ray, 3 star radius
+  uint32_t kinds;
+  double r_min;
+  const double* xy;
+  const double* dir;
+  const double* t_max;
+  const int32_t* exclude;
+  double* out_d;     // dist / t / r
+  double* out_pt;    // [n][2]
+  double* out_n;     // [n][2]
+  int32_t* out_seg;
+  int32_t* out_kind;
+  unsigned long long* err;
+};
+
+// launchers (defined in wg_walk.cu)
+cudaError_t launch_queries(const QueryArgs& a, cudaStream_t st);
+cudaError_t launch_walks(const WalkArgs& a, bool guided_exact_default, bool guided_generic,
+                         int blocks, cudaStream_t st);
+int walk_blocks_per_sm(bool guided_exact_default, bool guided_generic, int smem_bytes);
+cudaError_t launch_welford(const double* est, const int32_t* esc, int64_t n_points,
+                           int32_t n_rounds, wg_point_stats* stats, cudaStream_t st);
+cudaError_t launch_field_eval(const FieldView& f, int64_t n, const double* xy, double* out,
+                              cudaStream_t st);
+cudaError_t launch_normalize(int64_t n, const double* raw, int k, int dim, wg_mixture* out,
+                             cudaStream_t st);
+
+}  // namespace wg

@@ -1,0 +1,460 @@
+// Online training of the guiding field on device (proj/src/guide_train.cpp).
+//
+//   select_kernel  filter pdf_mis < floor; a deterministic 64-bit key per
+//                  record (hash of seed, round, point, depth) sorted with a
+//                  radix sort gives a uniformly random order: its first
+//                  min(n, cap) records are the round's training set, cut into
+//                  minibatches exactly like train_batch (guide_train.cpp:101-130)
+//   grad kernel    one CTA per 128-record tile: gather + MLP forward, per-record
+//                  KL / selection gradient (Eq. 13 / 16) in fp64, backward, and
+//                  the tile's weight gradients reduced in shared memory; grid
+//                  corners receive their share by atomics (wg_train_tc.cu holds
+//                  the tcgen05 version of the three GEMMs)
+//   adam_kernel    bias-corrected Adam with fp64 moments (guide_field.cpp:317-331)
+#include <cub/cub.cuh>
+
+#include "wg_kernels.cuh"
+#include "wg_sphdist.cuh"
+#include "wg_train.cuh"
+
+namespace wg {
+
+// ---------------------------------------------------------------- selection
+__global__ void select_keys_kernel(const DevRecord* recs, int64_t n, double pdf_floor,
+                                   uint64_t* keys, uint32_t* idx, unsigned long long* cnt) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint64_t key = ~0ull;
+  int usable = 0, low = 0;
+  if (i < n) {
+    const DevRecord r = recs[i];
+    if (r.flags & REC_VALID) {
+      if (static_cast<double>(r.pdf_mis) < pdf_floor) low = 1;
+      else {
+        usable = 1;
+        key = r.key;
+      }
+    }
+    keys[i] = key;
+    idx[i] = static_cast<uint32_t>(i);
+  }
+  // warp-aggregated counters: [0] valid records seen, [1] usable, [2] low pdf
+  unsigned seen = __popc(__ballot_sync(0xffffffffu, usable || low));
+  unsigned us = __popc(__ballot_sync(0xffffffffu, usable));
+  unsigned lo = __popc(__ballot_sync(0xffffffffu, low));
+  if ((threadIdx.x & 31) == 0) {
+    if (seen) atomicAdd(&cnt[0], seen);
+    if (us) atomicAdd(&cnt[1], us);
+    if (lo) atomicAdd(&cnt[2], lo);
+  }
+}
+
+size_t sort_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, static_cast<const uint64_t*>(nullptr),
+                                  static_cast<uint64_t*>(nullptr),
+                                  static_cast<const uint32_t*>(nullptr),
+                                  static_cast<uint32_t*>(nullptr), static_cast<int>(n));
+  return bytes;
+}
+
+cudaError_t launch_select(const DevRecord* recs, int64_t n, double pdf_floor, uint64_t* keys,
+                          uint64_t* keys_sorted, uint32_t* idx, uint32_t* idx_sorted, void* temp,
+                          size_t temp_bytes, unsigned long long* cnt, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  select_keys_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(recs, n, pdf_floor, keys,
+                                                                        idx, cnt);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys_sorted, idx, idx_sorted,
+                                         static_cast<int>(n), 0, 64, st);
+}
+
+// ---------------------------------------------------------------- loss grad
+// dV/dTheta' of one direction (sphdist.cpp:324-366); accumulates into g
+template <int K>
+WG_D double mix_grad_one(const Mix& m, const float* raw, double nx, double ny, double* g) {
+  double v[K];
+  double val = 0.0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    double dt = nx * m.mux[i] + ny * m.muy[i] + 0.0 * 0.0;
+    v[i] = exp(m.kappa[i] * dt + m.log_a[i]);
+    val += m.lambda[i] * v[i];
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i) g[3 * K + i] += m.lambda[i] * (v[i] - val);
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    double t = nx * m.mux[i] + ny * m.muy[i] + 0.0 * 0.0;
+    double lv = m.lambda[i] * v[i];
+    double ku = exp(static_cast<double>(raw[2 * K + i]));
+    if (ku > kKappaMin && ku < kKappaMax)
+      g[2 * K + i] += lv * (t - bessel_i1_over_i0(m.kappa[i])) * m.kappa[i];
+    double mx = raw[2 * i], my = raw[2 * i + 1];
+    double mn = sqrt(mx * mx + my * my + 0.0 * 0.0);
+    if (mn >= 1e-12) {
+      double s = lv * m.kappa[i] / mn;
+      g[2 * i] += (nx - m.mux[i] * t) * s;
+      g[2 * i + 1] += (ny - m.muy[i] * t) * s;
+    }
+  }
+  return val;
+}
+
+// kl_grad (guide_train.cpp:25-42) + selection_grad (:44-56) for one record;
+// writes dL/d(raw output) scaled by inv_count into dy. Returns false when the
+// record is skipped (V below the floor).
+template <int K>
+WG_D bool record_dy(const float* raw, const DevRecord& r, const TrainArgs& a, float* dy) {
+  constexpr int OD = 4 * K + 1;
+  double g[OD];
+#pragma unroll
+  for (int j = 0; j < OD; ++j) g[j] = 0.0;
+  Mix m;
+  normalize2<K>(raw, K, m);
+  const bool on_n = (r.flags & REC_ON_NEUMANN) != 0;
+  const double nx = r.nux, ny = r.nuy, px = r.nx, py = r.ny;
+  const double target = r.target;
+  if (target != 0.0) {
+    double dv[OD];
+#pragma unroll
+    for (int j = 0; j < OD; ++j) dv[j] = 0.0;
+    double v = mix_grad_one<K>(m, raw, nx, ny, dv);
+    if (on_n && a.reflect) {
+      double rx, ry;
+      reflect(nx, ny, px, py, &rx, &ry);
+      v += mix_grad_one<K>(m, raw, rx, ry, dv);
+    }
+    if (!(v > a.v_floor)) return false;
+    double s = -target / (static_cast<double>(r.pdf_mis) * v);
+#pragma unroll
+    for (int j = 0; j < OD - 1; ++j) g[j] = s * dv[j];
+  }
+  if (a.learn_selection) {
+    double pg = on_n ? (a.reflect ? reflected_pdf(m, nx, ny, px, py) : mixture_pdf(m, nx, ny))
+                     : mixture_pdf(m, nx, ny);
+    double pu = r.pdf_u;
+    double pnow = m.c * pg + (1.0 - m.c) * pu;
+    if (pnow > 0.0) {
+      double dc = -a.e_fraction * target * (pg - pu) / (pnow * static_cast<double>(r.pdf_mis));
+      g[OD - 1] = dc * m.c * (1.0 - m.c);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < OD; ++j) dy[j] = static_cast<float>(g[j] * a.inv_count);
+  return true;
+}
+
+// ---------------------------------------------------------------- tile kernel
+// CUDA-core tile: 128 records per CTA, thread = record. Activations and the
+// backward signals live in padded shared-memory tiles (row stride +1 float)
+// so row-per-thread writes and column-per-thread reads are conflict-free.
+namespace {
+constexpr int TB = 128;
+constexpr int IN = 16, HID = 64, K8 = 8, OD = 33;
+constexpr int SX = IN + 1, SH = HID + 1, SY = OD + 1;
+constexpr int MLPN = IN * HID + HID + HID * HID + HID + HID * OD + OD;  // 7393
+constexpr size_t TILE_SMEM =
+    sizeof(float) * (MLPN + TB * SX + 4 * TB * SH + TB * SY);
+}  // namespace
+
+__global__ void __launch_bounds__(TB) grad_tile_kernel(TrainArgs a) {
+  extern __shared__ __align__(16) float sm[];
+  float* W = sm;                    // MLP block, params layout
+  float* X = W + MLPN;              // [TB][SX]
+  float* H1 = X + TB * SX;          // [TB][SH] post-ReLU
+  float* H2 = H1 + TB * SH;
+  float* D2 = H2 + TB * SH;         // dL/dh2pre
+  float* D1 = D2 + TB * SH;         // dL/dh1pre
+  float* DY = D1 + TB * SH;         // [TB][SY]
+  const FieldView& f = a.f;
+  for (int i = threadIdx.x; i < MLPN; i += TB) W[i] = f.p[f.w1 + i];
+  const float* W1 = W;
+  const float* B1 = W1 + IN * HID;
+  const float* W2 = B1 + HID;
+  const float* B2 = W2 + HID * HID;
+  const float* W3 = B2 + HID;
+  const float* B3 = W3 + HID * OD;
+  __syncthreads();
+
+  const int t = threadIdx.x;
+  const int64_t ri = static_cast<int64_t>(blockIdx.x) * TB + t;
+  const bool live = ri < a.count;
+  DevRecord r{};
+  if (live) r = a.recs[a.order[a.begin + ri]];
+
+  // gather (fp32, guide_field.cpp:80-123) keeping corner indices/weights
+  float x[IN];
+  int cidx[4 * 4];
+  float cw[4 * 4];
+  {
+    double ex = f.bbox[2] - f.bbox[0], ey = f.bbox[3] - f.bbox[1];
+    float u = static_cast<float>(sclamp((static_cast<double>(r.x) - f.bbox[0]) / ex, 0.0, 1.0));
+    float v = static_cast<float>(sclamp((static_cast<double>(r.y) - f.bbox[1]) / ey, 0.0, 1.0));
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      int res = f.res[l];
+      float px = u * static_cast<float>(res - 1), py = v * static_cast<float>(res - 1);
+      int ix = imin(static_cast<int>(px), res - 2), iy = imin(static_cast<int>(py), res - 2);
+      float fx = px - ix, fy = py - iy;
+      int c00 = f.lvl_off[l] + (iy * res + ix) * 4;
+      int c10 = c00 + 4, c01 = c00 + res * 4, c11 = c01 + 4;
+      float w00 = (1.0f - fx) * (1.0f - fy), w10 = fx * (1.0f - fy);
+      float w01 = (1.0f - fx) * fy, w11 = fx * fy;
+      cidx[4 * l] = c00;
+      cidx[4 * l + 1] = c10;
+      cidx[4 * l + 2] = c01;
+      cidx[4 * l + 3] = c11;
+      cw[4 * l] = w00;
+      cw[4 * l + 1] = w10;
+      cw[4 * l + 2] = w01;
+      cw[4 * l + 3] = w11;
+      float4 e00 = __ldg(reinterpret_cast<const float4*>(f.p + c00));
+      float4 e10 = __ldg(reinterpret_cast<const float4*>(f.p + c10));
+      float4 e01 = __ldg(reinterpret_cast<const float4*>(f.p + c01));
+      float4 e11 = __ldg(reinterpret_cast<const float4*>(f.p + c11));
+      x[4 * l + 0] = w00 * e00.x + w10 * e10.x + w01 * e01.x + w11 * e11.x;
+      x[4 * l + 1] = w00 * e00.y + w10 * e10.y + w01 * e01.y + w11 * e11.y;
+      x[4 * l + 2] = w00 * e00.z + w10 * e10.z + w01 * e01.z + w11 * e11.z;
+      x[4 * l + 3] = w00 * e00.w + w10 * e10.w + w01 * e01.w + w11 * e11.w;
+    }
+  }
+  // forward; activations go straight to the thread's smem row
+  float* xr = X + t * SX;
+  float* h1r = H1 + t * SH;
+  float* h2r = H2 + t * SH;
+#pragma unroll
+  for (int i = 0; i < IN; ++i) xr[i] = x[i];
+  float y[OD];
+  {
+    float h[HID];
+#pragma unroll
+    for (int j = 0; j < HID; ++j) {
+      float acc = B1[j];
+#pragma unroll
+      for (int i = 0; i < IN; ++i) acc = fmaf(x[i], W1[i * HID + j], acc);
+      h[j] = acc > 0.0f ? acc : 0.0f;
+      h1r[j] = h[j];
+    }
+#pragma unroll 4
+    for (int j = 0; j < HID; ++j) {
+      float acc = B2[j];
+#pragma unroll
+      for (int i = 0; i < HID; ++i) acc = fmaf(h[i], W2[i * HID + j], acc);
+      h2r[j] = acc > 0.0f ? acc : 0.0f;
+    }
+#pragma unroll
+    for (int i = 0; i < HID; ++i) h[i] = h2r[i];
+#pragma unroll
+    for (int j = 0; j < OD; ++j) {
+      float acc = B3[j];
+#pragma unroll
+      for (int i = 0; i < HID; ++i) acc = fmaf(h[i], W3[i * OD + j], acc);
+      y[j] = acc;
+    }
+  }
+  // loss gradient at the raw outputs
+  float dy[OD];
+  bool used = false;
+  if (live) used = record_dy<K8>(y, r, a, dy);
+  if (!used) {
+#pragma unroll
+    for (int j = 0; j < OD; ++j) dy[j] = 0.0f;
+  }
+  {
+    unsigned c = __popc(__ballot_sync(0xffffffffu, used));
+    unsigned sk = __popc(__ballot_sync(0xffffffffu, live && !used));
+    if ((t & 31) == 0) {
+      if (c) atomicAdd(&a.counters[0], c);
+      if (sk) atomicAdd(&a.counters[1], sk);
+    }
+  }
+  // backward through the layers (guide_field.cpp:258-303), row in smem
+  float* d2r = D2 + t * SH;
+  float* d1r = D1 + t * SH;
+  float* dyr = DY + t * SY;
+#pragma unroll
+  for (int j = 0; j < OD; ++j) dyr[j] = dy[j];
+#pragma unroll 4
+  for (int i = 0; i < HID; ++i) {
+    float acc = 0.0f;
+#pragma unroll
+    for (int j = 0; j < OD; ++j) acc = fmaf(W3[i * OD + j], dy[j], acc);
+    d2r[i] = h2r[i] > 0.0f ? acc : 0.0f;
+  }
+  float dx[IN];
+  {
+    float dv[HID];
+#pragma unroll
+    for (int j = 0; j < HID; ++j) dv[j] = d2r[j];
+#pragma unroll 4
+    for (int i = 0; i < HID; ++i) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int j = 0; j < HID; ++j) acc = fmaf(W2[i * HID + j], dv[j], acc);
+      d1r[i] = h1r[i] > 0.0f ? acc : 0.0f;
+    }
+#pragma unroll
+    for (int j = 0; j < HID; ++j) dv[j] = d1r[j];
+#pragma unroll
+    for (int i = 0; i < IN; ++i) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int j = 0; j < HID; ++j) acc = fmaf(W1[i * HID + j], dv[j], acc);
+      dx[i] = acc;
+    }
+  }
+  // grid corners (guide_field.cpp:305-314)
+  if (used) {
+#pragma unroll
+    for (int l = 0; l < 4; ++l)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) atomicAdd(a.grad + cidx[4 * l + c] + q, cw[4 * l + c] * dx[4 * l + q]);
+  }
+  __syncthreads();
+  // dW3 = H2^T DY, dW2 = H1^T D2, dW1 = X^T D1, biases = column sums
+  const int gw1 = f.w1, gb1 = f.b1, gw2 = f.w2, gb2 = f.b2, gw3 = f.w3, gb3 = f.b3;
+  for (int e = t; e < HID * OD; e += TB) {
+    int i = e / OD, j = e % OD;
+    float acc = 0.0f;
+    for (int q = 0; q < TB; ++q) acc = fmaf(H2[q * SH + i], DY[q * SY + j], acc);
+    atomicAdd(a.grad + gw3 + e, acc);
+  }
+  for (int e = t; e < HID * HID; e += TB) {
+    int i = e / HID, j = e % HID;
+    float acc = 0.0f;
+    for (int q = 0; q < TB; ++q) acc = fmaf(H1[q * SH + i], D2[q * SH + j], acc);
+    atomicAdd(a.grad + gw2 + e, acc);
+  }
+  for (int e = t; e < IN * HID; e += TB) {
+    int i = e / HID, j = e % HID;
+    float acc = 0.0f;
+    for (int q = 0; q < TB; ++q) acc = fmaf(X[q * SX + i], D1[q * SH + j], acc);
+    atomicAdd(a.grad + gw1 + e, acc);
+  }
+  if (t < OD) {
+    float acc = 0.0f;
+    for (int q = 0; q < TB; ++q) acc += DY[q * SY + t];
+    atomicAdd(a.grad + gb3 + t, acc);
+  }
+  if (t < HID) {
+    float a1 = 0.0f, a2 = 0.0f;
+    for (int q = 0; q < TB; ++q) {
+      a1 += D1[q * SH + t];
+      a2 += D2[q * SH + t];
+    }
+    atomicAdd(a.grad + gb1 + t, a1);
+    atomicAdd(a.grad + gb2 + t, a2);
+  }
+}
+
+size_t grad_tile_smem() { return TILE_SMEM; }
+
+cudaError_t launch_grad_cuda_core(const TrainArgs& a, cudaStream_t st) {
+  if (a.count == 0) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(grad_tile_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(TILE_SMEM));
+  if (e != cudaSuccess) return e;
+  int blocks = static_cast<int>((a.count + TB - 1) / TB);
+  grad_tile_kernel<<<blocks, TB, TILE_SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- Adam
+// guide_field.cpp:317-331; also accumulates |g|^2 for TrainStats
+__global__ void adam_kernel(float* p, double* m, double* v, float* g, int64_t n, double lr,
+                            double b1, double b2, double eps, double bc1, double bc2,
+                            const float* count, double* norm2) {
+  // gradient sums arrive with their record count in g[n] (summed over ranks)
+  const double scale = count ? 1.0 / static_cast<double>(*count) : 1.0;
+  double local = 0.0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double gi = static_cast<double>(g[i]) * scale;
+    local += gi * gi;
+    double mi = m[i] = b1 * m[i] + (1.0 - b1) * gi;
+    double vi = v[i] = b2 * v[i] + (1.0 - b2) * gi * gi;
+    double up = lr * (mi / bc1) / (sqrt(vi / bc2) + eps);
+    p[i] = static_cast<float>(static_cast<double>(p[i]) - up);
+    g[i] = 0.0f;
+  }
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(norm2, local);
+}
+
+cudaError_t launch_adam(float* p, double* m, double* v, float* g, int64_t n, double lr, double b1,
+                        double b2, double eps, int64_t step, const float* count, double* norm2,
+                        cudaStream_t st) {
+  double bc1 = 1.0 - pow(b1, static_cast<double>(step));
+  double bc2 = 1.0 - pow(b2, static_cast<double>(step));
+  int blocks = static_cast<int>((n + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  adam_kernel<<<blocks, 256, 0, st>>>(p, m, v, g, n, lr, b1, b2, eps, bc1, bc2, count, norm2);
+  return cudaGetLastError();
+}
+
+// host records (wg_guide_record, fp64) -> device records
+__global__ void import_records_kernel(const wg_guide_record* in, int64_t n, DevRecord* out) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const wg_guide_record g = in[i];
+  DevRecord r{};
+  r.x = static_cast<float>(g.x[0]);
+  r.y = static_cast<float>(g.x[1]);
+  r.nux = static_cast<float>(g.nu[0]);
+  r.nuy = static_cast<float>(g.nu[1]);
+  r.nx = static_cast<float>(g.normal[0]);
+  r.ny = static_cast<float>(g.normal[1]);
+  r.pdf_mis = static_cast<float>(g.pdf_mis);
+  r.pdf_g = static_cast<float>(g.pdf_g);
+  r.pdf_u = static_cast<float>(g.pdf_u);
+  r.c = static_cast<float>(g.c);
+  r.target = static_cast<float>(g.target);
+  r.flags = REC_VALID | (g.on_neumann ? REC_ON_NEUMANN : 0u);
+  r.prev = -1;
+  r.key = static_cast<uint64_t>(i);
+  out[i] = r;
+}
+
+__global__ void export_records_kernel(const DevRecord* in, int64_t n, wg_guide_record* out,
+                                      unsigned long long* count) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const DevRecord r = in[i];
+  if (!(r.flags & REC_VALID)) return;
+  unsigned long long o = atomicAdd(count, 1ull);
+  wg_guide_record g{};
+  g.x[0] = r.x;
+  g.x[1] = r.y;
+  g.nu[0] = r.nux;
+  g.nu[1] = r.nuy;
+  g.nu[2] = 0.0;
+  g.target = r.target;
+  g.pdf_mis = r.pdf_mis;
+  g.pdf_g = r.pdf_g;
+  g.pdf_u = r.pdf_u;
+  g.c = r.c;
+  g.on_neumann = (r.flags & REC_ON_NEUMANN) ? 1 : 0;
+  g.normal[0] = r.nx;
+  g.normal[1] = r.ny;
+  out[o] = g;
+}
+
+cudaError_t launch_import_records(const wg_guide_record* in, int64_t n, DevRecord* out,
+                                  cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  import_records_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(in, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_export_records(const DevRecord* in, int64_t n, wg_guide_record* out,
+                                  unsigned long long* count, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  export_records_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(in, n, out, count);
+  return cudaGetLastError();
+}
+
+}  // namespace wg

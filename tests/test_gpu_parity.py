@@ -1,0 +1,250 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the
+same inputs. Geometry, field evaluation, normalisation and per-walk estimates
+are compared bit for bit or with the tolerance stated in each test."""
+import numpy as np
+import pytest
+
+from fixtures import Rng, probes, random_scene, segments_scene
+from paper_2410_18944_b200 import abi, api
+from paper_2410_18944_b200.scene import PRESET_NAMES, cell_centers, make_preset
+
+pytestmark = pytest.mark.gpu
+
+
+def _both(orc, scene):
+    return orc.scene(scene), api.Accel(scene)
+
+
+# ---------------------------------------------------------------- geometry
+@pytest.mark.parametrize("seed,n,mixed", [((101, 0), 1000, True), ((77, 3), 10000, False),
+                                          ((55, 1), 500, True)])
+def test_closest_point_bit_exact(gpu, orc, seed, n, mixed):
+    rng = Rng(*seed)
+    sc = random_scene(rng, n, mixed)
+    ho, acc = _both(orc, sc)
+    xy = probes(Rng(seed[0] + 1000, 0), 4000, -0.2, 1.2)
+    for kinds in (abi.KIND_ALL, abi.KIND_DIRICHLET, abi.KIND_NEUMANN):
+        po, do, so = orc.closest_point(ho, xy, kinds)
+        pg, dg, sg = acc.closest_point(xy, kinds)
+        assert np.array_equal(so, sg)  # segment index bit-exact
+        assert np.array_equal(do, dg)  # distance bit-exact (fp64, same op order)
+        m = so >= 0
+        assert np.array_equal(po[m], pg[m])
+
+
+def test_silhouette_and_star_radius_bit_exact(gpu, orc):
+    sc = random_scene(Rng(55, 1), 500)
+    ho, acc = _both(orc, sc)
+    xy = probes(Rng(9, 9), 4000, 0.0, 1.0)
+    assert np.array_equal(orc.closest_silhouette(ho, xy), acc.closest_silhouette(xy))
+    assert np.array_equal(orc.star_radius(ho, xy, 1e-3), acc.star_radius(xy, 1e-3))
+
+
+@pytest.mark.parametrize("kinds", [abi.KIND_ALL, abi.KIND_DIRICHLET, abi.KIND_NEUMANN])
+def test_ray_first_hit_bit_exact(gpu, orc, kinds):
+    sc = random_scene(Rng(13, 8), 1000)
+    ho, acc = _both(orc, sc)
+    rng = Rng(14, 0)
+    o = probes(rng, 4000, 0.0, 1.0)
+    ang = np.array([rng.uniform(0.0, 2 * np.pi) for _ in range(4000)])
+    d = np.stack([np.cos(ang), np.sin(ang)], 1)
+    ex = np.where(np.arange(4000) % 3 == 0, 7, -1).astype(np.int32)
+    a = orc.ray_first_hit(ho, o, d, 2.0, kinds, ex)
+    b = acc.ray_first_hit(o, d, 2.0, kinds, ex)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+def test_axis_parallel_rays_and_misses(gpu, orc):
+    sc = segments_scene([((0.0, 1.0), (1.0, 1.0), abi.DIRICHLET)], (-1, -1, 2, 2))
+    ho, acc = _both(orc, sc)
+    o = np.array([[0.5, 0.0], [0.0, 0.0], [0.5, 0.0]])
+    d = np.array([[0.0, 1.0], [1.0, 0.0], [0.0, 1.0]])
+    tm = np.array([10.0, 10.0, 0.5])
+    t, pt, n, seg, kind = acc.ray_first_hit(o, d, tm, abi.KIND_ALL)
+    assert t[0] == 1.0 and seg[0] == 0 and np.dot(n[0], d[0]) <= 0
+    assert seg[1] == -1 and np.isinf(t[1])  # parallel
+    assert seg[2] == -1  # beyond t_max
+    a = orc.ray_first_hit(ho, o, d, tm, abi.KIND_ALL)
+    assert all(np.array_equal(x, y) for x, y in zip(a, (t, pt, n, seg, kind)))
+
+
+def test_unbounded_star_raises_scene_error(gpu):
+    from paper_2410_18944_b200._lib import SceneError
+    sc = segments_scene([((0, 0), (1, 0), abi.NEUMANN), ((1, 0), (1, 1), abi.NEUMANN),
+                         ((1, 1), (0, 1), abi.NEUMANN), ((0, 1), (0, 0), abi.NEUMANN)],
+                        (0, 0, 1, 1))
+    acc = api.Accel(sc)
+    with pytest.raises(SceneError):
+        acc.star_radius(np.array([[0.5, 0.5]]), 0.01)
+
+
+@pytest.mark.parametrize("name", PRESET_NAMES)
+def test_presets_geometry_bit_exact(gpu, orc, name):
+    p = make_preset(name)
+    ho, acc = _both(orc, p.scene)
+    xy = cell_centers(64, 64, p.eval_bbox)
+    for kinds in (abi.KIND_ALL, abi.KIND_DIRICHLET):
+        a = orc.closest_point(ho, xy, kinds)
+        b = acc.closest_point(xy, kinds)
+        assert all(np.array_equal(x, y) for x, y in zip(a, b))
+    assert acc.t_epsilon == orc.fn("t_epsilon")(ho)
+
+
+# ---------------------------------------------------------------- field
+@pytest.mark.parametrize("cfg", [abi.field_config(),
+                                 abi.field_config((9, 17), features=2, hidden=16, mixture_k=4)])
+def test_field_init_and_exact_eval_bit_exact(gpu, orc, cfg):
+    bbox = (0.0, 0.0, 1.0, 1.0)
+    fo = orc.field(cfg, bbox, 1234)
+    fg = api.GuidingField(cfg, bbox, 1234)
+    assert np.array_equal(orc.field_params(fo), fg.params())
+    xy = probes(Rng(22, 0), 5000, -0.2, 1.2)
+    od = fg.output_dim
+    assert np.array_equal(orc.field_eval(fo, xy, od), fg.eval_batch(xy, api.MLP_EXACT))
+
+
+def test_normalize_params_matches_oracle(gpu, orc):
+    rng = np.random.default_rng(3)
+    raw = rng.normal(0, 1.5, (4000, 33))
+    raw[:10, 0:2] = 0.0  # zero-norm mean -> fallback direction
+    a = orc.normalize(raw, 8)
+    b = api.normalize_params(raw, 8)
+    for k in ("mu", "kappa", "lambda", "log_a", "c"):
+        np.testing.assert_allclose(b[k], a[k], rtol=1e-14, atol=1e-300)
+
+
+# ---------------------------------------------------------------- walks
+def _walk_parity(orc, scene, field_o, field_g, mode, xy, seed=1, wpp=0):
+    cfg = abi.solver_config(mode)
+    ho = orc.scene(scene)
+    est_o, esc_o, _ = orc.walks(ho, field_o, cfg, xy, seed, wpp)
+    acc = api.Accel(scene)
+    sol = api.Solver(acc, field_g, cfg, api.MLP_EXACT)
+    sol.set_points(xy)
+    sol.solve_rounds(seed, wpp, 1)
+    est_g, esc_g, steps = sol.walks()
+    return est_o, esc_o, est_g, esc_g
+
+
+@pytest.mark.parametrize("name", PRESET_NAMES)
+def test_uniform_walks_match_oracle_per_walk(gpu, orc, name):
+    """Same PCG32 stream per walk, fp64 everywhere: per-walk estimates agree to
+    1e-9 (ulp-level libm differences only) for >= 99.9% of walks."""
+    p = make_preset(name)
+    xy = cell_centers(64, 64, p.eval_bbox)
+    est_o, esc_o, est_g, esc_g = _walk_parity(orc, p.scene, None, None, "uniform", xy)
+    close = np.abs(est_o - est_g) <= 1e-9 * np.maximum(1.0, np.abs(est_o))
+    assert close.mean() >= 0.999, close.mean()
+    assert (esc_o == esc_g).mean() >= 0.999
+
+
+@pytest.mark.parametrize("mode", ["guiding_only", "fixed_mis", "learnable_mis"])
+def test_guided_walks_exact_mlp_match_oracle(gpu, orc, mode):
+    p = make_preset("curves")
+    cfg = abi.field_config()
+    fo = orc.field(cfg, p.scene.bbox, 31)
+    fg = api.GuidingField(cfg, p.scene.bbox, 31)
+    xy = cell_centers(48, 48, p.eval_bbox)
+    est_o, esc_o, est_g, esc_g = _walk_parity(orc, p.scene, fo, fg, mode, xy, seed=99)
+    close = np.abs(est_o - est_g) <= 1e-9 * np.maximum(1.0, np.abs(est_o))
+    assert close.mean() >= 0.99, close.mean()
+
+
+def test_multi_round_welford_matches_sequential_solve_batch(gpu, orc):
+    """wpp rounds run in one launch; Welford order equals sequential solve_batch."""
+    p = make_preset("neumann-strip-vlin")
+    xy = cell_centers(32, 32, p.eval_bbox)
+    cfg = abi.solver_config("uniform")
+    ho = orc.scene(p.scene)
+    st_o = np.zeros(len(xy), dtype=abi.POINT_STATS_DTYPE)
+    for w in range(8):
+        orc.solve_batch(ho, None, cfg, xy, st_o, 5, w)
+    sol = api.Solver(api.Accel(p.scene), None, cfg)
+    sol.set_points(xy)
+    sol.solve_rounds(5, 0, 8)
+    st_g = sol.stats()
+    assert np.array_equal(st_o["count"], st_g["count"])
+    close = np.abs(st_o["mean"] - st_g["mean"]) <= 1e-9
+    assert close.mean() >= 0.999
+
+
+def test_shard_invariance_of_walk_streams(gpu):
+    """RNG keyed by the global point index: two shards reproduce one run."""
+    p = make_preset("neumann-strip-vlin")
+    xy = cell_centers(32, 32, p.eval_bbox)
+    cfg = abi.solver_config("uniform")
+    acc = api.Accel(p.scene)
+    whole = api.Solver(acc, None, cfg)
+    whole.set_points(xy)
+    whole.solve_rounds(3, 0, 4)
+    parts = []
+    for r in range(2):
+        s = api.Solver(acc, None, cfg)
+        half = len(xy) // 2
+        s.set_points(xy[r * half:(r + 1) * half], global_offset=r * half)
+        s.solve_rounds(3, 0, 4)
+        parts.append(s.stats())
+    assert np.array_equal(np.concatenate(parts), whole.stats())
+
+
+def test_records_and_backfill(gpu, orc):
+    p = make_preset("curves")
+    cfg = abi.field_config()
+    fo = orc.field(cfg, p.scene.bbox, 31)
+    fg = api.GuidingField(cfg, p.scene.bbox, 31)
+    xy = cell_centers(24, 24, p.eval_bbox)
+    sc = abi.solver_config("learnable_mis")
+    ho = orc.scene(p.scene)
+    st_o = np.zeros(len(xy), dtype=abi.POINT_STATS_DTYPE)
+    rec_o = orc.solve_batch(ho, fo, sc, xy, st_o, 7, 0, collect=True)
+    sol = api.Solver(api.Accel(p.scene), fg, sc)
+    st_g = np.zeros(len(xy), dtype=abi.POINT_STATS_DTYPE)
+    rec_g = api.solve_batch(sol, xy, st_g, 7, 0, collect_records=True)
+    assert len(rec_g) == len(rec_o)
+    # record payload is fp32 on device: compare order-free sums to 1e-5
+    for k in ("target", "pdf_mis", "pdf_u"):
+        np.testing.assert_allclose(np.sort(rec_g[k]), np.sort(rec_o[k]), rtol=1e-5, atol=1e-6)
+    c = rec_o["c"] * rec_o["pdf_g"] + (1 - rec_o["c"]) * rec_o["pdf_u"]
+    np.testing.assert_allclose(rec_o["pdf_mis"], c, rtol=1e-12)
+
+
+# ---------------------------------------------------------------- training
+def test_minibatch_gradient_matches_oracle(gpu, orc):
+    """One minibatch gradient (fp32 device MLP) vs the oracle's fp64
+    eval_with_tape/backward on identical records: relative L2 error < 1e-3."""
+    p = make_preset("curves")
+    cfg = abi.field_config()
+    fo = orc.field(cfg, p.scene.bbox, 31)
+    fg = api.GuidingField(cfg, p.scene.bbox, 31)
+    xy = cell_centers(40, 40, p.eval_bbox)
+    sc = abi.solver_config("learnable_mis")
+    ho = orc.scene(p.scene)
+    st = np.zeros(len(xy), dtype=abi.POINT_STATS_DTYPE)
+    recs = orc.solve_batch(ho, fo, sc, xy, st, 7, 0, collect=True)[:4096]
+    tc = abi.train_config(seed=1)
+    g_o = orc.field_grad(fo, recs, tc)
+    sol = api.Solver(api.Accel(p.scene), fg, sc)
+    g_g = sol.field_grad(recs, tc)
+    emb = 87040
+    for sl in (slice(0, emb), slice(emb, None)):
+        err = np.linalg.norm(g_g[sl] - g_o[sl]) / np.linalg.norm(g_o[sl])
+        assert err < 1e-3, err
+
+
+def test_train_round_reduces_kl_and_updates_field(gpu):
+    p = make_preset("neumann-strip-vlin")
+    cfg = abi.field_config()
+    fg = api.GuidingField(cfg, p.scene.bbox, 1)
+    xy = cell_centers(128, 128, p.eval_bbox)
+    sol = api.Solver(api.Accel(p.scene), fg, abi.solver_config("learnable_mis"))
+    sol.set_points(xy)
+    p0 = fg.params()
+    tc = abi.train_config(seed=1)
+    sol.solve_rounds(1, 0, 1, collect=True)
+    st = sol.train_round(tc, 0)
+    assert st.steps == 2 and st.records_consumed > 30000
+    assert np.isfinite(st.mean_grad_norm)
+    p1 = fg.params()
+    assert not np.array_equal(p0, p1)
+    assert np.all(np.isfinite(p1))
