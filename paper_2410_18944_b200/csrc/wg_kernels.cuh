@@ -80,6 +80,10 @@ cudaError_t launch_queries(const QueryArgs& a, cudaStream_t st);
 cudaError_t launch_walks(const WalkArgs& a, bool guided_exact_default, bool guided_generic,
                          int blocks, cudaStream_t st);
 int walk_blocks_per_sm(bool guided_exact_default, bool guided_generic, int smem_bytes);
+// 8-lanes-per-walk guided kernel for the default field shape (wg_walk_g8.cu)
+int walk_g8_smem(const WalkArgs& a);
+int walk_g8_blocks_per_sm(int smem);
+cudaError_t launch_walks_g8(const WalkArgs& a, int blocks, cudaStream_t st);
 cudaError_t launch_welford(const double* est, const int32_t* esc, int64_t n_points,
                            int32_t n_rounds, wg_point_stats* stats, cudaStream_t st);
 cudaError_t launch_field_eval(const FieldView& f, int64_t n, const double* xy, double* out,

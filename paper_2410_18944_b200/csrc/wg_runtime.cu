@@ -357,18 +357,25 @@ void run_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t round
   a.rec_capacity = s->rec_capacity;
   a.key_seed = key_seed;
 
+  // guided walks on the default field shape run 8 lanes per walk
+  const bool g8 = dflt;
   int smem = (s->scene->smem_bytes > 0 ? ((s->scene->smem_bytes + 15) & ~15) : 0) +
              (guided ? ((int)sizeof(float) * s->field->view.mlp_count + 15) / 16 * 16 : 0);
-  int per_sm = std::max(1, walk_blocks_per_sm(dflt, guided && !dflt, smem));
+  if (g8) smem = walk_g8_smem(a);
+  const int lanes_per_walk = g8 ? 8 : 1;
+  const int block = g8 ? 256 : 128;
+  int per_sm = std::max(1, g8 ? walk_g8_blocks_per_sm(smem)
+                              : walk_blocks_per_sm(dflt, guided && !dflt, smem));
   CK(cudaEventRecord(s->ev0, s->stream));
   for (int32_t r0 = 0; r0 < rounds; r0 += chunk) {
     int32_t n = std::min(chunk, rounds - r0);
     a.wpp_first = wpp_first + r0;
     a.n_rounds = n;
     int64_t total = s->n_points * n;
-    int64_t want = (total + 127) / 128;
+    int64_t want = (total * lanes_per_walk + block - 1) / block;
     int blocks = static_cast<int>(std::min<int64_t>(want, (int64_t)per_sm * s->sm_count));
-    CKL(launch_walks(a, dflt, guided && !dflt, std::max(1, blocks), s->stream));
+    if (g8) CKL(launch_walks_g8(a, std::max(1, blocks), s->stream));
+    else CKL(launch_walks(a, dflt, guided && !dflt, std::max(1, blocks), s->stream));
     CKL(launch_welford(a.est, a.esc, s->n_points, n, s->stats.as<wg_point_stats>(), s->stream));
   }
   CK(cudaEventRecord(s->ev1, s->stream));
@@ -410,7 +417,8 @@ wg_train_stats train_records(wg_solver_s* s, int64_t n_recs, const wg_train_conf
        "device training is built for the default field shape (L=4, F=4, hidden 64, K=8, 2D)");
   wg_train_stats st{};
   CK(cudaEventRecord(s->ev2, s->stream));
-  ensure_train_buffers(s, std::max<int64_t>(n_recs, 1));
+  // size once for the whole record arena: no allocation churn between rounds
+  ensure_train_buffers(s, std::max<int64_t>(std::max(n_recs, s->rec_capacity), 1));
   unsigned long long* cnt = s->counters.as<unsigned long long>();
   CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 8, s->stream));
   const uint32_t* order;
