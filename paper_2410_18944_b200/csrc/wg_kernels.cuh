@@ -84,6 +84,12 @@ int walk_blocks_per_sm(bool guided_exact_default, bool guided_generic, int smem_
 int walk_g8_smem(const WalkArgs& a);
 int walk_g8_blocks_per_sm(int smem);
 cudaError_t launch_walks_g8(const WalkArgs& a, int blocks, cudaStream_t st);
+// tcgen05 MLP walk kernel / field evaluation (wg_walk_tc.cu)
+int walk_tc_smem(const WalkArgs& a);
+int walk_tc_blocks_per_sm(int smem);
+cudaError_t launch_walks_tc(const WalkArgs& a, int blocks, cudaStream_t st);
+cudaError_t launch_field_eval_tc(const FieldView& f, int64_t n, const double* xy, double* out,
+                                 int sm_count, cudaStream_t st);
 cudaError_t launch_welford(const double* est, const int32_t* esc, int64_t n_points,
                            int32_t n_rounds, wg_point_stats* stats, cudaStream_t st);
 cudaError_t launch_field_eval(const FieldView& f, int64_t n, const double* xy, double* out,

@@ -1,0 +1,210 @@
+// Guiding-field MLP (16 -> 64 -> 64 -> 33, ReLU) on the 5th-generation
+// tensor cores for one tile of 128 rows (one row per thread of a 128-thread
+// CTA; thread t <-> TMEM lane t <-> MMA row t).
+//
+//   layer l:  D[tmem] = A_l (128 x K, smem) * B_l^T (N x K, smem), fp32 accum
+//   A/B are fp32 values split into fp16 hi + lo; three MMAs per K-block
+//   (hi*hi, lo*hi, hi*lo) give ~22 significant bits per product, so the
+//   result tracks the fp32 reference MLP to ~1e-6 relative. Activations are
+//   scaled by powers of two before the split (exact) to stay in fp16's
+//   normal range; the epilogue undoes the scale, adds the bias and applies
+//   ReLU, then writes the next layer's A tile. TMEM: 128 columns
+//   (layer 1 -> cols 0-63, layer 2 -> 64-127, layer 3 -> 0-47).
+#pragma once
+
+#include "wg_field.cuh"
+#include "wg_umma.cuh"
+
+namespace wg {
+
+struct TcLayout {
+  static constexpr int M = 128, NIN = 16, NH = 64, NO = 33, NO_PAD = 48;
+  static constexpr uint32_t A_HI = 0;                      // 128 x 64 fp16
+  static constexpr uint32_t A_LO = A_HI + M * NH * 2;      // 16 KB each
+  static constexpr uint32_t B1_HI = A_LO + M * NH * 2;     // 64 x 16
+  static constexpr uint32_t B1_LO = B1_HI + NH * NIN * 2;
+  static constexpr uint32_t B2_HI = B1_LO + NH * NIN * 2;  // 64 x 64
+  static constexpr uint32_t B2_LO = B2_HI + NH * NH * 2;
+  static constexpr uint32_t B3_HI = B2_LO + NH * NH * 2;   // 48 x 64
+  static constexpr uint32_t B3_LO = B3_HI + NO_PAD * NH * 2;
+  static constexpr uint32_t BIAS = B3_LO + NO_PAD * NH * 2;  // 64 + 64 + 48 fp32
+  static constexpr uint32_t BAR = BIAS + (NH + NH + NO_PAD) * 4;
+  static constexpr uint32_t TMEM_SLOT = BAR + 8;
+  static constexpr uint32_t BYTES = TMEM_SLOT + 8;
+  static constexpr uint32_t TMEM_COLS = 128;
+};
+
+constexpr float kTcScaleIn = 1024.0f;   // layer-1 inputs (grid features)
+constexpr float kTcScaleHid = 64.0f;    // hidden activations
+
+// Stage B_l = W_l^T as split fp16 in the K-major layout, plus the biases.
+// Called by all threads of the CTA; caller syncs afterwards.
+__device__ __forceinline__ void tc_stage_weights(unsigned char* sm, const FieldView& f) {
+  using L = TcLayout;
+  const float* p = f.p;
+  auto put = [&](uint32_t hi_off, uint32_t lo_off, int n, int k, int K, float v) {
+    __half h, l;
+    umma::split_f16(v, h, l);
+    uint32_t o = umma::kmajor_off(n, k, K);
+    *reinterpret_cast<__half*>(sm + hi_off + o) = h;
+    *reinterpret_cast<__half*>(sm + lo_off + o) = l;
+  };
+  for (int e = threadIdx.x; e < L::NH * L::NIN; e += blockDim.x) {  // W1[k][n], k < 16
+    int n = e % L::NH, k = e / L::NH;
+    put(L::B1_HI, L::B1_LO, n, k, L::NIN, p[f.w1 + k * L::NH + n]);
+  }
+  for (int e = threadIdx.x; e < L::NH * L::NH; e += blockDim.x) {
+    int n = e % L::NH, k = e / L::NH;
+    put(L::B2_HI, L::B2_LO, n, k, L::NH, p[f.w2 + k * L::NH + n]);
+  }
+  for (int e = threadIdx.x; e < L::NO_PAD * L::NH; e += blockDim.x) {
+    int n = e % L::NO_PAD, k = e / L::NO_PAD;
+    put(L::B3_HI, L::B3_LO, n, k, L::NH, n < L::NO ? p[f.w3 + k * L::NO + n] : 0.0f);
+  }
+  float* bias = reinterpret_cast<float*>(sm + L::BIAS);
+  for (int i = threadIdx.x; i < L::NH; i += blockDim.x) {
+    bias[i] = p[f.b1 + i];
+    bias[L::NH + i] = p[f.b2 + i];
+  }
+  for (int i = threadIdx.x; i < L::NO_PAD; i += blockDim.x)
+    bias[2 * L::NH + i] = i < L::NO ? p[f.b3 + i] : 0.0f;
+  umma::fence_async_smem();
+}
+
+// One-time TMEM allocation (warp 0) and mbarrier init; caller syncs after.
+__device__ __forceinline__ void tc_setup(unsigned char* sm) {
+  using L = TcLayout;
+  if (threadIdx.x < 32) umma::tmem_alloc(reinterpret_cast<uint32_t*>(sm + L::TMEM_SLOT), L::TMEM_COLS);
+  if (threadIdx.x == 0) umma::mbar_init(reinterpret_cast<uint64_t*>(sm + L::BAR), 1);
+}
+
+__device__ __forceinline__ void tc_teardown(unsigned char* sm) {
+  using L = TcLayout;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    umma::fence_after();
+    umma::tmem_dealloc(*reinterpret_cast<uint32_t*>(sm + L::TMEM_SLOT), L::TMEM_COLS);
+  }
+}
+
+// write this thread's A row: K values (already scaled), split hi/lo
+template <int K>
+__device__ __forceinline__ void tc_put_row(unsigned char* sm, int row, const float* v) {
+  using L = TcLayout;
+#pragma unroll
+  for (int c = 0; c < K / 8; ++c) {
+    __half hi[8], lo[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) umma::split_f16(v[8 * c + i], hi[i], lo[i]);
+    uint32_t o = umma::kmajor_off(row, 8 * c, K);
+    *reinterpret_cast<uint4*>(sm + L::A_HI + o) = *reinterpret_cast<uint4*>(hi);
+    *reinterpret_cast<uint4*>(sm + L::A_LO + o) = *reinterpret_cast<uint4*>(lo);
+  }
+}
+
+// issue one layer (thread 0 only): K/16 K-blocks x 3 split terms
+template <int K, int N>
+__device__ __forceinline__ void tc_issue(unsigned char* sm, uint32_t tmem_d, uint32_t b_hi,
+                                         uint32_t b_lo) {
+  using L = TcLayout;
+  const uint32_t base = umma::smem_u32(sm);
+  constexpr uint32_t idesc = umma::idesc_f16(L::M, N);
+#pragma unroll
+  for (int kb = 0; kb < K / 16; ++kb) {
+    const uint32_t ko = kb * 256;
+    uint64_t ahi = umma::desc_kmajor(base + L::A_HI + ko, K);
+    uint64_t alo = umma::desc_kmajor(base + L::A_LO + ko, K);
+    uint64_t bhi = umma::desc_kmajor(base + b_hi + ko, K);
+    uint64_t blo = umma::desc_kmajor(base + b_lo + ko, K);
+    umma::mma_f16(tmem_d, ahi, bhi, idesc, kb > 0 ? 1u : 0u);
+    umma::mma_f16(tmem_d, alo, bhi, idesc, 1u);
+    umma::mma_f16(tmem_d, ahi, blo, idesc, 1u);
+  }
+  umma::commit(reinterpret_cast<uint64_t*>(sm + L::BAR));
+}
+
+// Forward pass of the whole 128-row tile. Every thread of the CTA calls it
+// with its row's 16 inputs (zeros for idle rows); out[0..32] = raw outputs.
+__device__ __forceinline__ void tc_forward(unsigned char* sm, uint32_t& phase, const float* x,
+                                           float* out) {
+  using L = TcLayout;
+  const int row = threadIdx.x;
+  const int warp = threadIdx.x >> 5;
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(sm + L::TMEM_SLOT);
+  const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  const float* bias = reinterpret_cast<const float*>(sm + L::BIAS);
+  float v[L::NH];
+  // ---- layer 1
+#pragma unroll
+  for (int i = 0; i < L::NIN; ++i) v[i] = x[i] * kTcScaleIn;
+  tc_put_row<L::NIN>(sm, row, v);
+  umma::fence_async_smem();
+  umma::fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    umma::fence_after();
+    tc_issue<L::NIN, L::NH>(sm, tmem + 0, L::B1_HI, L::B1_LO);
+  }
+  umma::mbar_wait(bar, phase);
+  phase ^= 1u;
+  umma::fence_after();
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    float a[16];
+    umma::ld_x16(trow + 16 * c, a);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      float h = a[i] * (1.0f / kTcScaleIn) + bias[16 * c + i];
+      v[16 * c + i] = (h > 0.0f ? h : 0.0f) * kTcScaleHid;
+    }
+  }
+  tc_put_row<L::NH>(sm, row, v);
+  umma::fence_async_smem();
+  umma::fence_before();
+  __syncthreads();
+  // ---- layer 2
+  if (threadIdx.x == 0) {
+    umma::fence_after();
+    tc_issue<L::NH, L::NH>(sm, tmem + 64, L::B2_HI, L::B2_LO);
+  }
+  umma::mbar_wait(bar, phase);
+  phase ^= 1u;
+  umma::fence_after();
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    float a[16];
+    umma::ld_x16(trow + 64 + 16 * c, a);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      float h = a[i] * (1.0f / kTcScaleHid) + bias[L::NH + 16 * c + i];
+      v[16 * c + i] = (h > 0.0f ? h : 0.0f) * kTcScaleHid;
+    }
+  }
+  tc_put_row<L::NH>(sm, row, v);
+  umma::fence_async_smem();
+  umma::fence_before();
+  __syncthreads();
+  // ---- layer 3
+  if (threadIdx.x == 0) {
+    umma::fence_after();
+    tc_issue<L::NH, L::NO_PAD>(sm, tmem + 0, L::B3_HI, L::B3_LO);
+  }
+  umma::mbar_wait(bar, phase);
+  phase ^= 1u;
+  umma::fence_after();
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    float a[16];
+    umma::ld_x16(trow + 16 * c, a);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      int j = 16 * c + i;
+      if (j < L::NO) out[j] = a[i] * (1.0f / kTcScaleHid) + bias[2 * L::NH + j];
+    }
+  }
+  // TMEM columns are rewritten by the next tile's MMAs: order these loads first
+  umma::fence_before();
+}
+
+}  // namespace wg

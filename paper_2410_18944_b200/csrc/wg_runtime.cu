@@ -357,15 +357,19 @@ void run_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t round
   a.rec_capacity = s->rec_capacity;
   a.key_seed = key_seed;
 
-  // guided walks on the default field shape run 8 lanes per walk
-  const bool g8 = dflt;
+  // guided walks on the default field shape: tcgen05 MLP tile kernel, or the
+  // bit-faithful CUDA-core MLP with 8 lanes per walk
+  const bool tc = dflt && s->mlp == WG_MLP_TENSOR;
+  const bool g8 = dflt && !tc;
   int smem = (s->scene->smem_bytes > 0 ? ((s->scene->smem_bytes + 15) & ~15) : 0) +
              (guided ? ((int)sizeof(float) * s->field->view.mlp_count + 15) / 16 * 16 : 0);
   if (g8) smem = walk_g8_smem(a);
+  if (tc) smem = walk_tc_smem(a);
   const int lanes_per_walk = g8 ? 8 : 1;
   const int block = g8 ? 256 : 128;
-  int per_sm = std::max(1, g8 ? walk_g8_blocks_per_sm(smem)
-                              : walk_blocks_per_sm(dflt, guided && !dflt, smem));
+  int per_sm = std::max(1, tc ? walk_tc_blocks_per_sm(smem)
+                              : g8 ? walk_g8_blocks_per_sm(smem)
+                                   : walk_blocks_per_sm(dflt, guided && !dflt, smem));
   CK(cudaEventRecord(s->ev0, s->stream));
   for (int32_t r0 = 0; r0 < rounds; r0 += chunk) {
     int32_t n = std::min(chunk, rounds - r0);
@@ -374,7 +378,8 @@ void run_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t round
     int64_t total = s->n_points * n;
     int64_t want = (total * lanes_per_walk + block - 1) / block;
     int blocks = static_cast<int>(std::min<int64_t>(want, (int64_t)per_sm * s->sm_count));
-    if (g8) CKL(launch_walks_g8(a, std::max(1, blocks), s->stream));
+    if (tc) CKL(launch_walks_tc(a, std::max(1, blocks), s->stream));
+    else if (g8) CKL(launch_walks_g8(a, std::max(1, blocks), s->stream));
     else CKL(launch_walks(a, dflt, guided && !dflt, std::max(1, blocks), s->stream));
     CKL(launch_welford(a.est, a.esc, s->n_points, n, s->stats.as<wg_point_stats>(), s->stream));
   }
@@ -840,12 +845,20 @@ int wostgpu_field_set_state(wg_field f, const float* p, const double* m, const d
 
 int wostgpu_field_eval_batch(wg_field f, int64_t n, const double* xy, double* out, int mlp) {
   return guarded([&] {
-    need(mlp == WG_MLP_EXACT, WG_ERR_NOT_BUILT, "tensor-core field evaluation not built yet");
+    need(mlp == WG_MLP_EXACT || default_shape(f->view), WG_ERR_NOT_BUILT,
+         "tensor-core field evaluation is built for the default field shape");
     if (n == 0) return;
     DBuf dxy, dout;
     dxy.upload(xy, 2 * n);
     dout.alloc(sizeof(double) * n * f->view.od);
-    CKL(launch_field_eval(f->view, n, dxy.as<double>(), dout.as<double>(), 0));
+    if (mlp == WG_MLP_TENSOR) {
+      int dev = 0, sms = 148;
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      CKL(launch_field_eval_tc(f->view, n, dxy.as<double>(), dout.as<double>(), sms, 0));
+    } else {
+      CKL(launch_field_eval(f->view, n, dxy.as<double>(), dout.as<double>(), 0));
+    }
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(out, dout.p, sizeof(double) * n * f->view.od, cudaMemcpyDeviceToHost));
   });

@@ -418,7 +418,6 @@ __global__ void normalize_kernel(int64_t n, const double* raw, int k, int dim, w
 }
 
 // ---------------------------------------------------------------- launchers
-static int g_launches_dummy = 0;
 
 cudaError_t launch_queries(const QueryArgs& a, cudaStream_t st) {
   if (a.n == 0) return cudaSuccess;

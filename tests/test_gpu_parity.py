@@ -248,3 +248,60 @@ def test_train_round_reduces_kl_and_updates_field(gpu):
     p1 = fg.params()
     assert not np.array_equal(p0, p1)
     assert np.all(np.isfinite(p1))
+
+
+# ---------------------------------------------------------------- tensor cores
+def _trained_like(params, rng):
+    """Field parameters with trained-scale magnitudes (features ~0.3,
+    non-trivial biases) so relative MLP errors are measured where they matter."""
+    p = params.copy()
+    emb = 87040
+    p[:emb] = rng.normal(0.0, 0.3, emb).astype(np.float32)
+    p[emb:] += rng.normal(0.0, 0.05, len(p) - emb).astype(np.float32)
+    return p
+
+
+@pytest.mark.parametrize("trained", [False, True])
+def test_tensor_core_mlp_matches_fp32_reference(gpu, orc, trained):
+    """tcgen05 MLP (split-fp16 operands, fp32 accumulation) vs the reference's
+    fp32 GuidingField::eval: |a-b| <= 1e-3 * max(|b|, 1e-3 * rowmax)."""
+    cfg = abi.field_config()
+    bbox = (0.0, 0.0, 1.0, 1.0)
+    fo = orc.field(cfg, bbox, 5)
+    fg = api.GuidingField(cfg, bbox, 5)
+    if trained:
+        p = _trained_like(fg.params(), np.random.default_rng(0))
+        fg.set_params(p)
+        orc.field_set_params(fo, p)
+    xy = probes(Rng(23, 0), 3001, -0.1, 1.1)
+    ref_out = orc.field_eval(fo, xy, 33)
+    tc_out = fg.eval_batch(xy, api.MLP_TENSOR)
+    rowmax = np.abs(ref_out).max(axis=1, keepdims=True)
+    tol = 1e-3 * np.maximum(np.abs(ref_out), 1e-3 * rowmax)
+    assert np.all(np.abs(tc_out - ref_out) <= tol), np.max(np.abs(tc_out - ref_out) / tol)
+
+
+def test_tensor_core_guided_walks_statistical_parity(gpu):
+    """Guided walks with the tcgen05 MLP vs the bit-faithful path on the same
+    (trained-like) field: per-point means agree within 3 standard errors."""
+    p = make_preset("neumann-strip-vlin")
+    cfg = abi.field_config()
+    fg = api.GuidingField(cfg, p.scene.bbox, 3)
+    fg.set_params(_trained_like(fg.params(), np.random.default_rng(1)))
+    xy = cell_centers(32, 32, p.eval_bbox)
+    sc = abi.solver_config("learnable_mis")
+    acc = api.Accel(p.scene)
+    stats = []
+    for mlp, seed in ((api.MLP_EXACT, 11), (api.MLP_TENSOR, 12)):
+        s = api.Solver(acc, fg, sc, mlp)
+        s.set_points(xy)
+        s.solve_rounds(seed, 0, 128)
+        stats.append(s.stats())
+    a, b = stats
+    se = np.sqrt(a["m2"] / (a["count"] * (a["count"] - 1)) + b["m2"] / (b["count"] * (b["count"] - 1)))
+    z = np.abs(a["mean"] - b["mean"]) / np.maximum(se, 1e-12)
+    assert np.mean(z > 3.0) < 0.01, np.mean(z > 3.0)
+    ref = np.array([p.analytic(x, y) for x, y in xy])
+    from paper_2410_18944_b200.scene import relmse
+    ra, rb = relmse(a["mean"], ref), relmse(b["mean"], ref)
+    assert abs(ra - rb) / ra < 0.25, (ra, rb)
