@@ -34,8 +34,6 @@ struct TcLayout {
   static constexpr uint32_t TMEM_COLS = 128;
 };
 
-constexpr float kTcScaleIn = 1024.0f;   // layer-1 inputs (grid features)
-constexpr float kTcScaleHid = 64.0f;    // hidden activations
 
 // Stage B_l = W_l^T as split fp16 in the K-major layout, plus the biases.
 // Called by all threads of the CTA; caller syncs afterwards.
@@ -87,6 +85,23 @@ __device__ __forceinline__ void tc_teardown(unsigned char* sm) {
   }
 }
 
+// Per-row power-of-two scale: brings the row's largest magnitude to [2^9, 2^10)
+// so the fp16 hi/lo split keeps ~22 bits relative to the row; the MMA output
+// row is multiplied back by `inv` in the epilogue (exact).
+template <int K>
+__device__ __forceinline__ void tc_row_scale(float* v, float& inv) {
+  float m = 0.0f;
+#pragma unroll
+  for (int i = 0; i < K; ++i) m = fmaxf(m, fabsf(v[i]));
+  int e = 0;
+  frexpf(m, &e);
+  if (m == 0.0f) e = 0;
+  const float s = ldexpf(1.0f, 10 - e);
+  inv = ldexpf(1.0f, e - 10);
+#pragma unroll
+  for (int i = 0; i < K; ++i) v[i] *= s;
+}
+
 // write this thread's A row: K values (already scaled), split hi/lo
 template <int K>
 __device__ __forceinline__ void tc_put_row(unsigned char* sm, int row, const float* v) {
@@ -135,9 +150,11 @@ __device__ __forceinline__ void tc_forward(unsigned char* sm, uint32_t& phase, c
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
   const float* bias = reinterpret_cast<const float*>(sm + L::BIAS);
   float v[L::NH];
+  float inv;
   // ---- layer 1
 #pragma unroll
-  for (int i = 0; i < L::NIN; ++i) v[i] = x[i] * kTcScaleIn;
+  for (int i = 0; i < L::NIN; ++i) v[i] = x[i];
+  tc_row_scale<L::NIN>(v, inv);
   tc_put_row<L::NIN>(sm, row, v);
   umma::fence_async_smem();
   umma::fence_before();
@@ -155,10 +172,11 @@ __device__ __forceinline__ void tc_forward(unsigned char* sm, uint32_t& phase, c
     umma::ld_x16(trow + 16 * c, a);
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      float h = a[i] * (1.0f / kTcScaleIn) + bias[16 * c + i];
-      v[16 * c + i] = (h > 0.0f ? h : 0.0f) * kTcScaleHid;
+      float h = a[i] * inv + bias[16 * c + i];
+      v[16 * c + i] = h > 0.0f ? h : 0.0f;
     }
   }
+  tc_row_scale<L::NH>(v, inv);
   tc_put_row<L::NH>(sm, row, v);
   umma::fence_async_smem();
   umma::fence_before();
@@ -177,10 +195,11 @@ __device__ __forceinline__ void tc_forward(unsigned char* sm, uint32_t& phase, c
     umma::ld_x16(trow + 64 + 16 * c, a);
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      float h = a[i] * (1.0f / kTcScaleHid) + bias[L::NH + 16 * c + i];
-      v[16 * c + i] = (h > 0.0f ? h : 0.0f) * kTcScaleHid;
+      float h = a[i] * inv + bias[L::NH + 16 * c + i];
+      v[16 * c + i] = h > 0.0f ? h : 0.0f;
     }
   }
+  tc_row_scale<L::NH>(v, inv);
   tc_put_row<L::NH>(sm, row, v);
   umma::fence_async_smem();
   umma::fence_before();
@@ -200,7 +219,7 @@ __device__ __forceinline__ void tc_forward(unsigned char* sm, uint32_t& phase, c
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       int j = 16 * c + i;
-      if (j < L::NO) out[j] = a[i] * (1.0f / kTcScaleHid) + bias[2 * L::NH + j];
+      if (j < L::NO) out[j] = a[i] * inv + bias[2 * L::NH + j];
     }
   }
   // TMEM columns are rewritten by the next tile's MMAs: order these loads first
