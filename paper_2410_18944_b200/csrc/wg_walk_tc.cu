@@ -13,8 +13,8 @@
 // shared memory for the whole launch. Statistics go through the same
 // [round][point] estimate buffer + Welford pass as the other walk kernels.
 #include "wg_kernels.cuh"
+#include "wg_mix32.cuh"
 #include "wg_mlp_tc.cuh"
-#include "wg_sphdist.cuh"
 
 namespace wg {
 
@@ -248,11 +248,12 @@ __global__ void __launch_bounds__(128) walk_kernel_tc(WalkArgs a) {
     if (!need) continue;
 
     // ---- phase C: decode + sample + move (wost.cpp:111-146, 218-264)
-    Mix m;
-    normalize2<8>(raw, 8, m);
-    if (a.sp.mode == WG_MODE_GUIDING_ONLY) m.c = 1.0;
-    else if (a.sp.mode == WG_MODE_FIXED_MIS) m.c = a.sp.fixed_c;
-    MisOut o = mis_sample(w.rng, m, w.on_n, w.nx, w.ny, a.sp.reflect != 0);
+    Mix32 m;
+    normalize32(raw, m);
+    double sel = m.c;
+    if (a.sp.mode == WG_MODE_GUIDING_ONLY) sel = 1.0;
+    else if (a.sp.mode == WG_MODE_FIXED_MIS) sel = a.sp.fixed_c;
+    MisOut o = mis_sample32(w.rng, m, sel, w.on_n, w.nx, w.ny, a.sp.reflect != 0);
     double mult = o.pu / o.pmis;
     if (w.rec >= 0) {
       DevRecord r;
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(128) walk_kernel_tc(WalkArgs a) {
       r.pdf_mis = static_cast<float>(o.pmis);
       r.pdf_g = static_cast<float>(o.pg);
       r.pdf_u = static_cast<float>(o.pu);
-      r.c = static_cast<float>(m.c);
+      r.c = static_cast<float>(sel);
       r.target = 0.0f;
       r.local = static_cast<float>(w.contrib);
       r.mult = static_cast<float>(mult);
