@@ -27,7 +27,9 @@ struct __align__(16) DevRecord {
   uint64_t key;  // deterministic selection key (seed, round, point, depth)
 };
 static_assert(sizeof(DevRecord) == 80, "record layout");
-enum : uint32_t { REC_ON_NEUMANN = 1u, REC_VALID = 2u };
+enum : uint32_t { REC_ON_NEUMANN = 1u, REC_VALID = 2u, REC_USABLE = 4u };
+
+struct TrainCtl;  // wg_train.cuh
 
 struct SolverParams {
   double eps, rmin, fixed_c, grazing_floor;
@@ -53,6 +55,8 @@ struct WalkArgs {
   unsigned long long* rec_counter;
   int64_t rec_capacity;
   uint64_t key_seed;
+  double pdf_floor;  // TrainConfig::pdf_floor, for the usable-record count
+  TrainCtl* ctl;     // round's record counts (collecting rounds)
   // counters: [0] steps, [1] escaped, [2] walks, [3] record overflow, [4] scene error
   unsigned long long* counters;
 };

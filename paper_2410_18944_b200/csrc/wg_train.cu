@@ -1,148 +1,92 @@
 // Online training of the guiding field on device (proj/src/guide_train.cpp).
 //
-//   select_kernel  filter pdf_mis < floor; a deterministic 64-bit key per
-//                  record (hash of seed, round, point, depth) sorted with a
-//                  radix sort gives a uniformly random order: its first
-//                  min(n, cap) records are the round's training set, cut into
-//                  minibatches exactly like train_batch (guide_train.cpp:101-130)
+//   compact_kernel usable records (pdf_mis >= floor) thinned by their
+//                  deterministic key to a random subset of expected size
+//                  min(n, cap), split into random minibatches (guide_train.cpp:101-130)
 //   grad kernel    one CTA per 128-record tile: gather + MLP forward, per-record
 //                  KL / selection gradient (Eq. 13 / 16) in fp64, backward, and
 //                  the tile's weight gradients reduced in shared memory; grid
 //                  corners receive their share by atomics (wg_train_tc.cu holds
 //                  the tcgen05 version of the three GEMMs)
 //   adam_kernel    bias-corrected Adam with fp64 moments (guide_field.cpp:317-331)
-#include <cub/cub.cuh>
-
 #include "wg_kernels.cuh"
 #include "wg_sphdist.cuh"
 #include "wg_train.cuh"
+#include "wg_loss.cuh"
 
 namespace wg {
 
 // ---------------------------------------------------------------- selection
-__global__ void select_keys_kernel(const DevRecord* recs, int64_t n, double pdf_floor,
-                                   uint64_t* keys, uint32_t* idx, unsigned long long* cnt) {
+// Training set of a round (train_batch, guide_train.cpp:101-130): usable
+// records (valid, pdf_mis >= floor) are thinned with probability
+// p = min(1, cap / usable) by their deterministic 64-bit key (a uniform
+// u = key / 2^64) and assigned to minibatch floor(u / p * n_mb); i.e. a
+// uniformly random subset of expected size min(usable, cap) in random
+// minibatches, without a sort. Device-only: the host never waits.
+__global__ void compact_kernel(const DevRecord* recs, const unsigned long long* rec_count,
+                               int64_t capacity, TrainCtl* ctl, TrainTotals* totals,
+                               uint32_t* lists, int64_t list_cap, int64_t max_records,
+                               int32_t minibatch) {
+  const int64_t n = static_cast<int64_t>(min(*rec_count, static_cast<unsigned long long>(capacity)));
+  const double usable = static_cast<double>(ctl->usable);
+  const double take = fmin(usable, static_cast<double>(max_records));
+  const int n_mb = take > 0.0 ? min(kMaxMinibatches, static_cast<int>(ceil(take / minibatch))) : 0;
+  const double p = usable > 0.0 ? fmin(1.0, static_cast<double>(max_records) / usable) : 0.0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    atomicAdd(&totals->seen, ctl->seen);
+    atomicAdd(&totals->low_pdf, ctl->low_pdf);
+  }
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const DevRecord r = recs[i];
+    if (!(r.flags & REC_VALID) || n_mb == 0) continue;
+    const double u = static_cast<double>(r.key >> 11) * 0x1.0p-53;
+    if (!(u < p) || !(r.flags & REC_USABLE)) continue;
+    int mb = static_cast<int>(u / p * n_mb);
+    mb = mb < n_mb - 1 ? mb : n_mb - 1;
+    unsigned long long slot = atomicAdd(&ctl->mb_count[mb], 1ull);
+    if (static_cast<int64_t>(slot) < list_cap) lists[mb * list_cap + static_cast<int64_t>(slot)] = static_cast<uint32_t>(i);
+    else atomicAdd(&totals->overflow, 1ull);
+  }
+}
+
+cudaError_t launch_compact(const DevRecord* recs, const unsigned long long* rec_count,
+                           int64_t capacity, TrainCtl* ctl, TrainTotals* totals, uint32_t* lists,
+                           int64_t list_cap, int64_t max_records, int32_t minibatch,
+                           cudaStream_t st) {
+  compact_kernel<<<148 * 4, 256, 0, st>>>(recs, rec_count, capacity, ctl, totals, lists, list_cap,
+                                         max_records, minibatch);
+  return cudaGetLastError();
+}
+
+// usable / low-pdf counts of imported records (train_batch with host records)
+__global__ void count_records_kernel(DevRecord* recs, int64_t n, double pdf_floor, TrainCtl* ctl) {
   int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  uint64_t key = ~0ull;
   int usable = 0, low = 0;
   if (i < n) {
-    const DevRecord r = recs[i];
+    DevRecord& r = recs[i];
     if (r.flags & REC_VALID) {
       if (static_cast<double>(r.pdf_mis) < pdf_floor) low = 1;
       else {
         usable = 1;
-        key = r.key;
+        r.flags |= REC_USABLE;
       }
     }
-    keys[i] = key;
-    idx[i] = static_cast<uint32_t>(i);
   }
-  // warp-aggregated counters: [0] valid records seen, [1] usable, [2] low pdf
-  unsigned seen = __popc(__ballot_sync(0xffffffffu, usable || low));
   unsigned us = __popc(__ballot_sync(0xffffffffu, usable));
   unsigned lo = __popc(__ballot_sync(0xffffffffu, low));
   if ((threadIdx.x & 31) == 0) {
-    if (seen) atomicAdd(&cnt[0], seen);
-    if (us) atomicAdd(&cnt[1], us);
-    if (lo) atomicAdd(&cnt[2], lo);
+    if (us) atomicAdd(&ctl->usable, us);
+    if (lo) atomicAdd(&ctl->low_pdf, lo);
+    if (us + lo) atomicAdd(&ctl->seen, us + lo);
   }
 }
 
-size_t sort_temp_bytes(int64_t n) {
-  size_t bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, bytes, static_cast<const uint64_t*>(nullptr),
-                                  static_cast<uint64_t*>(nullptr),
-                                  static_cast<const uint32_t*>(nullptr),
-                                  static_cast<uint32_t*>(nullptr), static_cast<int>(n));
-  return bytes;
-}
-
-cudaError_t launch_select(const DevRecord* recs, int64_t n, double pdf_floor, uint64_t* keys,
-                          uint64_t* keys_sorted, uint32_t* idx, uint32_t* idx_sorted, void* temp,
-                          size_t temp_bytes, unsigned long long* cnt, cudaStream_t st) {
+cudaError_t launch_count_records(DevRecord* recs, int64_t n, double pdf_floor, TrainCtl* ctl,
+                                 cudaStream_t st) {
   if (n == 0) return cudaSuccess;
-  select_keys_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(recs, n, pdf_floor, keys,
-                                                                        idx, cnt);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys_sorted, idx, idx_sorted,
-                                         static_cast<int>(n), 0, 64, st);
-}
-
-// ---------------------------------------------------------------- loss grad
-// dV/dTheta' of one direction (sphdist.cpp:324-366); accumulates into g
-template <int K>
-WG_D double mix_grad_one(const Mix& m, const float* raw, double nx, double ny, double* g) {
-  double v[K];
-  double val = 0.0;
-#pragma unroll
-  for (int i = 0; i < K; ++i) {
-    double dt = nx * m.mux[i] + ny * m.muy[i] + 0.0 * 0.0;
-    v[i] = exp(m.kappa[i] * dt + m.log_a[i]);
-    val += m.lambda[i] * v[i];
-  }
-#pragma unroll
-  for (int i = 0; i < K; ++i) g[3 * K + i] += m.lambda[i] * (v[i] - val);
-#pragma unroll
-  for (int i = 0; i < K; ++i) {
-    double t = nx * m.mux[i] + ny * m.muy[i] + 0.0 * 0.0;
-    double lv = m.lambda[i] * v[i];
-    double ku = exp(static_cast<double>(raw[2 * K + i]));
-    if (ku > kKappaMin && ku < kKappaMax)
-      g[2 * K + i] += lv * (t - bessel_i1_over_i0(m.kappa[i])) * m.kappa[i];
-    double mx = raw[2 * i], my = raw[2 * i + 1];
-    double mn = sqrt(mx * mx + my * my + 0.0 * 0.0);
-    if (mn >= 1e-12) {
-      double s = lv * m.kappa[i] / mn;
-      g[2 * i] += (nx - m.mux[i] * t) * s;
-      g[2 * i + 1] += (ny - m.muy[i] * t) * s;
-    }
-  }
-  return val;
-}
-
-// kl_grad (guide_train.cpp:25-42) + selection_grad (:44-56) for one record;
-// writes dL/d(raw output) scaled by inv_count into dy. Returns false when the
-// record is skipped (V below the floor).
-template <int K>
-WG_D bool record_dy(const float* raw, const DevRecord& r, const TrainArgs& a, float* dy) {
-  constexpr int OD = 4 * K + 1;
-  double g[OD];
-#pragma unroll
-  for (int j = 0; j < OD; ++j) g[j] = 0.0;
-  Mix m;
-  normalize2<K>(raw, K, m);
-  const bool on_n = (r.flags & REC_ON_NEUMANN) != 0;
-  const double nx = r.nux, ny = r.nuy, px = r.nx, py = r.ny;
-  const double target = r.target;
-  if (target != 0.0) {
-    double dv[OD];
-#pragma unroll
-    for (int j = 0; j < OD; ++j) dv[j] = 0.0;
-    double v = mix_grad_one<K>(m, raw, nx, ny, dv);
-    if (on_n && a.reflect) {
-      double rx, ry;
-      reflect(nx, ny, px, py, &rx, &ry);
-      v += mix_grad_one<K>(m, raw, rx, ry, dv);
-    }
-    if (!(v > a.v_floor)) return false;
-    double s = -target / (static_cast<double>(r.pdf_mis) * v);
-#pragma unroll
-    for (int j = 0; j < OD - 1; ++j) g[j] = s * dv[j];
-  }
-  if (a.learn_selection) {
-    double pg = on_n ? (a.reflect ? reflected_pdf(m, nx, ny, px, py) : mixture_pdf(m, nx, ny))
-                     : mixture_pdf(m, nx, ny);
-    double pu = r.pdf_u;
-    double pnow = m.c * pg + (1.0 - m.c) * pu;
-    if (pnow > 0.0) {
-      double dc = -a.e_fraction * target * (pg - pu) / (pnow * static_cast<double>(r.pdf_mis));
-      g[OD - 1] = dc * m.c * (1.0 - m.c);
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < OD; ++j) dy[j] = static_cast<float>(g[j] * a.inv_count);
-  return true;
+  count_records_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(recs, n, pdf_floor, ctl);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- tile kernel
@@ -179,9 +123,12 @@ __global__ void __launch_bounds__(TB) grad_tile_kernel(TrainArgs a) {
 
   const int t = threadIdx.x;
   const int64_t ri = static_cast<int64_t>(blockIdx.x) * TB + t;
-  const bool live = ri < a.count;
+  const int64_t count = static_cast<int64_t>(min(*a.count, static_cast<unsigned long long>(a.list_cap)));
+  if (static_cast<int64_t>(blockIdx.x) * TB >= count) return;
+  if (blockIdx.x == 0 && t == 0) a.grad[a.n_params] = static_cast<float>(count);
+  const bool live = ri < count;
   DevRecord r{};
-  if (live) r = a.recs[a.order[a.begin + ri]];
+  if (live) r = a.recs[a.list[ri]];
 
   // gather (fp32, guide_field.cpp:80-123) keeping corner indices/weights
   float x[IN];
@@ -265,8 +212,8 @@ __global__ void __launch_bounds__(TB) grad_tile_kernel(TrainArgs a) {
     unsigned c = __popc(__ballot_sync(0xffffffffu, used));
     unsigned sk = __popc(__ballot_sync(0xffffffffu, live && !used));
     if ((t & 31) == 0) {
-      if (c) atomicAdd(&a.counters[0], c);
-      if (sk) atomicAdd(&a.counters[1], sk);
+      if (c) atomicAdd(&a.totals->consumed, c);
+      if (sk) atomicAdd(&a.totals->skipped_v, sk);
     }
   }
   // backward through the layers (guide_field.cpp:258-303), row in smem
@@ -353,23 +300,43 @@ __global__ void __launch_bounds__(TB) grad_tile_kernel(TrainArgs a) {
 size_t grad_tile_smem() { return TILE_SMEM; }
 
 cudaError_t launch_grad_cuda_core(const TrainArgs& a, cudaStream_t st) {
-  if (a.count == 0) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(grad_tile_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(TILE_SMEM));
   if (e != cudaSuccess) return e;
-  int blocks = static_cast<int>((a.count + TB - 1) / TB);
+  int blocks = static_cast<int>((a.list_cap + TB - 1) / TB);
   grad_tile_kernel<<<blocks, TB, TILE_SMEM, st>>>(a);
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- Adam
-// guide_field.cpp:317-331; also accumulates |g|^2 for TrainStats
+// adam_step (guide_field.cpp:317-331). The minibatch's (global) record count
+// sits in g[n]; a step only happens when it is non-zero, exactly like the
+// reference which never steps on an empty minibatch.
+__global__ void adam_prep_kernel(AdamCtl* c, const float* count_slot, double b1, double b2) {
+  const double cnt = static_cast<double>(*count_slot);
+  if (cnt > 0.0) {
+    c->steps += 1;
+    c->bc1 = 1.0 - pow(b1, static_cast<double>(c->steps));
+    c->bc2 = 1.0 - pow(b2, static_cast<double>(c->steps));
+    c->scale = 1.0 / cnt;
+    c->active = 1;
+    c->norm2[(c->steps - 1) % kNormRing] = 0.0;
+  } else {
+    c->active = 0;
+  }
+}
+
+cudaError_t launch_adam_prep(AdamCtl* ctl, const float* count_slot, double b1, double b2,
+                             cudaStream_t st) {
+  adam_prep_kernel<<<1, 1, 0, st>>>(ctl, count_slot, b1, b2);
+  return cudaGetLastError();
+}
+
 __global__ void adam_kernel(float* p, double* m, double* v, float* g, int64_t n, double lr,
-                            double b1, double b2, double eps, double bc1, double bc2,
-                            const float* count, double* norm2) {
-  // gradient sums arrive with their record count in g[n] (summed over ranks)
-  const double scale = count ? 1.0 / static_cast<double>(*count) : 1.0;
+                            double b1, double b2, double eps, AdamCtl* c) {
+  if (!c->active) return;
+  const double scale = c->scale, bc1 = c->bc1, bc2 = c->bc2;
   double local = 0.0;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -379,20 +346,16 @@ __global__ void adam_kernel(float* p, double* m, double* v, float* g, int64_t n,
     double vi = v[i] = b2 * v[i] + (1.0 - b2) * gi * gi;
     double up = lr * (mi / bc1) / (sqrt(vi / bc2) + eps);
     p[i] = static_cast<float>(static_cast<double>(p[i]) - up);
-    g[i] = 0.0f;
   }
   for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
-  if ((threadIdx.x & 31) == 0) atomicAdd(norm2, local);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&c->norm2[(c->steps - 1) % kNormRing], local);
 }
 
 cudaError_t launch_adam(float* p, double* m, double* v, float* g, int64_t n, double lr, double b1,
-                        double b2, double eps, int64_t step, const float* count, double* norm2,
-                        cudaStream_t st) {
-  double bc1 = 1.0 - pow(b1, static_cast<double>(step));
-  double bc2 = 1.0 - pow(b2, static_cast<double>(step));
+                        double b2, double eps, AdamCtl* ctl, cudaStream_t st) {
   int blocks = static_cast<int>((n + 255) / 256);
-  if (blocks > 148 * 8) blocks = 148 * 8;
-  adam_kernel<<<blocks, 256, 0, st>>>(p, m, v, g, n, lr, b1, b2, eps, bc1, bc2, count, norm2);
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  adam_kernel<<<blocks, 256, 0, st>>>(p, m, v, g, n, lr, b1, b2, eps, ctl);
   return cudaGetLastError();
 }
 
@@ -415,7 +378,7 @@ __global__ void import_records_kernel(const wg_guide_record* in, int64_t n, DevR
   r.target = static_cast<float>(g.target);
   r.flags = REC_VALID | (g.on_neumann ? REC_ON_NEUMANN : 0u);
   r.prev = -1;
-  r.key = static_cast<uint64_t>(i);
+  r.key = Pcg::mix(0x696d706f7274ULL ^ Pcg::mix(static_cast<uint64_t>(i)));
   out[i] = r;
 }
 

@@ -1,34 +1,98 @@
-// Training kernels' argument block and launchers (wg_train.cu, wg_train_tc.cu).
+// Training kernels' argument blocks and launchers (wg_train.cu, wg_train_tc.cu).
+//
+// A training round runs entirely on the device with no host synchronisation:
+//   walk kernels count valid / usable records at backfill (TrainCtl),
+//   compact_kernel thins the usable records to the round's training set and
+//     splits it into minibatch index lists,
+//   per minibatch: grad tile kernel -> [NCCL allreduce] -> adam_prep -> adam,
+//   where the record count travels in the gradient buffer's last slot, so the
+//   (global) minibatch size and "is there a step at all" are decided on device.
 #pragma once
 
 #include "wg_kernels.cuh"
 
 namespace wg {
 
+constexpr int kMaxMinibatches = 8;
+constexpr int kNormRing = 4096;
+
+// per-solver, reset at the start of every collecting round
+struct TrainCtl {
+  unsigned long long seen, usable, low_pdf;  // filled at backfill
+  unsigned long long mb_count[kMaxMinibatches];
+  unsigned long long overflow;
+};
+
+// per-run totals (TrainStats, proj/include/wost/guide_train.hpp:48-58)
+struct TrainTotals {
+  unsigned long long seen, low_pdf, consumed, skipped_v, overflow;
+};
+
+// per-field optimizer control (device truth of GuidingField::adam_steps_)
+struct AdamCtl {
+  long long steps;
+  double bc1, bc2, scale;
+  int active;
+  int pad;
+  double norm2[kNormRing];  // |g|^2 of every step (ring)
+};
+
 struct TrainArgs {
   FieldView f;
   const DevRecord* recs;
-  const uint32_t* order;  // sorted record indices
-  int64_t begin, count;   // minibatch slice of `order`
-  float* grad;            // [n_params], accumulated
-  double inv_count;
+  const uint32_t* list;                // record indices of this minibatch
+  const unsigned long long* count;     // device: number of valid entries in list
+  int64_t list_cap;                    // grid covers list_cap records
+  float* grad;                         // [n_params + 1]; grad[n_params] = record count
+  int64_t n_params;
+  double inv_count;                    // 1.0 in training (mean taken by Adam)
   int32_t reflect, learn_selection;
   double e_fraction, v_floor;
-  unsigned long long* counters;  // [0] consumed, [1] skipped_low_v
+  TrainTotals* totals;
 };
 
-size_t sort_temp_bytes(int64_t n);
-cudaError_t launch_select(const DevRecord* recs, int64_t n, double pdf_floor, uint64_t* keys,
-                          uint64_t* keys_sorted, uint32_t* idx, uint32_t* idx_sorted, void* temp,
-                          size_t temp_bytes, unsigned long long* cnt, cudaStream_t st);
+cudaError_t launch_compact(const DevRecord* recs, const unsigned long long* rec_count,
+                           int64_t capacity, TrainCtl* ctl, TrainTotals* totals, uint32_t* lists,
+                           int64_t list_cap, int64_t max_records, int32_t minibatch,
+                           cudaStream_t st);
+cudaError_t launch_count_records(DevRecord* recs, int64_t n, double pdf_floor, TrainCtl* ctl,
+                                 cudaStream_t st);
 size_t grad_tile_smem();
 cudaError_t launch_grad_cuda_core(const TrainArgs& a, cudaStream_t st);
+cudaError_t launch_adam_prep(AdamCtl* ctl, const float* count_slot, double b1, double b2,
+                             cudaStream_t st);
 cudaError_t launch_adam(float* p, double* m, double* v, float* g, int64_t n, double lr, double b1,
-                        double b2, double eps, int64_t step, const float* count, double* norm2,
-                        cudaStream_t st);
+                        double b2, double eps, AdamCtl* ctl, cudaStream_t st);
 cudaError_t launch_import_records(const wg_guide_record* in, int64_t n, DevRecord* out,
                                   cudaStream_t st);
 cudaError_t launch_export_records(const DevRecord* in, int64_t n, wg_guide_record* out,
                                   unsigned long long* count, cudaStream_t st);
+
+// shared backfill (backfill_targets_append, proj/src/guide_train.cpp:58-79):
+// reverse suffix scan over a finished walk's record chain; also counts the
+// walk's records into the round's usable / low-pdf totals
+__device__ __forceinline__ void backfill_chain(DevRecord* recs, int last, double terminal,
+                                               double pdf_floor, TrainCtl* ctl) {
+  double un = terminal;
+  unsigned usable = 0, low = 0;
+  for (int i = last; i >= 0;) {
+    DevRecord& r = recs[i];
+    r.target = static_cast<float>(fabs(un));
+    r.flags |= REC_VALID;
+    if (static_cast<double>(r.pdf_mis) < pdf_floor) {
+      ++low;
+    } else {
+      ++usable;
+      r.flags |= REC_USABLE;
+    }
+    un = static_cast<double>(r.rr) * (static_cast<double>(r.local) + static_cast<double>(r.mult) * un);
+    i = r.prev;
+  }
+  if (ctl) {
+    if (usable) atomicAdd(&ctl->usable, static_cast<unsigned long long>(usable));
+    if (low) atomicAdd(&ctl->low_pdf, static_cast<unsigned long long>(low));
+    atomicAdd(&ctl->seen, static_cast<unsigned long long>(usable + low));
+  }
+}
 
 }  // namespace wg

@@ -12,6 +12,7 @@
 #include <cstdio>
 
 #include "wg_kernels.cuh"
+#include "wg_train.cuh"
 #include "wg_sphdist.cuh"
 
 namespace wg {
@@ -114,15 +115,7 @@ __device__ __forceinline__ void finish_walk(Lane& w, const WalkArgs& a, bool esc
   if (escaped) atomicAdd(&a.counters[1], 1ull);
   if (collect && !escaped && w.rec_ok) {
     // reverse suffix scan over this walk's records (guide_train.cpp:58-79)
-    double un = terminal;
-    for (int i = w.last_rec; i >= 0;) {
-      DevRecord& r = a.recs[i];
-      r.target = static_cast<float>(fabs(un));
-      r.flags |= REC_VALID;
-      un = static_cast<double>(r.rr) *
-           (static_cast<double>(r.local) + static_cast<double>(r.mult) * un);
-      i = r.prev;
-    }
+    backfill_chain(a.recs, w.last_rec, terminal, a.pdf_floor, a.ctl);
   }
   w.alive = false;
 }

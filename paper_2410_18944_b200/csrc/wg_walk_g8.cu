@@ -18,6 +18,7 @@
 //     every value is bit-identical to the sequential reference.
 // Only lane 0 writes results, records and counters.
 #include "wg_kernels.cuh"
+#include "wg_train.cuh"
 #include "wg_sphdist.cuh"
 
 namespace wg {
@@ -282,15 +283,7 @@ __global__ void __launch_bounds__(256) walk_kernel_g8(WalkArgs a) {
       atomicAdd(&a.counters[0], static_cast<unsigned long long>(w.depth));
       if (escaped) atomicAdd(&a.counters[1], 1ull);
       if (collect && !escaped && w.rec_ok) {  // backfill, guide_train.cpp:58-79
-        double un = terminal;
-        for (int i = w.last_rec; i >= 0;) {
-          DevRecord& r = a.recs[i];
-          r.target = static_cast<float>(fabs(un));
-          r.flags |= REC_VALID;
-          un = static_cast<double>(r.rr) *
-               (static_cast<double>(r.local) + static_cast<double>(r.mult) * un);
-          i = r.prev;
-        }
+        backfill_chain(a.recs, w.last_rec, terminal, a.pdf_floor, a.ctl);
       }
     }
     w.alive = false;

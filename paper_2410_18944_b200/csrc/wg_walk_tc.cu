@@ -13,6 +13,7 @@
 // shared memory for the whole launch. Statistics go through the same
 // [round][point] estimate buffer + Welford pass as the other walk kernels.
 #include "wg_kernels.cuh"
+#include "wg_train.cuh"
 #include "wg_mix32.cuh"
 #include "wg_mlp_tc.cuh"
 
@@ -43,14 +44,7 @@ __device__ __forceinline__ void t_finish(TLane& w, const WalkArgs& a, bool escap
   atomicAdd(&a.counters[0], static_cast<unsigned long long>(w.depth));
   if (escaped) atomicAdd(&a.counters[1], 1ull);
   if (collect && !escaped && w.rec_ok) {  // backfill_targets_append, guide_train.cpp:58-79
-    double un = terminal;
-    for (int i = w.last_rec; i >= 0;) {
-      DevRecord& r = a.recs[i];
-      r.target = static_cast<float>(fabs(un));
-      r.flags |= REC_VALID;
-      un = static_cast<double>(r.rr) * (static_cast<double>(r.local) + static_cast<double>(r.mult) * un);
-      i = r.prev;
-    }
+    backfill_chain(a.recs, w.last_rec, terminal, a.pdf_floor, a.ctl);
   }
   w.alive = false;
 }
