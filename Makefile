@@ -21,7 +21,7 @@ build/%.o: $(PKG)/csrc/%.cu $(HDR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(PKG)/libwostgpu.so: $(OBJ)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lnccl -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart -ldl
 
 oracle:
 	$(MAKE) -C oracle all

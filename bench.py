@@ -190,10 +190,10 @@ def main():
     preset = make_preset(PRESET)
     bb = preset.scene.bbox
     # weak scaling: rank r owns rows [GRID r, GRID (r+1)) of a GRID x GRID*world grid
+    from paper_2410_18944_b200.parallel import broadcast_comm_id, shard_points
     all_pts = cell_centers(GRID, GRID * world, bb)
     n_local = GRID * GRID
-    pts = np.ascontiguousarray(all_pts[rank * n_local:(rank + 1) * n_local])
-    offset = rank * n_local
+    pts, offset = shard_points(all_pts, world, rank)
 
     fcfg = abi.field_config()
     field = api.GuidingField(fcfg, bb, SEED)
@@ -202,9 +202,7 @@ def main():
     solver = api.Solver(api.Accel(preset.scene), field, scfg,
                         api.MLP_TENSOR if args.mlp == "tensor" else api.MLP_EXACT)
     if world > 1:
-        uid = [api.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        solver.attach_comm(uid[0], world, rank)
+        solver.attach_comm(broadcast_comm_id(dist, rank), world, rank)
     tcfg = abi.train_config(seed=SEED)
     solver.set_points(pts, offset)
     zero_stats = np.zeros(n_local, dtype=abi.POINT_STATS_DTYPE)

@@ -1,12 +1,36 @@
 // Host runtime behind the C-ABI (include/wostgpu.h), part 1: device binding,
 // scene + BVH build and upload, batched Accel queries, guiding-field state and
 // evaluation. The solver (walk rounds, training, Engine loop) is wg_solver.cu.
+#include <dlfcn.h>
+
 #include <map>
 
 #include "wg_runtime.hpp"
 
 using namespace wg;
 using namespace wgrt;
+
+namespace wgrt {
+const NcclApi& nccl() {
+  static NcclApi api;
+  static bool loaded = false;
+  if (!loaded) {
+    // prefer a copy already mapped by the process (e.g. torch's), else the system one
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    need(h != nullptr, WG_ERR_CUDA, "NCCL (libnccl.so.2) not found");
+    api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+    api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(h, "ncclAllReduce"));
+    api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+    api.getErrorString = reinterpret_cast<decltype(api.getErrorString)>(dlsym(h, "ncclGetErrorString"));
+    need(api.getUniqueId && api.commInitRank && api.allReduce && api.commDestroy && api.getErrorString,
+         WG_ERR_CUDA, "NCCL symbols missing");
+    loaded = true;
+  }
+  return api;
+}
+}  // namespace wgrt
 
 namespace {
 

@@ -43,11 +43,25 @@ struct WgError : std::runtime_error {
     CK(expr);                  \
     ::wgrt::g_launches += 1;   \
   } while (0)
-#define NCK(expr)                                                                             \
-  do {                                                                                        \
-    ncclResult_t r_ = (expr);                                                                 \
-    if (r_ != ncclSuccess)                                                                    \
-      throw ::wgrt::WgError(WG_ERR_CUDA, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
+// NCCL is resolved at run time (dlopen) instead of linked: the process may
+// already hold torch's bundled libnccl.so.2, and linking the system copy would
+// shadow it. Only the five entry points below are used.
+struct NcclApi {
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+const NcclApi& nccl();  // wg_core.cu
+
+#define NCK(expr)                                                                    \
+  do {                                                                               \
+    ncclResult_t r_ = (expr);                                                        \
+    if (r_ != ncclSuccess)                                                           \
+      throw ::wgrt::WgError(WG_ERR_CUDA,                                             \
+                            std::string(#expr) + ": " + ::wgrt::nccl().getErrorString(r_)); \
   } while (0)
 
 template <class F>

@@ -232,7 +232,7 @@ void enqueue_train(wg_solver_s* s, const wg_train_config& tc) {
     enqueue_minibatch(s, tc, b, 1.0);
     float* count_slot = s->grad.as<float>() + f->n_params;
     if (s->comm)
-      NCK(ncclAllReduce(s->grad.p, s->grad.p, f->n_params + 1, ncclFloat, ncclSum, s->comm,
+      NCK(nccl().allReduce(s->grad.p, s->grad.p, f->n_params + 1, ncclFloat, ncclSum, s->comm,
                         s->stream));
     CKL(launch_adam_prep(actl, count_slot, tc.beta1, tc.beta2, s->stream));
     CKL(launch_adam(f->p.as<float>(), f->m.as<double>(), f->v.as<double>(), s->grad.as<float>(),
@@ -335,7 +335,7 @@ int wostgpu_solver_destroy(wg_solver s) {
   return guarded([&] {
     if (!s) return;
     cudaStreamSynchronize(s->stream);
-    if (s->comm) ncclCommDestroy(s->comm);
+    if (s->comm) nccl().commDestroy(s->comm);
     for (cudaEvent_t e : s->ev_walk) cudaEventDestroy(e);
     for (cudaEvent_t e : s->ev_train) cudaEventDestroy(e);
     cudaEventDestroy(s->ev_run0);
@@ -560,7 +560,7 @@ int wostgpu_run_profile(wg_solver s, double* walk_ms, double* train_ms, int64_t*
 int wostgpu_comm_unique_id(char id[128]) {
   return guarded([&] {
     ncclUniqueId u;
-    NCK(ncclGetUniqueId(&u));
+    NCK(nccl().getUniqueId(&u));
     static_assert(sizeof(u) == 128, "nccl id size");
     std::memcpy(id, &u, 128);
   });
@@ -570,7 +570,7 @@ int wostgpu_solver_attach_comm(wg_solver s, const char id[128], int32_t nranks, 
   return guarded([&] {
     ncclUniqueId u;
     std::memcpy(&u, id, 128);
-    NCK(ncclCommInitRank(&s->comm, nranks, u, rank));
+    NCK(nccl().commInitRank(&s->comm, nranks, u, rank));
     s->nranks = nranks;
     s->rank = rank;
   });
