@@ -166,7 +166,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mlp", default="exact", choices=["exact", "tensor"])
+    ap.add_argument("--mlp", default="tensor", choices=["exact", "tensor"])
     ap.add_argument("--ref-rounds", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -175,7 +175,7 @@ class Solver:
     (wost.hpp:33-51, solver.cpp:53-105) resident on one GPU."""
 
     def __init__(self, accel: Accel, field: GuidingField | None, cfg: abi.SolverConfig,
-                 mlp=MLP_EXACT):
+                 mlp=MLP_TENSOR):
         self.accel, self.field, self.cfg = accel, field, cfg
         h = C.c_void_p()
         check(load().wostgpu_solver_create(accel.h, field.h if field else None, C.byref(cfg),

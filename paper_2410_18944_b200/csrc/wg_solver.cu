@@ -321,7 +321,7 @@ int wostgpu_solver_create(wg_scene scene, wg_field field, const wg_solver_config
     s->scene = scene;
     s->field = field;
     s->cfg = *cfg;
-    s->mlp = WG_MLP_EXACT;
+    s->mlp = WG_MLP_TENSOR;  // fast path; WG_MLP_EXACT = bit-faithful reference arithmetic
     CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&s->ev_run0));
     CK(cudaEventCreate(&s->ev_run1));

@@ -198,7 +198,7 @@ def test_records_and_backfill(gpu, orc):
     ho = orc.scene(p.scene)
     st_o = np.zeros(len(xy), dtype=abi.POINT_STATS_DTYPE)
     rec_o = orc.solve_batch(ho, fo, sc, xy, st_o, 7, 0, collect=True)
-    sol = api.Solver(api.Accel(p.scene), fg, sc)
+    sol = api.Solver(api.Accel(p.scene), fg, sc, api.MLP_EXACT)
     st_g = np.zeros(len(xy), dtype=abi.POINT_STATS_DTYPE)
     rec_g = api.solve_batch(sol, xy, st_g, 7, 0, collect_records=True)
     assert len(rec_g) == len(rec_o)
@@ -305,3 +305,14 @@ def test_tensor_core_guided_walks_statistical_parity(gpu):
     from paper_2410_18944_b200.scene import relmse
     ra, rb = relmse(a["mean"], ref), relmse(b["mean"], ref)
     assert abs(ra - rb) / ra < 0.25, (ra, rb)
+
+
+def test_cpp_facade_drop_in_run(gpu, tmp_path):
+    """The reference-shaped C++ API (include/wostgpu.hpp) runs the Engine loop:
+    guided learnable-MIS beats uniform at equal samples on neumann-strip-vlin."""
+    import subprocess
+    from test_host import build_facade_demo
+    exe = build_facade_demo(tmp_path)
+    out = subprocess.run([exe, "32", "64"], capture_output=True, text=True, check=True).stdout.split()
+    rel_u, rel_g, steps = float(out[0]), float(out[1]), int(out[2])
+    assert steps > 0 and rel_g < rel_u, out

@@ -101,3 +101,18 @@ def test_ctypes_struct_layouts_match_header(tmp_path):
                      abi.GUIDE_RECORD_DTYPE.itemsize, abi.POINT_STATS_DTYPE.itemsize,
                      C.sizeof(abi.ValueSpec), C.sizeof(abi.FieldConfig), abi.MIXTURE_DTYPE.itemsize]
     assert abi.field_param_count(abi.field_config()) == 94433  # guide_field.hpp defaults
+
+
+def build_facade_demo(out_dir):
+    """Compile tests/cpp/facade_demo.cpp (the C++ drop-in facade) with g++."""
+    import subprocess
+    exe = os.path.join(str(out_dir), "facade_demo")
+    lib_dir = os.path.dirname(_lib.LIB_PATH)
+    subprocess.run(["/usr/bin/g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "facade_demo.cpp"), "-o", exe, "-L", lib_dir,
+                    "-lwostgpu", f"-Wl,-rpath,{lib_dir}"], check=True)
+    return exe
+
+
+def test_cpp_facade_compiles_and_links(tmp_path):
+    assert os.path.exists(build_facade_demo(tmp_path))
