@@ -17,7 +17,12 @@
 namespace wg {
 
 struct Mix32 {
-  float mux[8], muy[8], kappa[8], lambda[8];
+  // mean directions stay fp64: a sampled direction inherits |mu|, and a step
+  // of length R along a direction with |nu| = 1 + 6e-8 (fp32 normalisation)
+  // overshoots a Dirichlet wall on the bbox edge by more than the 1e-9 diag
+  // escape pad (wost.cpp:259-263)
+  double mux[8], muy[8];
+  float kappa[8], lambda[8];
   float lne[8];  // log normaliser + kappa: v_i = exp(kappa_i (t_i - 1) + lne_i)
   float c;
 };
@@ -53,12 +58,12 @@ WG_D void normalize32(const float* raw, Mix32& m) {
   const float iz = 1.0f / z;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    float x = raw[2 * i], y = raw[2 * i + 1];
-    float n = sqrtf(x * x + y * y);
-    if (n < 1e-12f) {  // fallback_mu, sphdist.cpp:274-278
-      float a = static_cast<float>(kTwoPi * i / kMaxK);
-      m.mux[i] = cosf(a);
-      m.muy[i] = sinf(a);
+    double x = raw[2 * i], y = raw[2 * i + 1];
+    double n = sqrt(x * x + y * y);
+    if (n < 1e-12) {  // fallback_mu, sphdist.cpp:274-278
+      double a = kTwoPi * i / kMaxK;
+      m.mux[i] = cos(a);
+      m.muy[i] = sin(a);
     } else {
       m.mux[i] = x / n;
       m.muy[i] = y / n;
@@ -112,7 +117,8 @@ WG_D double vm_angle_stable(Pcg& rng, double kappa) {
 WG_D void mixture_sample32(Pcg& rng, const Mix32& m, double* ox, double* oy) {
   double u = rng.uni();
   float acc = 0.0f;
-  float mux = m.mux[7], muy = m.muy[7], kap = m.kappa[7];
+  double mux = m.mux[7], muy = m.muy[7];
+  float kap = m.kappa[7];
   bool found = false;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {  // register-resident select of the picked lobe
