@@ -108,9 +108,14 @@ __device__ __forceinline__ void tc_put_row(unsigned char* sm, int row, const flo
   using L = TcLayout;
 #pragma unroll
   for (int c = 0; c < K / 8; ++c) {
-    __half hi[8], lo[8];
+    __half2 hi[4], lo[4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) umma::split_f16(v[8 * c + i], hi[i], lo[i]);
+    for (int i = 0; i < 4; ++i) {  // packed F2FP conversions, two values at a time
+      float2 x = make_float2(v[8 * c + 2 * i], v[8 * c + 2 * i + 1]);
+      hi[i] = __float22half2_rn(x);
+      float2 b = __half22float2(hi[i]);
+      lo[i] = __float22half2_rn(make_float2(x.x - b.x, x.y - b.y));
+    }
     uint32_t o = umma::kmajor_off(row, 8 * c, K);
     *reinterpret_cast<uint4*>(sm + L::A_HI + o) = *reinterpret_cast<uint4*>(hi);
     *reinterpret_cast<uint4*>(sm + L::A_LO + o) = *reinterpret_cast<uint4*>(lo);
@@ -136,6 +141,29 @@ __device__ __forceinline__ void tc_issue(unsigned char* sm, uint32_t tmem_d, uin
     umma::mma_f16(tmem_d, ahi, blo, idesc, 1u);
   }
   umma::commit(reinterpret_cast<uint64_t*>(sm + L::BAR));
+}
+
+// Bilinear multi-resolution gather (guide_field.cpp:80-123) for the default
+// shape (4 levels x 4 features): one 16-byte load per lattice corner.
+__device__ __forceinline__ void tc_gather(const FieldView& f, double x, double y, float* in) {
+  double ex = f.bbox[2] - f.bbox[0], ey = f.bbox[3] - f.bbox[1];
+  float u = static_cast<float>(sclamp((x - f.bbox[0]) / ex, 0.0, 1.0));
+  float v = static_cast<float>(sclamp((y - f.bbox[1]) / ey, 0.0, 1.0));
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    const int res = f.res[l];
+    float px = u * static_cast<float>(res - 1), py = v * static_cast<float>(res - 1);
+    int ix = imin(static_cast<int>(px), res - 2), iy = imin(static_cast<int>(py), res - 2);
+    float fx = px - ix, fy = py - iy;
+    const float4* base = reinterpret_cast<const float4*>(f.p + f.lvl_off[l] + (iy * res + ix) * 4);
+    float4 a = __ldg(base), b = __ldg(base + 1), c = __ldg(base + res), d = __ldg(base + res + 1);
+    float w00 = (1.0f - fx) * (1.0f - fy), w10 = fx * (1.0f - fy);
+    float w01 = (1.0f - fx) * fy, w11 = fx * fy;
+    in[4 * l + 0] = (w00 * a.x + w10 * b.x) + (w01 * c.x + w11 * d.x);
+    in[4 * l + 1] = (w00 * a.y + w10 * b.y) + (w01 * c.y + w11 * d.y);
+    in[4 * l + 2] = (w00 * a.z + w10 * b.z) + (w01 * c.z + w11 * d.z);
+    in[4 * l + 3] = (w00 * a.w + w10 * b.w) + (w01 * c.w + w11 * d.w);
+  }
 }
 
 // Forward pass of the whole 128-row tile. Every thread of the CTA calls it
@@ -167,13 +195,13 @@ __device__ __forceinline__ void tc_forward(unsigned char* sm, uint32_t& phase, c
   phase ^= 1u;
   umma::fence_after();
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    float a[16];
-    umma::ld_x16(trow + 16 * c, a);
+  for (int c = 0; c < 2; ++c) {
+    float a[32];
+    umma::ld_x32(trow + 32 * c, a);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      float h = a[i] * inv + bias[16 * c + i];
-      v[16 * c + i] = h > 0.0f ? h : 0.0f;
+    for (int i = 0; i < 32; ++i) {
+      float h = a[i] * inv + bias[32 * c + i];
+      v[32 * c + i] = h > 0.0f ? h : 0.0f;
     }
   }
   tc_row_scale<L::NH>(v, inv);
@@ -190,13 +218,13 @@ __device__ __forceinline__ void tc_forward(unsigned char* sm, uint32_t& phase, c
   phase ^= 1u;
   umma::fence_after();
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    float a[16];
-    umma::ld_x16(trow + 64 + 16 * c, a);
+  for (int c = 0; c < 2; ++c) {
+    float a[32];
+    umma::ld_x32(trow + 64 + 32 * c, a);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      float h = a[i] * inv + bias[L::NH + 16 * c + i];
-      v[16 * c + i] = h > 0.0f ? h : 0.0f;
+    for (int i = 0; i < 32; ++i) {
+      float h = a[i] * inv + bias[L::NH + 32 * c + i];
+      v[32 * c + i] = h > 0.0f ? h : 0.0f;
     }
   }
   tc_row_scale<L::NH>(v, inv);

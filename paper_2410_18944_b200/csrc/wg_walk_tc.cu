@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(128) walk_kernel_tc(WalkArgs a) {
     // ---- phase B: guiding-field MLP for the whole tile on the tensor cores
     float xin[TcLayout::NIN];
     if (need) {
-      field_gather(fv, w.x, w.y, xin);
+      tc_gather(fv, w.x, w.y, xin);
     } else {
 #pragma unroll
       for (int i = 0; i < TcLayout::NIN; ++i) xin[i] = 0.0f;
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(128) field_eval_tc_kernel(FieldView f, int64_t
   for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
     int64_t i = t * 128 + threadIdx.x;
     float xin[16], o[33];
-    if (i < n) field_gather(f, xy[2 * i], xy[2 * i + 1], xin);
+    if (i < n) tc_gather(f, xy[2 * i], xy[2 * i + 1], xin);
     else
       for (int k = 0; k < 16; ++k) xin[k] = 0.0f;
     tc_forward(smem, phase, xin, o);
