@@ -59,6 +59,9 @@ struct WalkArgs {
   TrainCtl* ctl;     // round's record counts (collecting rounds)
   // counters: [0] steps, [1] escaped, [2] walks, [3] record overflow, [4] scene error
   unsigned long long* counters;
+  // optional per-CTA phase timing [gridDim][4]: cycles in phase A (begin
+  // step + barrier), B (MLP), C (sample + move), iterations (WOSTGPU_PHASE_PROF)
+  unsigned long long* phase_prof;
 };
 
 struct QueryArgs {

@@ -6,6 +6,9 @@
 // synchronisation: walk kernel -> Welford -> [compaction -> per minibatch:
 // gradient tile -> NCCL allreduce -> Adam prep -> Adam]. The host only waits
 // when a caller asks for results (statistics, records, TrainStats, timings).
+#include <cstdio>
+#include <cstdlib>
+
 #include "wg_runtime.hpp"
 
 using namespace wg;
@@ -50,6 +53,7 @@ struct wg_solver_s {
   DBuf totals;    // TrainTotals (per run / train call)
   DBuf lists, grad;
   int64_t list_cap = 0;
+  DBuf phase_prof;  // WOSTGPU_PHASE_PROF diagnostics
   // timing: event pairs around walk launches and training rounds
   std::vector<cudaEvent_t> ev_walk, ev_train;
   int n_walk_ev = 0, n_train_ev = 0;
@@ -172,9 +176,29 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
     a.n_rounds = n;
     int64_t want = (s->n_points * n * lanes_per_walk + block - 1) / block;
     int blocks = static_cast<int>(std::min<int64_t>(want, (int64_t)per_sm * s->sms));
+    static const bool phase_prof = std::getenv("WOSTGPU_PHASE_PROF") != nullptr;
+    if (phase_prof && tc) {
+      s->phase_prof.alloc(sizeof(unsigned long long) * 4 * blocks);
+      CK(cudaMemsetAsync(s->phase_prof.p, 0, sizeof(unsigned long long) * 4 * blocks, s->stream));
+      a.phase_prof = s->phase_prof.as<unsigned long long>();
+    }
     CK(cudaEventRecord(pool_event(s->ev_walk, s->n_walk_ev), s->stream));
     if (tc) CKL(launch_walks_tc(a, std::max(1, blocks), s->stream));
-    else if (g8) CKL(launch_walks_g8(a, std::max(1, blocks), s->stream));
+    if (phase_prof && tc) {  // diagnostics: cycles per CTA iteration of the slowest CTA
+      std::vector<unsigned long long> h(4 * blocks);
+      CK(cudaMemcpyAsync(h.data(), s->phase_prof.p, sizeof(unsigned long long) * 4 * blocks,
+                         cudaMemcpyDeviceToHost, s->stream));
+      CK(cudaStreamSynchronize(s->stream));
+      int worst = 0;
+      for (int b = 0; b < blocks; ++b)
+        if (h[4 * b] + h[4 * b + 1] + h[4 * b + 2] > h[4 * worst] + h[4 * worst + 1] + h[4 * worst + 2])
+          worst = b;
+      double it = static_cast<double>(std::max<unsigned long long>(h[4 * worst + 3], 1));
+      std::fprintf(stderr, "[phase] cta %d iters %.0f cycles/iter A %.0f B %.0f C %.0f\n", worst, it,
+                   h[4 * worst] / it, h[4 * worst + 1] / it, h[4 * worst + 2] / it);
+    }
+    if (tc) {
+    } else if (g8) CKL(launch_walks_g8(a, std::max(1, blocks), s->stream));
     else CKL(launch_walks(a, dflt, guided && !dflt, std::max(1, blocks), s->stream));
     CK(cudaEventRecord(pool_event(s->ev_walk, s->n_walk_ev), s->stream));
     CKL(launch_welford(a.est, a.esc, s->n_points, n, s->stats.as<wg_point_stats>(), s->stream));

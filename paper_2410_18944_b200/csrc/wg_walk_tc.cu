@@ -197,7 +197,13 @@ __global__ void __launch_bounds__(128) walk_kernel_tc(WalkArgs a) {
   w.rec_left = 0;
   int64_t walks_done = 0;
 
+  long long t_iter = a.phase_prof ? clock64() : 0;
   for (;;) {
+    if (a.phase_prof) {  // phase C of the previous iteration ends here
+      long long t_top = clock64();
+      if (threadIdx.x == 0) a.phase_prof[4 * blockIdx.x + 2] += static_cast<unsigned long long>(t_top - t_iter);
+      t_iter = t_top;
+    }
     // ---- phase A: every slot advances to a walk that needs a direction
     bool need = false;
     for (;;) {
@@ -228,6 +234,11 @@ __global__ void __launch_bounds__(128) walk_kernel_tc(WalkArgs a) {
       }
     }
     if (!__syncthreads_or(need)) break;
+    long long t_b = a.phase_prof ? clock64() : 0;
+    if (a.phase_prof && threadIdx.x == 0) {
+      a.phase_prof[4 * blockIdx.x + 0] += static_cast<unsigned long long>(t_b - t_iter);
+      a.phase_prof[4 * blockIdx.x + 3] += 1;
+    }
 
     // ---- phase B: guiding-field MLP for the whole tile on the tensor cores
     float xin[TcLayout::NIN];
@@ -239,6 +250,11 @@ __global__ void __launch_bounds__(128) walk_kernel_tc(WalkArgs a) {
     }
     float raw[TcLayout::NO];
     tc_forward(tc, phase, xin, raw);
+    if (a.phase_prof) {
+      long long t_c = clock64();
+      if (threadIdx.x == 0) a.phase_prof[4 * blockIdx.x + 1] += static_cast<unsigned long long>(t_c - t_b);
+      t_iter = t_c;  // phase C is charged to the next iteration's phase A slot
+    }
     if (!need) continue;
 
     // ---- phase C: decode + sample + move (wost.cpp:111-146, 218-264)
