@@ -10,24 +10,32 @@
 
 namespace wg {
 
-// Guide record as kept in HBM during a collecting round (80 B). One per walk
-// step, appended by the walk kernel, completed by the walk's own backfill at
-// termination (backfill_targets_append, proj/src/guide_train.cpp:58-79).
+// Guide record as kept in HBM during a collecting round (80 B), one per walk
+// step, appended by the walk kernel.
+//
+// Target without a backward pass: backfill_targets_append
+// (proj/src/guide_train.cpp:58-79) runs u_k = rr_k (local_k + mult_k u_{k+1})
+// backwards from the terminal value. Unrolled, u_0 = P_{k+1} + Q_{k+1} u_{k+1}
+// with P_{k+1} = the walk's accumulated estimate after step k's local term and
+// Q_{k+1} = its throughput after step k's multiplier, and u_0 is the walk's
+// final estimate. So each record stores (P, Q) when it is written and the
+// target |u_{k+1}| = |(u_0 - P) / Q| is formed later, in one parallel pass,
+// from the walk's final estimate — no per-walk serial chain in the walk kernel.
 struct __align__(16) DevRecord {
   float x, y;
   float nux, nuy;
   float nx, ny;
   float pdf_mis, pdf_g, pdf_u, c;
-  float target;  // |u(x_{k+1})| after backfill
-  float local;   // <N> - <S> of this step (own throughput frame)
-  float mult;    // p_u / p_mis
-  float rr;      // roulette reweight
-  int32_t prev;  // previous record of the same walk, -1 for the first
+  float target;  // |u(x_{k+1})|, filled by the finalise pass
+  float acc_p;   // P: accumulated estimate after this step's local term
+  float thr_q;   // Q: throughput after this step's multiplier (0 = walk died)
+  float pad_;
+  int32_t walk;  // estimate-buffer slot of the walk (round * n_points + point); -1 imported
   uint32_t flags;
   uint64_t key;  // deterministic selection key (seed, round, point, depth)
 };
 static_assert(sizeof(DevRecord) == 80, "record layout");
-enum : uint32_t { REC_ON_NEUMANN = 1u, REC_VALID = 2u, REC_USABLE = 4u };
+enum : uint32_t { REC_ON_NEUMANN = 1u, REC_VALID = 2u, REC_USABLE = 4u, REC_WRITTEN = 8u };
 
 struct TrainCtl;  // wg_train.cuh
 

@@ -205,6 +205,15 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
   }
 }
 
+// targets + validity + usable counts of the arena's records (see DevRecord)
+void enqueue_finalize(wg_solver_s* s, double pdf_floor) {
+  s->ctl.alloc(sizeof(TrainCtl));
+  CK(cudaMemsetAsync(s->ctl.p, 0, sizeof(TrainCtl), s->stream));
+  CKL(launch_finalize_records(s->recs.as<DevRecord>(), s->rec_counter.as<unsigned long long>(),
+                              s->rec_capacity, s->est.as<double>(), s->esc.as<int32_t>(), pdf_floor,
+                              s->ctl.as<TrainCtl>(), s->stream));
+}
+
 void ensure_train_buffers(wg_solver_s* s, const wg_train_config& tc) {
   need(tc.minibatch >= 1, WG_ERR_INVALID, "minibatch must be >= 1");
   const int n_mb = static_cast<int>((tc.max_records_per_round + tc.minibatch - 1) / tc.minibatch);
@@ -246,6 +255,7 @@ void enqueue_train(wg_solver_s* s, const wg_train_config& tc) {
        "device training is built for the default field shape (L=4, F=4, hidden 64, K=8, 2D)");
   ensure_train_buffers(s, tc);
   CK(cudaEventRecord(pool_event(s->ev_train, s->n_train_ev), s->stream));
+  enqueue_finalize(s, tc.pdf_floor);
   CKL(launch_compact(s->recs.as<DevRecord>(), s->rec_counter.as<unsigned long long>(),
                      s->rec_capacity, s->ctl.as<TrainCtl>(), s->totals.as<TrainTotals>(),
                      s->lists.as<uint32_t>(), s->list_cap, tc.max_records_per_round, tc.minibatch,
@@ -320,9 +330,7 @@ void import_records(wg_solver_s* s, const wg_guide_record* recs, int64_t n, doub
   s->rec_counter.alloc(sizeof(unsigned long long));
   unsigned long long nn = static_cast<unsigned long long>(n);
   CK(cudaMemcpyAsync(s->rec_counter.p, &nn, sizeof(nn), cudaMemcpyHostToDevice, s->stream));
-  s->ctl.alloc(sizeof(TrainCtl));
-  CK(cudaMemsetAsync(s->ctl.p, 0, sizeof(TrainCtl), s->stream));
-  CKL(launch_count_records(s->recs.as<DevRecord>(), n, pdf_floor, s->ctl.as<TrainCtl>(), s->stream));
+  enqueue_finalize(s, pdf_floor);
   CK(cudaStreamSynchronize(s->stream));  // h goes out of scope
 }
 
@@ -431,6 +439,7 @@ int wostgpu_solve_batch(wg_solver s, int64_t n, const double* xy, wg_point_stats
 int wostgpu_fetch_records(wg_solver s, wg_guide_record* out, int64_t capacity, int64_t* n) {
   return guarded([&] {
     need(s->have_records, WG_ERR_INVALID, "no collecting round has run");
+    enqueue_finalize(s, 1e-8);  // targets from the walks' final estimates
     unsigned long long total = 0;
     CK(cudaMemcpyAsync(&total, s->rec_counter.p, 8, cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));

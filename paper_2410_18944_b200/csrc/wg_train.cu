@@ -59,33 +59,56 @@ cudaError_t launch_compact(const DevRecord* recs, const unsigned long long* rec_
   return cudaGetLastError();
 }
 
-// usable / low-pdf counts of imported records (train_batch with host records)
-__global__ void count_records_kernel(DevRecord* recs, int64_t n, double pdf_floor, TrainCtl* ctl) {
-  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  int usable = 0, low = 0;
-  if (i < n) {
+// Finalise a round's records: target |u_{k+1}| = |(u_0 - P) / Q| from the
+// walk's final estimate (the backfill of guide_train.cpp:58-79 without its
+// serial chain, see DevRecord), drop records of escaped walks (the reference
+// only backfills non-escaped walks, wost.cpp:373-383), and count usable /
+// low-pdf records for the selection. Imported records (walk < 0) keep their
+// target. Grid-stride over the device-side record count.
+__global__ void finalize_records_kernel(DevRecord* recs, const unsigned long long* rec_count,
+                                        int64_t capacity, const double* est, const int32_t* esc,
+                                        double pdf_floor, TrainCtl* ctl) {
+  const int64_t n = static_cast<int64_t>(min(*rec_count, static_cast<unsigned long long>(capacity)));
+  unsigned usable = 0, low = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     DevRecord& r = recs[i];
-    if (r.flags & REC_VALID) {
-      if (static_cast<double>(r.pdf_mis) < pdf_floor) low = 1;
-      else {
-        usable = 1;
-        r.flags |= REC_USABLE;
+    uint32_t fl = r.flags;
+    if (!(fl & REC_WRITTEN)) continue;  // unused slot of a lane's chunk
+    fl &= REC_WRITTEN | REC_ON_NEUMANN;
+    if (r.walk >= 0) {
+      if (esc[r.walk]) {
+        r.flags = fl;  // not valid
+        continue;
       }
+      const double q = r.thr_q;
+      r.target = q == 0.0 ? 0.0f
+                          : static_cast<float>(fabs((est[r.walk] - static_cast<double>(r.acc_p)) / q));
     }
+    fl |= REC_VALID;
+    if (static_cast<double>(r.pdf_mis) < pdf_floor) {
+      ++low;
+    } else {
+      ++usable;
+      fl |= REC_USABLE;
+    }
+    r.flags = fl;
   }
-  unsigned us = __popc(__ballot_sync(0xffffffffu, usable));
-  unsigned lo = __popc(__ballot_sync(0xffffffffu, low));
-  if ((threadIdx.x & 31) == 0) {
-    if (us) atomicAdd(&ctl->usable, us);
-    if (lo) atomicAdd(&ctl->low_pdf, lo);
-    if (us + lo) atomicAdd(&ctl->seen, us + lo);
+  for (int o = 16; o > 0; o >>= 1) {
+    usable += __shfl_down_sync(0xffffffffu, usable, o);
+    low += __shfl_down_sync(0xffffffffu, low, o);
+  }
+  if ((threadIdx.x & 31) == 0 && (usable | low)) {
+    atomicAdd(&ctl->usable, static_cast<unsigned long long>(usable));
+    atomicAdd(&ctl->low_pdf, static_cast<unsigned long long>(low));
+    atomicAdd(&ctl->seen, static_cast<unsigned long long>(usable + low));
   }
 }
 
-cudaError_t launch_count_records(DevRecord* recs, int64_t n, double pdf_floor, TrainCtl* ctl,
-                                 cudaStream_t st) {
-  if (n == 0) return cudaSuccess;
-  count_records_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(recs, n, pdf_floor, ctl);
+cudaError_t launch_finalize_records(DevRecord* recs, const unsigned long long* rec_count,
+                                    int64_t capacity, const double* est, const int32_t* esc,
+                                    double pdf_floor, TrainCtl* ctl, cudaStream_t st) {
+  finalize_records_kernel<<<148 * 4, 256, 0, st>>>(recs, rec_count, capacity, est, esc, pdf_floor, ctl);
   return cudaGetLastError();
 }
 
@@ -376,8 +399,8 @@ __global__ void import_records_kernel(const wg_guide_record* in, int64_t n, DevR
   r.pdf_u = static_cast<float>(g.pdf_u);
   r.c = static_cast<float>(g.c);
   r.target = static_cast<float>(g.target);
-  r.flags = REC_VALID | (g.on_neumann ? REC_ON_NEUMANN : 0u);
-  r.prev = -1;
+  r.flags = REC_WRITTEN | (g.on_neumann ? REC_ON_NEUMANN : 0u);
+  r.walk = -1;
   r.key = Pcg::mix(0x696d706f7274ULL ^ Pcg::mix(static_cast<uint64_t>(i)));
   out[i] = r;
 }

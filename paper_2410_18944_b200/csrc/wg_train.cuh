@@ -55,8 +55,9 @@ cudaError_t launch_compact(const DevRecord* recs, const unsigned long long* rec_
                            int64_t capacity, TrainCtl* ctl, TrainTotals* totals, uint32_t* lists,
                            int64_t list_cap, int64_t max_records, int32_t minibatch,
                            cudaStream_t st);
-cudaError_t launch_count_records(DevRecord* recs, int64_t n, double pdf_floor, TrainCtl* ctl,
-                                 cudaStream_t st);
+cudaError_t launch_finalize_records(DevRecord* recs, const unsigned long long* rec_count,
+                                    int64_t capacity, const double* est, const int32_t* esc,
+                                    double pdf_floor, TrainCtl* ctl, cudaStream_t st);
 size_t grad_tile_smem();
 cudaError_t launch_grad_cuda_core(const TrainArgs& a, cudaStream_t st);
 cudaError_t launch_adam_prep(AdamCtl* ctl, const float* count_slot, double b1, double b2,
@@ -67,32 +68,5 @@ cudaError_t launch_import_records(const wg_guide_record* in, int64_t n, DevRecor
                                   cudaStream_t st);
 cudaError_t launch_export_records(const DevRecord* in, int64_t n, wg_guide_record* out,
                                   unsigned long long* count, cudaStream_t st);
-
-// shared backfill (backfill_targets_append, proj/src/guide_train.cpp:58-79):
-// reverse suffix scan over a finished walk's record chain; also counts the
-// walk's records into the round's usable / low-pdf totals
-__device__ __forceinline__ void backfill_chain(DevRecord* recs, int last, double terminal,
-                                               double pdf_floor, TrainCtl* ctl) {
-  double un = terminal;
-  unsigned usable = 0, low = 0;
-  for (int i = last; i >= 0;) {
-    DevRecord& r = recs[i];
-    r.target = static_cast<float>(fabs(un));
-    r.flags |= REC_VALID;
-    if (static_cast<double>(r.pdf_mis) < pdf_floor) {
-      ++low;
-    } else {
-      ++usable;
-      r.flags |= REC_USABLE;
-    }
-    un = static_cast<double>(r.rr) * (static_cast<double>(r.local) + static_cast<double>(r.mult) * un);
-    i = r.prev;
-  }
-  if (ctl) {
-    if (usable) atomicAdd(&ctl->usable, static_cast<unsigned long long>(usable));
-    if (low) atomicAdd(&ctl->low_pdf, static_cast<unsigned long long>(low));
-    atomicAdd(&ctl->seen, static_cast<unsigned long long>(usable + low));
-  }
-}
 
 }  // namespace wg

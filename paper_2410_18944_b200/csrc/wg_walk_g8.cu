@@ -282,9 +282,7 @@ __global__ void __launch_bounds__(256) walk_kernel_g8(WalkArgs a) {
       if (a.steps) a.steps[slot] = w.depth;
       atomicAdd(&a.counters[0], static_cast<unsigned long long>(w.depth));
       if (escaped) atomicAdd(&a.counters[1], 1ull);
-      if (collect && !escaped && w.rec_ok) {  // backfill, guide_train.cpp:58-79
-        backfill_chain(a.recs, w.last_rec, terminal, a.pdf_floor, a.ctl);
-      }
+      (void)terminal;  // targets are formed later from (est, P, Q): see DevRecord
     }
     w.alive = false;
   };
@@ -455,11 +453,13 @@ __global__ void __launch_bounds__(256) walk_kernel_g8(WalkArgs a) {
       r.pdf_u = static_cast<float>(pu);
       r.c = static_cast<float>(m.c);
       r.target = 0.0f;
-      r.local = static_cast<float>(contrib);
-      r.mult = static_cast<float>(mult);
-      r.rr = static_cast<float>(rr);
-      r.prev = w.last_rec;
-      r.flags = w.on_n ? REC_ON_NEUMANN : 0u;
+      r.acc_p = static_cast<float>(w.acc);
+      r.thr_q = static_cast<float>(w.T * mult);
+      r.pad_ = 0.0f;
+      r.walk = static_cast<int32_t>(static_cast<int64_t>(w.round) * a.n_points + w.point);
+      r.flags = REC_WRITTEN | (w.on_n ? REC_ON_NEUMANN : 0u);
+      (void)rr;
+      (void)contrib;
       r.key = Pcg::mix(a.key_seed ^ Pcg::mix((static_cast<uint64_t>(a.point_offset + w.point) << 20) ^
                                              static_cast<uint64_t>(w.depth)));
       a.recs[rec] = r;

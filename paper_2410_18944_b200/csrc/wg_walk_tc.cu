@@ -43,9 +43,8 @@ __device__ __forceinline__ void t_finish(TLane& w, const WalkArgs& a, bool escap
   if (a.steps) a.steps[slot] = w.depth;
   atomicAdd(&a.counters[0], static_cast<unsigned long long>(w.depth));
   if (escaped) atomicAdd(&a.counters[1], 1ull);
-  if (collect && !escaped && w.rec_ok) {  // backfill_targets_append, guide_train.cpp:58-79
-    backfill_chain(a.recs, w.last_rec, terminal, a.pdf_floor, a.ctl);
-  }
+  (void)terminal;  // targets are formed later from (est, P, Q): see DevRecord
+  (void)collect;
   w.alive = false;
 }
 
@@ -278,11 +277,11 @@ __global__ void __launch_bounds__(128) walk_kernel_tc(WalkArgs a) {
       r.pdf_u = static_cast<float>(o.pu);
       r.c = static_cast<float>(sel);
       r.target = 0.0f;
-      r.local = static_cast<float>(w.contrib);
-      r.mult = static_cast<float>(mult);
-      r.rr = static_cast<float>(w.rr);
-      r.prev = w.last_rec;
-      r.flags = w.on_n ? REC_ON_NEUMANN : 0u;
+      r.acc_p = static_cast<float>(w.acc);
+      r.thr_q = static_cast<float>(w.T * mult);
+      r.pad_ = 0.0f;
+      r.walk = static_cast<int32_t>(static_cast<int64_t>(w.round) * a.n_points + w.point);
+      r.flags = REC_WRITTEN | (w.on_n ? REC_ON_NEUMANN : 0u);
       r.key = Pcg::mix(a.key_seed ^ Pcg::mix((static_cast<uint64_t>(a.point_offset + w.point) << 20) ^
                                              static_cast<uint64_t>(w.depth)));
       a.recs[w.rec] = r;
