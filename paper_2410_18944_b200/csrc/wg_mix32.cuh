@@ -17,11 +17,11 @@
 namespace wg {
 
 struct Mix32 {
-  // mean directions stay fp64: a sampled direction inherits |mu|, and a step
-  // of length R along a direction with |nu| = 1 + 6e-8 (fp32 normalisation)
-  // overshoots a Dirichlet wall on the bbox edge by more than the 1e-9 diag
-  // escape pad (wost.cpp:259-263)
-  double mux[8], muy[8];
+  // fp32 mean directions; a SAMPLED direction is renormalised in fp64 (a step
+  // of length R along |nu| = 1 + 6e-8 would overshoot a Dirichlet wall on the
+  // bbox edge by more than the 1e-9 diag escape pad, wost.cpp:259-263). The
+  // density evaluates the same promoted mu, so sampler and pdf stay consistent.
+  float mux[8], muy[8];
   float kappa[8], lambda[8];
   float lne[8];  // log normaliser + kappa: v_i = exp(kappa_i (t_i - 1) + lne_i)
   float c;
@@ -58,12 +58,12 @@ WG_D void normalize32(const float* raw, Mix32& m) {
   const float iz = 1.0f / z;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    double x = raw[2 * i], y = raw[2 * i + 1];
-    double n = sqrt(x * x + y * y);
-    if (n < 1e-12) {  // fallback_mu, sphdist.cpp:274-278
-      double a = kTwoPi * i / kMaxK;
-      m.mux[i] = cos(a);
-      m.muy[i] = sin(a);
+    float x = raw[2 * i], y = raw[2 * i + 1];
+    float n = sqrtf(x * x + y * y);
+    if (n < 1e-12f) {  // fallback_mu, sphdist.cpp:274-278
+      float a = static_cast<float>(kTwoPi * i / kMaxK);
+      m.mux[i] = cosf(a);
+      m.muy[i] = sinf(a);
     } else {
       m.mux[i] = x / n;
       m.muy[i] = y / n;
@@ -117,7 +117,7 @@ WG_D double vm_angle_stable(Pcg& rng, double kappa) {
 WG_D void mixture_sample32(Pcg& rng, const Mix32& m, double* ox, double* oy) {
   double u = rng.uni();
   float acc = 0.0f;
-  double mux = m.mux[7], muy = m.muy[7];
+  float mux = m.mux[7], muy = m.muy[7];
   float kap = m.kappa[7];
   bool found = false;
 #pragma unroll
@@ -132,8 +132,10 @@ WG_D void mixture_sample32(Pcg& rng, const Mix32& m, double* ox, double* oy) {
   }
   double th = vm_angle_stable(rng, kap);
   double c = cos(th), s = sin(th);
-  *ox = c * mux - s * muy;
-  *oy = c * muy + s * mux;
+  double dx = c * mux - s * muy, dy = c * muy + s * mux;
+  double inv = 1.0 / sqrt(dx * dx + dy * dy);  // exact unit length (see Mix32)
+  *ox = dx * inv;
+  *oy = dy * inv;
 }
 
 WG_D void reflected_sample32(Pcg& rng, const Mix32& m, double px, double py, double* ox, double* oy) {
