@@ -1,9 +1,452 @@
-// tcgen05 (5th-generation tensor core) version of the training tile: placeholder
-// until the UMMA kernel lands; the runtime falls back to nothing — callers
-// select WG_MLP_EXACT explicitly when this reports unavailable.
+// Training tile on the 5th-generation tensor cores: forward, KL / selection
+// loss gradient, backward and weight gradients for 128 records per tile
+// (eval_with_tape + kl_grad + selection_grad + backward,
+// proj/src/guide_field.cpp:223-315, proj/src/guide_train.cpp:25-56).
+//
+// One CTA = 128 threads = 128 records = one M = 128 UMMA tile; persistent over
+// the minibatch's tiles. Per tile (all operands split fp16 hi/lo, three MMAs
+// per K-block, fp32 accumulation in TMEM):
+//   F1  H1 = relu(X W1 + b1)            A = X  (K-major)      -> TMEM c0
+//   F2  H2 = relu(H1 W2 + b2)           A = H1                -> c64
+//   F3  Y  = H2 W3 + b3                 A = H2                -> c128
+//       dY = dL/dY per record (fp64 mixture / selection gradient, CUDA cores)
+//   G3  dH2 = dY W3^T . [H2 > 0]        A = dY, B = W3        -> c0
+//       dW3|db3 += [H2|1]^T dY          A = H2 tile read MN-major, B = dY MN-major -> cW3
+//   G2  dH1 = dH2 W2^T . [H1 > 0]                             -> c64
+//       dW2|db2 += [H1|1]^T dH2                               -> cW2
+//   G1  dX  = dH1 W1^T                                        -> c128
+//       dW1|db1 += [X|1]^T dH1                                -> cW1
+// The activation tiles written K-major for the forward are read again,
+// MN-major, as the A / B operands of the weight-gradient GEMMs (the UMMA
+// descriptor only swaps LBO / SBO); a column of ones appended to X, H1 and H2
+// makes row 16 / 64 of each weight-gradient product the bias gradient. Each
+// tensor gets a tile-wide power-of-two scale (exact, undone in the epilogue)
+// so the fp16 split keeps ~22 bits. Weight / bias gradients leave TMEM once per
+// tile by atomics; dX goes to the grid corners by atomics.
+#include "wg_loss.cuh"
+#include "wg_mlp_tc.cuh"
 #include "wg_train.cuh"
 
 namespace wg {
-bool tc_grad_available() { return false; }
-cudaError_t launch_grad_tc(const TrainArgs&, cudaStream_t) { return cudaErrorNotSupported; }
+
+namespace {
+
+constexpr int TM = 128;
+constexpr int KX = 24, KH = 72, KY = 48;  // padded K extents of X|1, H|1, dY
+constexpr uint32_t AX = KX * TM * 2, AH = KH * TM * 2, AY = KY * TM * 2;
+constexpr uint32_t BW1 = 64 * 16 * 2, BW2 = 64 * 64 * 2, BW3F = 48 * 64 * 2, BW3B = 64 * 48 * 2,
+                   BW1B = 16 * 64 * 2;
+// shared-memory carve-up (bytes)
+constexpr uint32_t S_XH = 0, S_XL = S_XH + AX;
+constexpr uint32_t S_H1H = S_XL + AX, S_H1L = S_H1H + AH;  // H1, later dH1
+constexpr uint32_t S_H2H = S_H1L + AH, S_H2L = S_H2H + AH;  // H2, later dH2
+constexpr uint32_t S_YH = S_H2L + AH, S_YL = S_YH + AY;     // dY
+constexpr uint32_t S_B1H = S_YL + AY, S_B1L = S_B1H + BW1;  // forward weights
+constexpr uint32_t S_B2H = S_B1L + BW1, S_B2L = S_B2H + BW2;
+constexpr uint32_t S_B3H = S_B2L + BW2, S_B3L = S_B3H + BW3F;
+constexpr uint32_t S_C3H = S_B3L + BW3F, S_C3L = S_C3H + BW3B;  // backward weights
+constexpr uint32_t S_C2H = S_C3L + BW3B, S_C2L = S_C2H + BW2;
+constexpr uint32_t S_C1H = S_C2L + BW2, S_C1L = S_C1H + BW1B;
+constexpr uint32_t S_BIAS = S_C1L + BW1B;            // b1 64, b2 64, b3 48
+constexpr uint32_t S_MAX = S_BIAS + (64 + 64 + 48) * 4;  // 8 x u32 tile maxima
+constexpr uint32_t S_BAR = S_MAX + 32;
+constexpr uint32_t S_TMEM = S_BAR + 8;
+constexpr uint32_t SMEM_BYTES = S_TMEM + 8;
+// TMEM columns
+constexpr uint32_t C0 = 0, C64 = 64, C128 = 128, CW3 = 192, CW2 = 256, CW1 = 320;
+
+__device__ __forceinline__ uint64_t desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | ((static_cast<uint64_t>(lbo >> 4) & 0x3FFFull) << 16) |
+         ((static_cast<uint64_t>(sbo >> 4) & 0x3FFFull) << 32) | (1ull << 46);
+}
+
+// kind::f16, fp32 accumulate; a_mn / b_mn select MN-major operands
+__device__ __forceinline__ uint32_t idesc(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | (static_cast<uint32_t>(a_mn) << 15) | (static_cast<uint32_t>(b_mn) << 16) |
+         (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+// split fp16 store of K values into row `row` of a K-major tile (K multiple of 8)
+template <int K>
+__device__ __forceinline__ void put_row(unsigned char* sm, uint32_t hi_off, uint32_t lo_off, int row,
+                                        const float* v) {
+#pragma unroll
+  for (int c = 0; c < K / 8; ++c) {
+    __half2 hi[4], lo[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 x = make_float2(v[8 * c + 2 * i], v[8 * c + 2 * i + 1]);
+      hi[i] = __float22half2_rn(x);
+      float2 b = __half22float2(hi[i]);
+      lo[i] = __float22half2_rn(make_float2(x.x - b.x, x.y - b.y));
+    }
+    uint32_t o = umma::kmajor_off(row, 8 * c, K);
+    *reinterpret_cast<uint4*>(sm + hi_off + o) = *reinterpret_cast<uint4*>(hi);
+    *reinterpret_cast<uint4*>(sm + lo_off + o) = *reinterpret_cast<uint4*>(lo);
+  }
+}
+
+// tile-wide max |v| -> power-of-two scale bringing it to [2^9, 2^10)
+__device__ __forceinline__ float tile_scale(unsigned char* sm, int slot, const float* v, int n,
+                                            float& inv) {
+  float m = 0.0f;
+  for (int i = 0; i < n; ++i) m = fmaxf(m, fabsf(v[i]));
+  // positive floats order like their bit patterns
+  atomicMax(reinterpret_cast<unsigned*>(sm + S_MAX) + slot, __float_as_uint(m));
+  __syncthreads();
+  float tm = __uint_as_float(reinterpret_cast<volatile unsigned*>(sm + S_MAX)[slot]);
+  int e = 0;
+  frexpf(tm, &e);
+  if (tm == 0.0f) e = 0;
+  inv = ldexpf(1.0f, e - 10);
+  return ldexpf(1.0f, 10 - e);
+}
+
+// one A x B^T product into TMEM: K/16 K-steps x 3 split terms
+__device__ __forceinline__ void gemm(uint32_t tmem_d, uint32_t a_hi, uint32_t a_lo, uint32_t a_lbo,
+                                     uint32_t a_sbo, uint32_t a_step, uint32_t b_hi, uint32_t b_lo,
+                                     uint32_t b_lbo, uint32_t b_sbo, uint32_t b_step, int ksteps,
+                                     uint32_t id, bool accumulate) {
+  for (int k = 0; k < ksteps; ++k) {
+    uint64_t ah = desc(a_hi + k * a_step, a_lbo, a_sbo), al = desc(a_lo + k * a_step, a_lbo, a_sbo);
+    uint64_t bh = desc(b_hi + k * b_step, b_lbo, b_sbo), bl = desc(b_lo + k * b_step, b_lbo, b_sbo);
+    umma::mma_f16(tmem_d, ah, bh, id, (accumulate || k > 0) ? 1u : 0u);
+    umma::mma_f16(tmem_d, al, bh, id, 1u);
+    umma::mma_f16(tmem_d, ah, bl, id, 1u);
+  }
+}
+
+__device__ __forceinline__ void wait_mma(unsigned char* sm, uint32_t& phase) {
+  umma::mbar_wait(reinterpret_cast<uint64_t*>(sm + S_BAR), phase);
+  phase ^= 1u;
+  umma::fence_after();
+}
+
+__device__ __forceinline__ void publish_smem() {
+  umma::fence_async_smem();
+  umma::fence_before();
+  __syncthreads();
+}
+
+template <int NC>
+__device__ __forceinline__ void ld_row(uint32_t taddr, float* v) {
+#pragma unroll
+  for (int c = 0; c < NC / 16; ++c) {
+    float a[16];
+    umma::ld_x16(taddr + 16 * c, a);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[16 * c + i] = a[i];
+  }
+}
+
+// weight-gradient rows leave TMEM: rows [0, nrow) -> grad[w + i * ldw + j],
+// row `bias_row` -> grad[b + j]; only warps holding those lanes load
+template <int NC>
+__device__ __forceinline__ void flush_dw(uint32_t trow, int row, int nrow, int bias_row, int ncol,
+                                         float inv_w, float inv_b, float* grad, int w, int ldw, int b) {
+  const int warp = threadIdx.x >> 5;
+  if (warp * 32 > bias_row) return;  // warp-uniform: no lanes of interest
+  float v[NC];
+  ld_row<NC>(trow, v);
+  if (row < nrow) {
+    for (int j = 0; j < ncol; ++j) atomicAdd(grad + w + row * ldw + j, v[j] * inv_w);
+  } else if (row == bias_row) {
+    for (int j = 0; j < ncol; ++j) atomicAdd(grad + b + j, v[j] * inv_b);
+  }
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(128, 1) grad_tc_kernel(TrainArgs a) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  const FieldView& f = a.f;
+  const int t = threadIdx.x, warp = t >> 5;
+  const int64_t count = static_cast<int64_t>(min(*a.count, static_cast<unsigned long long>(a.list_cap)));
+  const int64_t tiles = (count + TM - 1) / TM;
+  if (static_cast<int64_t>(blockIdx.x) >= tiles) return;
+  if (blockIdx.x == 0 && t == 0) a.grad[a.n_params] = static_cast<float>(count);
+
+  // ---- stage weights (split fp16) and biases
+  {
+    const float* p = f.p;
+    auto put = [&](uint32_t hi, uint32_t lo, int n, int k, int K, float v) {
+      __half h = __float2half_rn(v), l = __float2half_rn(v - __half2float(h));
+      uint32_t o = umma::kmajor_off(n, k, K);
+      *reinterpret_cast<__half*>(sm + hi + o) = h;
+      *reinterpret_cast<__half*>(sm + lo + o) = l;
+    };
+    for (int e = t; e < 64 * 16; e += TM) {  // B1[n][k] = W1[k][n]
+      int n = e % 64, k = e / 64;
+      put(S_B1H, S_B1L, n, k, 16, p[f.w1 + k * 64 + n]);
+    }
+    for (int e = t; e < 64 * 64; e += TM) {  // B2[n][k] = W2[k][n]; C2[n][k] = W2[n][k]
+      int n = e % 64, k = e / 64;
+      put(S_B2H, S_B2L, n, k, 64, p[f.w2 + k * 64 + n]);
+      put(S_C2H, S_C2L, k, n, 64, p[f.w2 + k * 64 + n]);
+    }
+    for (int e = t; e < 48 * 64; e += TM) {  // B3[n][k] = W3[k][n] (n < 33)
+      int n = e % 48, k = e / 48;
+      float w = n < 33 ? p[f.w3 + k * 33 + n] : 0.0f;
+      put(S_B3H, S_B3L, n, k, 64, w);
+      put(S_C3H, S_C3L, k, n, 48, w);  // C3[n=i][k=j] = W3[i][j]
+    }
+    for (int e = t; e < 16 * 64; e += TM) {  // C1[n=i][k=j] = W1[i][j]
+      int n = e / 64, k = e % 64;
+      put(S_C1H, S_C1L, n, k, 64, p[f.w1 + n * 64 + k]);
+    }
+    float* bias = reinterpret_cast<float*>(sm + S_BIAS);
+    for (int i = t; i < 64; i += TM) {
+      bias[i] = p[f.b1 + i];
+      bias[64 + i] = p[f.b2 + i];
+    }
+    for (int i = t; i < 48; i += TM) bias[128 + i] = i < 33 ? p[f.b3 + i] : 0.0f;
+  }
+  if (warp == 0) umma::tmem_alloc(reinterpret_cast<uint32_t*>(sm + S_TMEM), 512);
+  if (t == 0) umma::mbar_init(reinterpret_cast<uint64_t*>(sm + S_BAR), 1);
+  publish_smem();
+  umma::fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(sm + S_TMEM);
+  const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  const uint32_t base = umma::smem_u32(sm);
+  const float* bias = reinterpret_cast<const float*>(sm + S_BIAS);
+  uint32_t phase = 0;
+  unsigned consumed = 0, skipped = 0;
+
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    if (t < 8) reinterpret_cast<unsigned*>(sm + S_MAX)[t] = 0u;
+    __syncthreads();
+    const int64_t ri = tile * TM + t;
+    const bool live = ri < count;
+    DevRecord r{};
+    if (live) r = a.recs[a.list[ri]];
+    // ---- gather (guide_field.cpp:80-123), corners kept for the scatter
+    float x[16];
+    int cidx[16];
+    float cw[16];
+    {
+      double ex = f.bbox[2] - f.bbox[0], ey = f.bbox[3] - f.bbox[1];
+      float u = static_cast<float>(sclamp((static_cast<double>(r.x) - f.bbox[0]) / ex, 0.0, 1.0));
+      float v = static_cast<float>(sclamp((static_cast<double>(r.y) - f.bbox[1]) / ey, 0.0, 1.0));
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        int res = f.res[l];
+        float px = u * static_cast<float>(res - 1), py = v * static_cast<float>(res - 1);
+        int ix = imin(static_cast<int>(px), res - 2), iy = imin(static_cast<int>(py), res - 2);
+        float fx = px - ix, fy = py - iy;
+        int c00 = f.lvl_off[l] + (iy * res + ix) * 4;
+        cidx[4 * l] = c00;
+        cidx[4 * l + 1] = c00 + 4;
+        cidx[4 * l + 2] = c00 + res * 4;
+        cidx[4 * l + 3] = c00 + res * 4 + 4;
+        cw[4 * l] = (1.0f - fx) * (1.0f - fy);
+        cw[4 * l + 1] = fx * (1.0f - fy);
+        cw[4 * l + 2] = (1.0f - fx) * fy;
+        cw[4 * l + 3] = fx * fy;
+        float4 e0 = __ldg(reinterpret_cast<const float4*>(f.p + cidx[4 * l]));
+        float4 e1 = __ldg(reinterpret_cast<const float4*>(f.p + cidx[4 * l + 1]));
+        float4 e2 = __ldg(reinterpret_cast<const float4*>(f.p + cidx[4 * l + 2]));
+        float4 e3 = __ldg(reinterpret_cast<const float4*>(f.p + cidx[4 * l + 3]));
+        x[4 * l + 0] = cw[4 * l] * e0.x + cw[4 * l + 1] * e1.x + cw[4 * l + 2] * e2.x + cw[4 * l + 3] * e3.x;
+        x[4 * l + 1] = cw[4 * l] * e0.y + cw[4 * l + 1] * e1.y + cw[4 * l + 2] * e2.y + cw[4 * l + 3] * e3.y;
+        x[4 * l + 2] = cw[4 * l] * e0.z + cw[4 * l + 1] * e1.z + cw[4 * l + 2] * e2.z + cw[4 * l + 3] * e3.z;
+        x[4 * l + 3] = cw[4 * l] * e0.w + cw[4 * l + 1] * e1.w + cw[4 * l + 2] * e2.w + cw[4 * l + 3] * e3.w;
+      }
+      if (!live)
+        for (int i = 0; i < 16; ++i) x[i] = 0.0f;
+    }
+    float inv_x, inv_h1, inv_h2, inv_dy, inv_d2, inv_d1;
+    float row[KH];
+    // ---- X | 1
+    {
+      float s = tile_scale(sm, 0, x, 16, inv_x);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) row[i] = x[i] * s;
+      row[16] = live ? 1.0f : 0.0f;
+#pragma unroll
+      for (int i = 17; i < KX; ++i) row[i] = 0.0f;
+      put_row<KX>(sm, S_XH, S_XL, t, row);
+    }
+    publish_smem();
+    if (t == 0) {  // F1: [128 x 24(16 used)] x W1 -> c0
+      umma::fence_after();
+      gemm(tmem + C0, base + S_XH, base + S_XL, 128, (KX / 8) * 128, 256, base + S_B1H, base + S_B1L,
+           128, 256, 256, 1, idesc(128, 64, 0, 0), false);
+      umma::commit(reinterpret_cast<uint64_t*>(sm + S_BAR));
+    }
+    wait_mma(sm, phase);
+    uint64_t mask1 = 0, mask2 = 0;
+    {
+      float h[64];
+      ld_row<64>(trow + C0, h);
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        float z = h[i] * inv_x + bias[i];
+        h[i] = z > 0.0f ? z : 0.0f;
+        if (z > 0.0f) mask1 |= 1ull << i;
+      }
+      float s = tile_scale(sm, 1, h, 64, inv_h1);
+#pragma unroll
+      for (int i = 0; i < 64; ++i) row[i] = h[i] * s;
+      row[64] = live ? 1.0f : 0.0f;
+#pragma unroll
+      for (int i = 65; i < KH; ++i) row[i] = 0.0f;
+      put_row<KH>(sm, S_H1H, S_H1L, t, row);
+    }
+    publish_smem();
+    if (t == 0) {  // F2 -> c64
+      umma::fence_after();
+      gemm(tmem + C64, base + S_H1H, base + S_H1L, 128, (KH / 8) * 128, 256, base + S_B2H, base + S_B2L,
+           128, 1024, 256, 4, idesc(128, 64, 0, 0), false);
+      umma::commit(reinterpret_cast<uint64_t*>(sm + S_BAR));
+    }
+    wait_mma(sm, phase);
+    {
+      float h[64];
+      ld_row<64>(trow + C64, h);
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        float z = h[i] * inv_h1 + bias[64 + i];
+        h[i] = z > 0.0f ? z : 0.0f;
+        if (z > 0.0f) mask2 |= 1ull << i;
+      }
+      float s = tile_scale(sm, 2, h, 64, inv_h2);
+#pragma unroll
+      for (int i = 0; i < 64; ++i) row[i] = h[i] * s;
+      row[64] = live ? 1.0f : 0.0f;
+#pragma unroll
+      for (int i = 65; i < KH; ++i) row[i] = 0.0f;
+      put_row<KH>(sm, S_H2H, S_H2L, t, row);
+    }
+    publish_smem();
+    if (t == 0) {  // F3 -> c128 (N = 48)
+      umma::fence_after();
+      gemm(tmem + C128, base + S_H2H, base + S_H2L, 128, (KH / 8) * 128, 256, base + S_B3H, base + S_B3L,
+           128, 1024, 256, 4, idesc(128, 48, 0, 0), false);
+      umma::commit(reinterpret_cast<uint64_t*>(sm + S_BAR));
+    }
+    wait_mma(sm, phase);
+    // ---- loss gradient at the raw outputs (fp64)
+    {
+      float y[48];
+      ld_row<48>(trow + C128, y);
+#pragma unroll
+      for (int j = 0; j < 33; ++j) y[j] = y[j] * inv_h2 + bias[128 + j];
+      float dy[33];
+      bool used = live && record_dy<8>(y, r, a, dy);
+      if (used) ++consumed;
+      else if (live) ++skipped;
+#pragma unroll
+      for (int j = 0; j < 48; ++j) row[j] = (used && j < 33) ? dy[j] : 0.0f;
+      float s = tile_scale(sm, 3, row, 33, inv_dy);
+#pragma unroll
+      for (int j = 0; j < 48; ++j) row[j] *= s;
+      put_row<KY>(sm, S_YH, S_YL, t, row);
+    }
+    publish_smem();
+    if (t == 0) {  // G3: dH2 -> c0 ; dW3 | db3 -> cW3
+      umma::fence_after();
+      gemm(tmem + C0, base + S_YH, base + S_YL, 128, (KY / 8) * 128, 256, base + S_C3H, base + S_C3L,
+           128, (KY / 8) * 128, 256, 3, idesc(128, 64, 0, 0), false);
+      gemm(tmem + CW3, base + S_H2H, base + S_H2L, (KH / 8) * 128, 128, 2 * (KH / 8) * 128,
+           base + S_YH, base + S_YL, (KY / 8) * 128, 128, 2 * (KY / 8) * 128, 8,
+           idesc(128, 48, 1, 1), false);
+      umma::commit(reinterpret_cast<uint64_t*>(sm + S_BAR));
+    }
+    wait_mma(sm, phase);
+    flush_dw<48>(trow + CW3, t, 64, 64, 33, inv_h2 * inv_dy, inv_dy, a.grad, f.w3, 33, f.b3);
+    {
+      float d[64];
+      ld_row<64>(trow + C0, d);
+#pragma unroll
+      for (int i = 0; i < 64; ++i) d[i] = (mask2 >> i & 1ull) ? d[i] * inv_dy : 0.0f;
+      float s = tile_scale(sm, 4, d, 64, inv_d2);
+#pragma unroll
+      for (int i = 0; i < 64; ++i) row[i] = d[i] * s;
+#pragma unroll
+      for (int i = 64; i < KH; ++i) row[i] = 0.0f;
+      put_row<KH>(sm, S_H2H, S_H2L, t, row);  // dH2 replaces H2
+    }
+    publish_smem();
+    if (t == 0) {  // G2: dH1 -> c64 ; dW2 | db2 -> cW2
+      umma::fence_after();
+      gemm(tmem + C64, base + S_H2H, base + S_H2L, 128, (KH / 8) * 128, 256, base + S_C2H, base + S_C2L,
+           128, 1024, 256, 4, idesc(128, 64, 0, 0), false);
+      gemm(tmem + CW2, base + S_H1H, base + S_H1L, (KH / 8) * 128, 128, 2 * (KH / 8) * 128,
+           base + S_H2H, base + S_H2L, (KH / 8) * 128, 128, 2 * (KH / 8) * 128, 8,
+           idesc(128, 64, 1, 1), false);
+      umma::commit(reinterpret_cast<uint64_t*>(sm + S_BAR));
+    }
+    wait_mma(sm, phase);
+    flush_dw<64>(trow + CW2, t, 64, 64, 64, inv_h1 * inv_d2, inv_d2, a.grad, f.w2, 64, f.b2);
+    {
+      float d[64];
+      ld_row<64>(trow + C64, d);
+#pragma unroll
+      for (int i = 0; i < 64; ++i) d[i] = (mask1 >> i & 1ull) ? d[i] * inv_d2 : 0.0f;
+      float s = tile_scale(sm, 5, d, 64, inv_d1);
+#pragma unroll
+      for (int i = 0; i < 64; ++i) row[i] = d[i] * s;
+#pragma unroll
+      for (int i = 64; i < KH; ++i) row[i] = 0.0f;
+      put_row<KH>(sm, S_H1H, S_H1L, t, row);  // dH1 replaces H1
+    }
+    publish_smem();
+    if (t == 0) {  // G1: dX -> c128 (N = 16) ; dW1 | db1 -> cW1
+      umma::fence_after();
+      gemm(tmem + C128, base + S_H1H, base + S_H1L, 128, (KH / 8) * 128, 256, base + S_C1H, base + S_C1L,
+           128, 1024, 256, 4, idesc(128, 16, 0, 0), false);
+      gemm(tmem + CW1, base + S_XH, base + S_XL, (KX / 8) * 128, 128, 2 * (KX / 8) * 128,
+           base + S_H1H, base + S_H1L, (KH / 8) * 128, 128, 2 * (KH / 8) * 128, 8,
+           idesc(128, 64, 1, 1), false);
+      umma::commit(reinterpret_cast<uint64_t*>(sm + S_BAR));
+    }
+    wait_mma(sm, phase);
+    flush_dw<64>(trow + CW1, t, 16, 16, 64, inv_x * inv_d1, inv_d1, a.grad, f.w1, 64, f.b1);
+    {
+      float dx[16];
+      ld_row<16>(trow + C128, dx);
+      if (live) {  // grid corners (guide_field.cpp:305-314)
+#pragma unroll
+        for (int l = 0; l < 4; ++l)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              atomicAdd(a.grad + cidx[4 * l + c] + q, cw[4 * l + c] * dx[4 * l + q] * inv_d1);
+      }
+    }
+    umma::fence_before();
+    __syncthreads();  // TMEM / smem reuse by the next tile
+  }
+  unsigned c = consumed, sk = skipped;
+  for (int o = 16; o > 0; o >>= 1) {
+    c += __shfl_down_sync(0xffffffffu, c, o);
+    sk += __shfl_down_sync(0xffffffffu, sk, o);
+  }
+  if ((t & 31) == 0) {
+    if (c) atomicAdd(&a.totals->consumed, static_cast<unsigned long long>(c));
+    if (sk) atomicAdd(&a.totals->skipped_v, static_cast<unsigned long long>(sk));
+  }
+  __syncthreads();
+  if (warp == 0) {
+    umma::fence_after();
+    umma::tmem_dealloc(tmem, 512);
+  }
+}
+
+bool tc_grad_available() { return true; }
+
+cudaError_t launch_grad_tc(const TrainArgs& a, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(grad_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(SMEM_BYTES));
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t tiles = (a.list_cap + TM - 1) / TM;
+  int blocks = static_cast<int>(tiles < sms ? tiles : sms);
+  grad_tc_kernel<<<blocks, TM, SMEM_BYTES, st>>>(a);
+  return cudaGetLastError();
+}
+
 }  // namespace wg
