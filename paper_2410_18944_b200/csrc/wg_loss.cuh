@@ -4,6 +4,7 @@
 // Shared by the CUDA-core and the tcgen05 training tiles.
 #pragma once
 
+#include "wg_mix32.cuh"
 #include "wg_sphdist.cuh"
 #include "wg_train.cuh"
 
@@ -85,5 +86,82 @@ WG_D bool record_dy(const float* raw, const DevRecord& r, const TrainArgs& a, fl
   return true;
 }
 
+
+
+// fp32 variant for the tensor-core training tile: same formulas, per-component
+// math in fp32 with the vMF exponent formed as kappa (t - 1) + lne (Mix32) and
+// I1/I0 by rational approximation; sampling-time quantities (target, pdf_mis,
+// pdf_u) come from the record.
+__device__ __forceinline__ float mix_grad_one32(const Mix32& m, const float* raw, const float* inv_mn,
+                                                const bool* kap_free, float nx, float ny, float* g) {
+  float v[8], t[8];
+  float val = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    t[i] = nx * m.mux[i] + ny * m.muy[i];
+    v[i] = __expf(m.kappa[i] * (t[i] - 1.0f) + m.lne[i]);
+    val += m.lambda[i] * v[i];
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float lv = m.lambda[i] * v[i];
+    g[24 + i] += lv - m.lambda[i] * val;
+    if (kap_free[i]) g[16 + i] += lv * (t[i] - i1_over_i0_f(m.kappa[i])) * m.kappa[i];
+    const float s = lv * m.kappa[i] * inv_mn[i];
+    g[2 * i] += (nx - m.mux[i] * t[i]) * s;
+    g[2 * i + 1] += (ny - m.muy[i] * t[i]) * s;
+  }
+  return val;
+}
+
+__device__ __forceinline__ bool record_dy32(const float* raw, const DevRecord& r, const TrainArgs& a,
+                                            float* dy) {
+  float g[33];
+#pragma unroll
+  for (int j = 0; j < 33; ++j) g[j] = 0.0f;
+  Mix32 m;
+  normalize32(raw, m);
+  float inv_mn[8];
+  bool kap_free[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float mx = raw[2 * i], my = raw[2 * i + 1];
+    const float mn = sqrtf(mx * mx + my * my);
+    inv_mn[i] = mn >= 1e-12f ? 1.0f / mn : 0.0f;  // zero-norm means get no mu gradient
+    const float ku = __expf(raw[16 + i]);
+    kap_free[i] = ku > static_cast<float>(kKappaMin) && ku < static_cast<float>(kKappaMax);
+  }
+  const bool on_n = (r.flags & REC_ON_NEUMANN) != 0;
+  const float nx = r.nux, ny = r.nuy, px = r.nx, py = r.ny;
+  const float target = r.target;
+  if (target != 0.0f) {  // kl_grad, guide_train.cpp:25-42
+    float dv[33];
+#pragma unroll
+    for (int j = 0; j < 33; ++j) dv[j] = 0.0f;
+    float v = mix_grad_one32(m, raw, inv_mn, kap_free, nx, ny, dv);
+    if (on_n && a.reflect) {
+      const float d = 2.0f * (nx * px + ny * py);
+      v += mix_grad_one32(m, raw, inv_mn, kap_free, nx - px * d, ny - py * d, dv);
+    }
+    if (!(static_cast<double>(v) > a.v_floor)) return false;
+    const float s = -target / (r.pdf_mis * v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) g[j] = s * dv[j];
+  }
+  if (a.learn_selection) {  // selection_grad, guide_train.cpp:44-56
+    double pg = on_n ? (a.reflect ? reflected_pdf32(m, nx, ny, px, py) : mixture_pdf32(m, nx, ny))
+                     : mixture_pdf32(m, nx, ny);
+    const double c = m.c, pu = r.pdf_u;
+    const double pnow = c * pg + (1.0 - c) * pu;
+    if (pnow > 0.0) {
+      const double dc = -a.e_fraction * target * (pg - pu) / (pnow * static_cast<double>(r.pdf_mis));
+      g[32] = static_cast<float>(dc * c * (1.0 - c));
+    }
+  }
+  const float ic = static_cast<float>(a.inv_count);
+#pragma unroll
+  for (int j = 0; j < 33; ++j) dy[j] = g[j] * ic;
+  return true;
+}
 
 }  // namespace wg

@@ -42,6 +42,26 @@ WG_D float log_i0e(float x) {
   return __logf(p) - 0.5f * __logf(x);
 }
 
+// I1(x) / I0(x) for x >= 0 (A&S 9.8.1-9.8.4; the e^x / sqrt(x) factors
+// cancel above 3.75), relative error < 3e-7
+WG_D float i1_over_i0_f(float x) {
+  if (x < 3.75f) {
+    float t = x * (1.0f / 3.75f);
+    t *= t;
+    float p0 = 1.0f + t * (3.5156229f + t * (3.0899424f + t * (1.2067492f + t * (0.2659732f +
+               t * (0.0360768f + t * 0.0045813f)))));
+    float p1 = 0.5f + t * (0.87890594f + t * (0.51498869f + t * (0.15084934f + t * (0.02658733f +
+               t * (0.00301532f + t * 0.00032411f)))));
+    return x * p1 / p0;
+  }
+  float t = 3.75f / x;
+  float q0 = 0.39894228f + t * (0.01328592f + t * (0.00225319f + t * (-0.00157565f + t * (0.00916281f +
+             t * (-0.02057706f + t * (0.02635537f + t * (-0.01647633f + t * 0.00392377f)))))));
+  float q1 = 0.39894228f + t * (-0.03988024f + t * (-0.00362018f + t * (0.00163801f + t * (-0.01031555f +
+             t * (0.02282967f + t * (-0.02895312f + t * (0.01787654f + t * -0.00420059f)))))));
+  return q1 / q0;
+}
+
 // normalize_params (sphdist.cpp:287-310) for K = 8, dim 2, from fp32 MLP outputs
 WG_D void normalize32(const float* raw, Mix32& m) {
   float cr = raw[32];

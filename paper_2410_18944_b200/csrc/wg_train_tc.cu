@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(128, 1) grad_tc_kernel(TrainArgs a) {
 #pragma unroll
       for (int j = 0; j < 33; ++j) y[j] = y[j] * inv_h2 + bias[128 + j];
       float dy[33];
-      bool used = live && record_dy<8>(y, r, a, dy);
+      bool used = live && record_dy32(y, r, a, dy);
       if (used) ++consumed;
       else if (live) ++skipped;
 #pragma unroll
