@@ -34,3 +34,10 @@ clean:
 	rm -rf build $(PKG)/libwostgpu.so
 
 .PHONY: all oracle clean
+
+# diagnostic build: per-sub-phase clock64 totals of the tensor-core walk kernel
+# (overwrites the library; rebuild with `make` afterwards)
+subprof: $(OBJ)
+	$(NVCC) $(NVFLAGS) -fmad=true -DWG_SUBPROF -c $(PKG)/csrc/wg_walk_tc.cu -o build/wg_walk_tc_sub.o
+	$(NVCC) $(ARCH) -shared -o $(PKG)/libwostgpu.so $(filter-out build/wg_walk_tc.o,$(OBJ)) build/wg_walk_tc_sub.o -lcudart -ldl
+.PHONY: subprof

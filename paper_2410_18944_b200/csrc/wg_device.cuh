@@ -194,13 +194,16 @@ WG_D CP closest_point(const SceneView& s, double x, double y, unsigned kinds) {
 }
 
 // Accel::closest_silhouette (geom2d.cpp:182-200). The result is the minimum
-// over candidate vertices, so any visiting order gives the same value.
+// over candidate vertices, so any visiting order gives the same value; the
+// scan compares squared distances and takes one sqrt at the end, which is the
+// same value (a correctly rounded sqrt is monotone, so min and sqrt commute).
 WG_D double closest_silhouette(const SceneView& s, double x, double y) {
   double best = dinf();
+#pragma unroll 2
   for (int v = 0; v < s.n_sil; ++v) {
     const SilVertex sv = s.sil[v];
     double dx = sv.px - x, dy = sv.py - y;
-    double d = sqrt(dx * dx + dy * dy);
+    double d = dx * dx + dy * dy;
     if (d >= best) continue;
     bool cand = sv.n_count < 2;
     if (!cand) {
@@ -215,7 +218,7 @@ WG_D double closest_silhouette(const SceneView& s, double x, double y) {
     }
     if (cand) best = d;
   }
-  return best;
+  return best == dinf() ? best : sqrt(best);
 }
 
 // slab test, geom2d.cpp:55-76

@@ -102,6 +102,7 @@ cudaError_t launch_walks_g8(const WalkArgs& a, int blocks, cudaStream_t st);
 // tcgen05 MLP walk kernel / field evaluation (wg_walk_tc.cu)
 int walk_tc_smem(const WalkArgs& a);
 int walk_tc_blocks_per_sm(int smem);
+int walk_tc_block();
 cudaError_t launch_walks_tc(const WalkArgs& a, int blocks, cudaStream_t st);
 cudaError_t launch_field_eval_tc(const FieldView& f, int64_t n, const double* xy, double* out,
                                  int sm_count, cudaStream_t st);

@@ -24,6 +24,7 @@ struct Mix32 {
   float mux[8], muy[8];
   float kappa[8], lambda[8];
   float lne[8];  // log normaliser + kappa: v_i = exp(kappa_i (t_i - 1) + lne_i)
+  float hk[8];   // kappa_i / (2 + |mu_i|^2 - 1): see mixture_pdf32
   float c;
 };
 
@@ -40,6 +41,20 @@ WG_D float log_i0e(float x) {
   float p = 0.39894228f + t * (0.01328592f + t * (0.00225319f + t * (-0.00157565f + t * (0.00916281f +
             t * (-0.02057706f + t * (0.02635537f + t * (-0.01647633f + t * 0.00392377f)))))));
   return __logf(p) - 0.5f * __logf(x);
+}
+
+// branch-free log_i0e: both rational forms, one select (lets the unrolled
+// lobes interleave instead of serialising divergent branches)
+WG_D float log_i0e_nb(float x) {
+  float t = x * (1.0f / 3.75f);
+  t *= t;
+  const float p = 1.0f + t * (3.5156229f + t * (3.0899424f + t * (1.2067492f + t * (0.2659732f +
+                  t * (0.0360768f + t * 0.0045813f)))));
+  const float u = __fdividef(3.75f, fmaxf(x, 3.75f));
+  const float q = 0.39894228f + u * (0.01328592f + u * (0.00225319f + u * (-0.00157565f + u * (0.00916281f +
+                  u * (-0.02057706f + u * (0.02635537f + u * (-0.01647633f + u * 0.00392377f)))))));
+  const bool lo = x < 3.75f;
+  return __logf(lo ? p : q) - (lo ? x : 0.5f * __logf(x));
 }
 
 // I1(x) / I0(x) for x >= 0 (A&S 9.8.1-9.8.4; the e^x / sqrt(x) factors
@@ -62,10 +77,28 @@ WG_D float i1_over_i0_f(float x) {
   return q1 / q0;
 }
 
-// normalize_params (sphdist.cpp:287-310) for K = 8, dim 2, from fp32 MLP outputs
+// fallback_mu directions (cos, sin)(2 pi i / 8) (sphdist.cpp:274-278)
+// (indexed with unrolled constants, so the tables fold into immediates)
+WG_D float fallback_cos(int i) {
+  const float t[8] = {1.0f, 0.707106769f, 6.12323426e-17f, -0.707106769f,
+                      -1.0f, -0.707106769f, -1.83697015e-16f, 0.707106769f};
+  return t[i];
+}
+WG_D float fallback_sin(int i) {
+  const float t[8] = {0.0f, 0.707106769f, 1.0f, 0.707106769f,
+                      1.22464685e-16f, -0.707106769f, -1.0f, -0.707106769f};
+  return t[i];
+}
+
+// normalize_params (sphdist.cpp:287-310) for K = 8, dim 2, from fp32 MLP
+// outputs. Branch-free so the eight lobes interleave: log I0 evaluates both
+// A&S forms and selects, the unit vector uses rsqrt (|mu| = 1 to 1 ulp; the
+// sampler renormalises its output in fp64 and the density uses |nu - mu|).
 WG_D void normalize32(const float* raw, Mix32& m) {
-  float cr = raw[32];
-  m.c = cr >= 0.0f ? 1.0f / (1.0f + __expf(-cr)) : __expf(cr) / (1.0f + __expf(cr));
+  const float cr = raw[32];
+  const float ec = __expf(-fabsf(cr));  // sigmoid without overflow
+  const float sg = 1.0f / (1.0f + ec);
+  m.c = cr >= 0.0f ? sg : ec * sg;
   float mx = raw[24];
 #pragma unroll
   for (int i = 1; i < 8; ++i) mx = fmaxf(mx, raw[24 + i]);
@@ -75,34 +108,41 @@ WG_D void normalize32(const float* raw, Mix32& m) {
     e[i] = __expf(raw[24 + i] - mx);
     z += e[i];
   }
-  const float iz = 1.0f / z;
+  const float iz = __frcp_rn(z);
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    float x = raw[2 * i], y = raw[2 * i + 1];
-    float n = sqrtf(x * x + y * y);
-    if (n < 1e-12f) {  // fallback_mu, sphdist.cpp:274-278
-      float a = static_cast<float>(kTwoPi * i / kMaxK);
-      m.mux[i] = cosf(a);
-      m.muy[i] = sinf(a);
-    } else {
-      m.mux[i] = x / n;
-      m.muy[i] = y / n;
-    }
-    float k = fminf(fmaxf(__expf(raw[16 + i]), 1e-6f), 1e4f);
+    const float x = raw[2 * i], y = raw[2 * i + 1];
+    const float n2 = x * x + y * y;
+    const float r = rsqrtf(n2);
+    // fallback_mu (sphdist.cpp:274-278) for |mu| < 1e-12
+    const bool fb = !(n2 >= 1e-24f);
+    m.mux[i] = fb ? fallback_cos(i) : x * r;
+    m.muy[i] = fb ? fallback_sin(i) : y * r;
+    const float k = fminf(fmaxf(__expf(raw[16 + i]), 1e-6f), 1e4f);
     m.kappa[i] = k;
+    const float eps = fmaf(m.mux[i], m.mux[i], fmaf(m.muy[i], m.muy[i], -1.0f));  // |mu|^2 - 1
+    m.hk[i] = __fdividef(k, 2.0f + eps);
     m.lambda[i] = e[i] * iz;
-    m.lne[i] = -log_i0e(k) - 1.8378770664093453f;  // - log(2 pi)
+    m.lne[i] = -log_i0e_nb(k) - 1.8378770664093453f;  // - log(2 pi)
   }
 }
 
-// mixture_pdf (sphdist.cpp:176-185)
+// mixture_pdf (sphdist.cpp:176-185) of the lobes around mu_i / |mu_i| (the
+// directions the sampler draws around). For unit nu and |mu|^2 = 1 + eps,
+// kappa (nu.mu^ - 1) = -kappa |nu - mu|^2 / (2 + eps) exactly: no
+// cancellation near the mode, so the exponent is formed in fp32 with full
+// relative accuracy; nu enters as an fp32 hi + lo pair, so nu - mu is exact
+// to fp32 rounding even for concentrated lobes (fx - mu is Sterbenz-exact).
 WG_D double mixture_pdf32(const Mix32& m, double nx, double ny) {
+  const float fx = static_cast<float>(nx), fy = static_cast<float>(ny);
+  const float lx = static_cast<float>(nx - static_cast<double>(fx));
+  const float ly = static_cast<float>(ny - static_cast<double>(fy));
   float s = 0.0f;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    double t = nx * m.mux[i] + ny * m.muy[i];
-    float arg = static_cast<float>(static_cast<double>(m.kappa[i]) * (t - 1.0)) + m.lne[i];
-    s += m.lambda[i] * __expf(arg);
+    const float dx = (fx - m.mux[i]) + lx, dy = (fy - m.muy[i]) + ly;
+    const float arg = fmaf(-m.hk[i], fmaf(dx, dx, dy * dy), m.lne[i]);
+    s = fmaf(m.lambda[i], __expf(arg), s);
   }
   return s;
 }
@@ -114,28 +154,50 @@ WG_D double reflected_pdf32(const Mix32& m, double nx, double ny, double px, dou
   return mixture_pdf32(m, nx, ny) + mixture_pdf32(m, rx, ry);
 }
 
-// Best-Fisher with the cancellation-free rho (fp64)
-WG_D double vm_angle_stable(Pcg& rng, double kappa) {
-  double s = sqrt(1.0 + 4.0 * kappa * kappa);
-  double tau = 1.0 + s;
-  double rho = 2.0 * kappa * tau / ((s + 1.0) * (tau + sqrt(2.0 * tau)));
-  double r = (1.0 + rho * rho) / (2.0 * rho);
+// Best-Fisher (sphdist.cpp:120-140) in fp32, returning the sampled angle as
+// (cos th, sin th) directly. Every quantity that the reference forms by
+// cancellation is rewritten exactly:
+//   r - 1 = (1 - rho)^2 / (2 rho),  1 - z = 2 sin^2(pi u1 / 2),
+//   r - f = (r - 1)(r + 1) / (r + z),  1 - f = (r - 1)(1 - z) / (r + z),
+// so cv = kappa (r - f) and sin th = sqrt((1 - f)(1 + f)) keep full fp32
+// relative accuracy for concentrated lobes (kappa up to 1e4), and no acos /
+// cos / sin is needed (cos(acos f) = f). The envelope test is exact for any
+// r > 1, so fp32 rounding of rho only changes the acceptance rate. Same
+// three uniforms per accepted proposal (u1, u2, u3) as the reference.
+WG_D void vm_cos_sin(Pcg& rng, float kappa, float* oc, float* os) {
+  const float s = sqrtf(fmaf(4.0f * kappa, kappa, 1.0f));
+  const float tau = 1.0f + s;
+  const float rho = __fdividef(2.0f * kappa * tau, (s + 1.0f) * (tau + sqrtf(2.0f * tau)));
+  const float rm1 = __fdividef((1.0f - rho) * (1.0f - rho), 2.0f * rho);  // r - 1 > 0
+  const float r = 1.0f + rm1;
   for (;;) {
-    double u1 = rng.uni_pos();
-    double z = cos(kPi * u1);
-    double f = (1.0 + r * z) / (r + z);
-    double cv = kappa * (r - f);
-    double u2 = rng.uni_pos();
-    if (cv * (2.0 - cv) - u2 > 0.0 || log(cv / u2) + 1.0 - cv >= 0.0) {
-      double u3 = rng.uni();
-      double th = acos(sclamp(f, -1.0, 1.0));
-      return u3 < 0.5 ? -th : th;
+    const float u1 = static_cast<float>(rng.uni_pos());
+    const float h = sinpif(0.5f * u1);
+    const float omz = 2.0f * h * h;  // 1 - z
+    const float inv = __frcp_rn(r + 1.0f - omz);  // 1 / (r + z)
+    const float cv = kappa * rm1 * (r + 1.0f) * inv;
+    const float omf = rm1 * omz * inv;  // 1 - f
+    const float u2 = static_cast<float>(rng.uni_pos());
+    if (cv * (2.0f - cv) - u2 > 0.0f || __logf(__fdividef(cv, u2)) + 1.0f - cv >= 0.0f) {
+      const float u3 = static_cast<float>(rng.uni());
+      const float sn = sqrtf(fmaxf(omf * (2.0f - omf), 0.0f));
+      *oc = fminf(fmaxf(1.0f - omf, -1.0f), 1.0f);
+      *os = u3 < 0.5f ? -sn : sn;
+      return;
     }
   }
 }
 
+// unit fp32 direction -> fp64 with |nu| = 1 to fp64 rounding (see Mix32)
+WG_D void unit64(float x, float y, double* ox, double* oy) {
+  const double dx = x, dy = y;
+  const double inv = rsqrt(dx * dx + dy * dy);
+  *ox = dx * inv;
+  *oy = dy * inv;
+}
+
 WG_D void mixture_sample32(Pcg& rng, const Mix32& m, double* ox, double* oy) {
-  double u = rng.uni();
+  const float u = static_cast<float>(rng.uni());
   float acc = 0.0f;
   float mux = m.mux[7], muy = m.muy[7];
   float kap = m.kappa[7];
@@ -150,12 +212,9 @@ WG_D void mixture_sample32(Pcg& rng, const Mix32& m, double* ox, double* oy) {
       kap = m.kappa[i];
     }
   }
-  double th = vm_angle_stable(rng, kap);
-  double c = cos(th), s = sin(th);
-  double dx = c * mux - s * muy, dy = c * muy + s * mux;
-  double inv = 1.0 / sqrt(dx * dx + dy * dy);  // exact unit length (see Mix32)
-  *ox = dx * inv;
-  *oy = dy * inv;
+  float c, sn;
+  vm_cos_sin(rng, kap, &c, &sn);
+  unit64(c * mux - sn * muy, c * muy + sn * mux, ox, oy);
 }
 
 WG_D void reflected_sample32(Pcg& rng, const Mix32& m, double px, double py, double* ox, double* oy) {
@@ -175,6 +234,23 @@ WG_D void reflected_sample32(Pcg& rng, const Mix32& m, double px, double py, dou
   }
 }
 
+// uniform_dir_sample (sphdist.cpp:226-243) with one fp32 sincospi per
+// proposal: full circle, or the hemisphere around the Neumann normal by flipping
+WG_D void uniform_sample32(Pcg& rng, bool on_n, double px, double py, double* ox, double* oy) {
+  for (;;) {
+    float sn, cs;
+    sincospif(2.0f * static_cast<float>(rng.uni()), &sn, &cs);
+    double nx, ny;
+    unit64(cs, sn, &nx, &ny);
+    const double d = on_n ? nx * px + ny * py : 1.0;
+    if (d != 0.0) {
+      *ox = d > 0.0 ? nx : -nx;
+      *oy = d > 0.0 ? ny : -ny;
+      return;
+    }
+  }
+}
+
 // mis_sample (sphdist.cpp:254-270) on the fp32 mixture
 WG_D MisOut mis_sample32(Pcg& rng, const Mix32& m, double c, bool on_n, double px, double py,
                          bool refl) {
@@ -184,7 +260,7 @@ WG_D MisOut mis_sample32(Pcg& rng, const Mix32& m, double c, bool on_n, double p
     if (on_n && refl) reflected_sample32(rng, m, px, py, &o.nx, &o.ny);
     else mixture_sample32(rng, m, &o.nx, &o.ny);
   } else {
-    uniform_sample(rng, on_n, px, py, &o.nx, &o.ny);
+    uniform_sample32(rng, on_n, px, py, &o.nx, &o.ny);
   }
   o.pg = on_n ? (refl ? reflected_pdf32(m, o.nx, o.ny, px, py) : mixture_pdf32(m, o.nx, o.ny))
               : mixture_pdf32(m, o.nx, o.ny);

@@ -166,7 +166,7 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
   if (g8) smem = walk_g8_smem(a);
   if (tc) smem = walk_tc_smem(a);
   const int lanes_per_walk = g8 ? 8 : 1;
-  const int block = g8 ? 256 : 128;
+  const int block = g8 ? 256 : tc ? walk_tc_block() : 128;
   const int per_sm = std::max(1, tc ? walk_tc_blocks_per_sm(smem)
                                     : g8 ? walk_g8_blocks_per_sm(smem)
                                          : walk_blocks_per_sm(dflt, guided && !dflt, smem));
@@ -178,24 +178,25 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
     int blocks = static_cast<int>(std::min<int64_t>(want, (int64_t)per_sm * s->sms));
     static const bool phase_prof = std::getenv("WOSTGPU_PHASE_PROF") != nullptr;
     if (phase_prof && tc) {
-      s->phase_prof.alloc(sizeof(unsigned long long) * 4 * blocks);
-      CK(cudaMemsetAsync(s->phase_prof.p, 0, sizeof(unsigned long long) * 4 * blocks, s->stream));
+      s->phase_prof.alloc(sizeof(unsigned long long) * 8 * blocks);
+      CK(cudaMemsetAsync(s->phase_prof.p, 0, sizeof(unsigned long long) * 8 * blocks, s->stream));
       a.phase_prof = s->phase_prof.as<unsigned long long>();
     }
     CK(cudaEventRecord(pool_event(s->ev_walk, s->n_walk_ev), s->stream));
     if (tc) CKL(launch_walks_tc(a, std::max(1, blocks), s->stream));
     if (phase_prof && tc) {  // diagnostics: cycles per CTA iteration of the slowest CTA
-      std::vector<unsigned long long> h(4 * blocks);
-      CK(cudaMemcpyAsync(h.data(), s->phase_prof.p, sizeof(unsigned long long) * 4 * blocks,
+      std::vector<unsigned long long> h(8 * blocks);
+      CK(cudaMemcpyAsync(h.data(), s->phase_prof.p, sizeof(unsigned long long) * 8 * blocks,
                          cudaMemcpyDeviceToHost, s->stream));
       CK(cudaStreamSynchronize(s->stream));
       int worst = 0;
+      auto tot = [&](int b) { return h[8 * b] + h[8 * b + 1] + h[8 * b + 2]; };
       for (int b = 0; b < blocks; ++b)
-        if (h[4 * b] + h[4 * b + 1] + h[4 * b + 2] > h[4 * worst] + h[4 * worst + 1] + h[4 * worst + 2])
-          worst = b;
-      double it = static_cast<double>(std::max<unsigned long long>(h[4 * worst + 3], 1));
-      std::fprintf(stderr, "[phase] cta %d iters %.0f cycles/iter A %.0f B %.0f C %.0f\n", worst, it,
-                   h[4 * worst] / it, h[4 * worst + 1] / it, h[4 * worst + 2] / it);
+        if (tot(b) > tot(worst)) worst = b;
+      const unsigned long long* q = &h[8 * worst];
+      double it = static_cast<double>(std::max<unsigned long long>(q[3], 1));
+      std::fprintf(stderr, "[phase] cta %d iters %.0f cycles/iter A %.0f B %.0f (gather %.0f prep %.0f mma %.0f) C %.0f\n",
+                   worst, it, q[0] / it, q[1] / it, q[5] / it, q[6] / it, q[4] / it, q[2] / it);
     }
     if (tc) {
     } else if (g8) CKL(launch_walks_g8(a, std::max(1, blocks), s->stream));

@@ -12,10 +12,27 @@
 // Walk state stays in registers; the scene and the split fp16 weights stay in
 // shared memory for the whole launch. Statistics go through the same
 // [round][point] estimate buffer + Welford pass as the other walk kernels.
+#include <cstdio>
+#include <cstdlib>
+
 #include "wg_kernels.cuh"
 #include "wg_train.cuh"
 #include "wg_mix32.cuh"
 #include "wg_mlp_tc.cuh"
+
+// WG_SUBPROF (diagnostic builds only): per-thread clock64 totals of the
+// sub-phases of a step, summed over all walks and printed by the last CTA.
+#ifdef WG_SUBPROF
+__device__ unsigned long long g_sub[16];
+__device__ unsigned int g_sub_done;
+#define SUB_T(v) long long v = clock64()
+#define SUB_ADD(i, t0) (sub[i] += clock64() - (t0))
+#define SUB_CNT(i) (++sub[i])
+#else
+#define SUB_T(v)
+#define SUB_ADD(i, t0)
+#define SUB_CNT(i)
+#endif
 
 namespace wg {
 
@@ -34,6 +51,95 @@ struct TLane {
 };
 
 __host__ __device__ __forceinline__ size_t al16(size_t b) { return (b + 15) & ~size_t(15); }
+
+// Small scenes (the benchmark square has 4 segments): visit every segment in
+// BVH leaf order without the traversal stack. Same per-segment arithmetic as
+// closest_point / ray_first_hit (wg_device.cuh), branch-uniform across the
+// warp (every lane tests the same segment); a one-leaf BVH visits segments in
+// exactly this order, otherwise only exact-distance ties can resolve to a
+// different (equidistant) segment.
+constexpr int kSmallScene = 16;
+
+__device__ __forceinline__ CP cp_small(const SceneView& s, double x, double y, unsigned kinds) {
+  CP best{0.0, 0.0, dinf(), -1};
+  double bd2 = dinf();
+#pragma unroll 4
+  for (int i = 0; i < s.n_segs; ++i) {
+    const Seg g = s.segs[i];
+    if (!((g.kind == WG_DIRICHLET ? 1u : 2u) & kinds)) continue;
+    double ux = g.bx - g.ax, uy = g.by - g.ay;
+    double t = ((x - g.ax) * ux + (y - g.ay) * uy) / (ux * ux + uy * uy);
+    t = sclamp(t, 0.0, 1.0);
+    double px = g.ax + t * ux, py = g.ay + t * uy;
+    double dx = px - x, dy = py - y;
+    double d2 = dx * dx + dy * dy;
+    if (d2 < bd2) {
+      bd2 = d2;
+      best.px = px;
+      best.py = py;
+      best.seg = g.id;
+    }
+  }
+  if (best.seg >= 0) best.d = sqrt(bd2);
+  return best;
+}
+
+__device__ __forceinline__ Hit ray_small(const SceneView& s, double ox, double oy, double dx, double dy,
+                                         double t_max, unsigned kinds, int exclude) {
+  double bt = t_max, bsp = 0.0;
+  int bi = -1;
+#pragma unroll 4
+  for (int i = 0; i < s.n_segs; ++i) {
+    const Seg g = s.segs[i];
+    if (!((g.kind == WG_DIRICHLET ? 1u : 2u) & kinds)) continue;
+    if (g.id == exclude) continue;
+    double ux = g.bx - g.ax, uy = g.by - g.ay;
+    double wx = g.ax - ox, wy = g.ay - oy;
+    double den = dx * uy - dy * ux;
+    if (den == 0.0) continue;
+    double t = (wx * uy - wy * ux) / den;
+    double sp = (wx * dy - wy * dx) / den;
+    if (sp < 0.0 || sp > 1.0) continue;
+    if (t > s.t_eps && t <= bt) {
+      bt = t;
+      bi = i;
+      bsp = sp;
+    }
+  }
+  Hit h;
+  h.seg = -1;
+  h.kind = -1;
+  h.t = dinf();
+  h.px = h.py = h.nx = h.ny = 0.0;
+  if (bi < 0) return h;
+  const Seg g = s.segs[bi];
+  h.t = bt;
+  double ux = g.bx - g.ax, uy = g.by - g.ay;
+  h.px = g.ax + bsp * ux;
+  h.py = g.ay + bsp * uy;
+  double px = -uy, py = ux;
+  double l = sqrt(px * px + py * py);
+  double nx = px / l, ny = py / l;
+  if (nx * dx + ny * dy > 0.0) {
+    nx = -nx;
+    ny = -ny;
+  }
+  h.nx = nx;
+  h.ny = ny;
+  h.seg = g.id;
+  h.kind = g.kind;
+  return h;
+}
+
+__device__ __forceinline__ CP t_closest(const SceneView& s, double x, double y, unsigned kinds) {
+  return s.n_segs <= kSmallScene ? cp_small(s, x, y, kinds) : closest_point(s, x, y, kinds);
+}
+
+__device__ __forceinline__ Hit t_ray(const SceneView& s, double ox, double oy, double dx, double dy,
+                                     double t_max, unsigned kinds, int exclude) {
+  return s.n_segs <= kSmallScene ? ray_small(s, ox, oy, dx, dy, t_max, kinds, exclude)
+                                 : ray_first_hit(s, ox, oy, dx, dy, t_max, kinds, exclude);
+}
 
 __device__ __forceinline__ void t_finish(TLane& w, const WalkArgs& a, bool escaped, double terminal,
                                          bool collect) {
@@ -69,8 +175,12 @@ __device__ double t_greens_radius(double u, double R) {  // wost.cpp:37-65, d = 
 }
 
 // begin_step (wost.cpp:148-216); false when the walk terminated
-__device__ __forceinline__ bool t_begin(TLane& w, const WalkArgs& a, const SceneView& s, bool collect) {
-  CP cd = closest_point(s, w.x, w.y, WG_KIND_DIRICHLET);
+__device__ __forceinline__ bool t_begin(TLane& w, const WalkArgs& a, const SceneView& s, bool collect,
+                                        long long* sub) {
+  (void)sub;
+  SUB_T(t0);
+  CP cd = t_closest(s, w.x, w.y, WG_KIND_DIRICHLET);
+  SUB_ADD(0, t0);
   if (cd.seg >= 0 && cd.d <= a.sp.eps) {
     double g = eval_value(s.values[s.seg_value[cd.seg]], cd.px, cd.py);
     w.acc += w.T * g;
@@ -91,7 +201,10 @@ __device__ __forceinline__ bool t_begin(TLane& w, const WalkArgs& a, const Scene
     w.T /= q;
     w.rr = 1.0 / q;
   }
+  SUB_T(t1);
   double dsil = closest_silhouette(s, w.x, w.y);
+  SUB_ADD(1, t1);
+  SUB_T(t2);
   double dd = cd.seg >= 0 ? cd.d : dinf();
   if (dd == dinf() && dsil == dinf()) {
     atomicOr(&a.counters[4], 1ull);
@@ -102,10 +215,10 @@ __device__ __forceinline__ bool t_begin(TLane& w, const WalkArgs& a, const Scene
   double contrib = 0.0;
   if (!s.source_zero) {
     double dx, dy;
-    uniform_sample(w.rng, w.on_n, w.nx, w.ny, &dx, &dy);
+    uniform_sample32(w.rng, w.on_n, w.nx, w.ny, &dx, &dy);
     double r = t_greens_radius(w.rng.uni(), w.R);
     double yx = w.x + dx * r, yy = w.y + dy * r;
-    Hit h = ray_first_hit(s, w.x, w.y, dx, dy, r, WG_KIND_ALL, -1);
+    Hit h = t_ray(s, w.x, w.y, dx, dy, r, WG_KIND_ALL, -1);
     double wt = h.seg >= 0 ? 0.0 : w.R * w.R / 4.0;
     if (wt != 0.0) {
       double f = 0.0;
@@ -115,8 +228,8 @@ __device__ __forceinline__ bool t_begin(TLane& w, const WalkArgs& a, const Scene
   }
   if (s.has_flux) {
     double dx, dy;
-    uniform_sample(w.rng, w.on_n, w.nx, w.ny, &dx, &dy);
-    Hit h = ray_first_hit(s, w.x, w.y, dx, dy, w.R, WG_KIND_NEUMANN, w.seg);
+    uniform_sample32(w.rng, w.on_n, w.nx, w.ny, &dx, &dy);
+    Hit h = t_ray(s, w.x, w.y, dx, dy, w.R, WG_KIND_NEUMANN, w.seg);
     double add = 0.0;
     if (h.seg >= 0) {
       double hv = eval_value(s.values[s.seg_value[h.seg]], h.px, h.py);
@@ -130,6 +243,7 @@ __device__ __forceinline__ bool t_begin(TLane& w, const WalkArgs& a, const Scene
   }
   w.acc += w.T * contrib;
   w.contrib = contrib;
+  SUB_ADD(2, t2);
   w.rec = -1;
   if (collect && w.rec_ok) {
     if (w.rec_left == 0) {
@@ -152,12 +266,15 @@ __device__ __forceinline__ bool t_begin(TLane& w, const WalkArgs& a, const Scene
 
 }  // namespace
 
-__global__ void __launch_bounds__(128) walk_kernel_tc(WalkArgs a) {
-  extern __shared__ __align__(128) unsigned char smem[];
+// kWarp = false: the CTA's 128 walks share one M = 128 tile and step in
+// lockstep (CTA barrier per step). kWarp = true: every warp runs its own MLP
+// chain (tcw_forward) and advances independently of the other warps.
+template <bool kWarp>
+__device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* smem) {
   unsigned char* tc = smem;  // TcLayout block first (128-B aligned)
   SceneView s = a.scene;
   if (a.scene_smem_bytes > 0) {
-    unsigned char* p = smem + al16(TcLayout::BYTES);
+    unsigned char* p = smem + al16(kWarp ? TcLayoutW::BYTES : TcLayout::BYTES);
     size_t off = 0;
     auto carve = [&](size_t bytes) {
       unsigned char* q = p + off;
@@ -177,8 +294,12 @@ __global__ void __launch_bounds__(128) walk_kernel_tc(WalkArgs a) {
     s.sil = sil;
     s.sil_n = sn;
   }
-  tc_stage_weights(tc, a.field);
-  tc_setup(tc);
+  if (kWarp) {
+    tcw_stage_weights(tc, a.field);
+  } else {
+    tc_stage_weights(tc, a.field);
+    tc_setup(tc);
+  }
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
@@ -197,10 +318,12 @@ __global__ void __launch_bounds__(128) walk_kernel_tc(WalkArgs a) {
   int64_t walks_done = 0;
 
   long long t_iter = a.phase_prof ? clock64() : 0;
+  long long bpa[3] = {0, 0, 0};
+  long long sub[12] = {};
   for (;;) {
     if (a.phase_prof) {  // phase C of the previous iteration ends here
       long long t_top = clock64();
-      if (threadIdx.x == 0) a.phase_prof[4 * blockIdx.x + 2] += static_cast<unsigned long long>(t_top - t_iter);
+      if (threadIdx.x == 0) a.phase_prof[8 * blockIdx.x + 2] += static_cast<unsigned long long>(t_top - t_iter);
       t_iter = t_top;
     }
     // ---- phase A: every slot advances to a walk that needs a direction
@@ -227,19 +350,25 @@ __global__ void __launch_bounds__(128) walk_kernel_tc(WalkArgs a) {
         next += stride;
         ++walks_done;
       }
-      if (t_begin(w, a, s, collect)) {
+      if (t_begin(w, a, s, collect, sub)) {
         need = true;
         break;
       }
     }
-    if (!__syncthreads_or(need)) break;
+    if (kWarp) {
+      if (!__any_sync(0xffffffffu, need)) break;
+    } else {
+      if (!__syncthreads_or(need)) break;
+    }
     long long t_b = a.phase_prof ? clock64() : 0;
     if (a.phase_prof && threadIdx.x == 0) {
-      a.phase_prof[4 * blockIdx.x + 0] += static_cast<unsigned long long>(t_b - t_iter);
-      a.phase_prof[4 * blockIdx.x + 3] += 1;
+      a.phase_prof[8 * blockIdx.x + 0] += static_cast<unsigned long long>(t_b - t_iter);
+      a.phase_prof[8 * blockIdx.x + 3] += 1;
     }
 
     // ---- phase B: guiding-field MLP for the whole tile on the tensor cores
+    SUB_T(tg);
+    long long t_g = a.phase_prof ? clock64() : 0;
     float xin[TcLayout::NIN];
     if (need) {
       tc_gather(fv, w.x, w.y, xin);
@@ -247,23 +376,40 @@ __global__ void __launch_bounds__(128) walk_kernel_tc(WalkArgs a) {
 #pragma unroll
       for (int i = 0; i < TcLayout::NIN; ++i) xin[i] = 0.0f;
     }
+    if (a.phase_prof) t_g = clock64() - t_g;
+    SUB_ADD(3, tg);
+    SUB_T(tb);
     float raw[TcLayout::NO];
-    tc_forward(tc, phase, xin, raw);
+    if (kWarp) tcw_forward(tc, phase, xin, raw, a.phase_prof ? &bpa[0] : nullptr);
+    else tc_forward(tc, phase, xin, raw, a.phase_prof ? bpa : nullptr);
+    if (a.phase_prof && threadIdx.x == 0) {
+      a.phase_prof[8 * blockIdx.x + 4] += static_cast<unsigned long long>(bpa[0]);
+      a.phase_prof[8 * blockIdx.x + 6] += static_cast<unsigned long long>(bpa[1]);
+      a.phase_prof[8 * blockIdx.x + 5] += static_cast<unsigned long long>(t_g);
+    }
+    bpa[0] = bpa[1] = bpa[2] = 0;
     if (a.phase_prof) {
       long long t_c = clock64();
-      if (threadIdx.x == 0) a.phase_prof[4 * blockIdx.x + 1] += static_cast<unsigned long long>(t_c - t_b);
+      if (threadIdx.x == 0) a.phase_prof[8 * blockIdx.x + 1] += static_cast<unsigned long long>(t_c - t_b);
       t_iter = t_c;  // phase C is charged to the next iteration's phase A slot
     }
+    SUB_ADD(4, tb);
     if (!need) continue;
+    SUB_CNT(11);
 
     // ---- phase C: decode + sample + move (wost.cpp:111-146, 218-264)
+    SUB_T(tn);
     Mix32 m;
     normalize32(raw, m);
+    SUB_ADD(5, tn);
+    SUB_T(ts);
     double sel = m.c;
     if (a.sp.mode == WG_MODE_GUIDING_ONLY) sel = 1.0;
     else if (a.sp.mode == WG_MODE_FIXED_MIS) sel = a.sp.fixed_c;
     MisOut o = mis_sample32(w.rng, m, sel, w.on_n, w.nx, w.ny, a.sp.reflect != 0);
     double mult = o.pu / o.pmis;
+    SUB_ADD(6, ts);
+    SUB_T(tr);
     if (w.rec >= 0) {
       DevRecord r;
       r.x = static_cast<float>(w.x);
@@ -287,11 +433,14 @@ __global__ void __launch_bounds__(128) walk_kernel_tc(WalkArgs a) {
       a.recs[w.rec] = r;
       w.last_rec = w.rec;
     }
+    SUB_ADD(7, tr);
     if (mult == 0.0) {
       t_finish(w, a, false, 0.0, collect);
       continue;
     }
-    Hit h = ray_first_hit(s, w.x, w.y, o.nx, o.ny, w.R, WG_KIND_NEUMANN, w.seg);
+    SUB_T(th);
+    Hit h = t_ray(s, w.x, w.y, o.nx, o.ny, w.R, WG_KIND_NEUMANN, w.seg);
+    SUB_ADD(8, th);
     if (h.seg >= 0) {
       w.x = h.px;
       w.y = h.py;
@@ -314,7 +463,35 @@ __global__ void __launch_bounds__(128) walk_kernel_tc(WalkArgs a) {
   unsigned long long wd = static_cast<unsigned long long>(walks_done);
   for (int o = 16; o > 0; o >>= 1) wd += __shfl_down_sync(0xffffffffu, wd, o);
   if ((threadIdx.x & 31) == 0) atomicAdd(&a.counters[2], wd);
-  tc_teardown(tc);
+#ifdef WG_SUBPROF
+  for (int i = 0; i < 12; ++i) atomicAdd(&g_sub[i], static_cast<unsigned long long>(sub[i]));
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&g_sub_done, 1u) == gridDim.x - 1) {
+      __threadfence();
+      double n = static_cast<double>(g_sub[11] > 0 ? g_sub[11] : 1);
+      printf("[sub] steps %.0f cyc/step: cp %.0f sil %.0f begin_rest %.0f gather %.0f mlp %.0f norm %.0f "
+             "sample %.0f rec %.0f ray %.0f\n",
+             n, g_sub[0] / n, g_sub[1] / n, g_sub[2] / n, g_sub[3] / n, g_sub[4] / n, g_sub[5] / n,
+             g_sub[6] / n, g_sub[7] / n, g_sub[8] / n);
+      for (int i = 0; i < 16; ++i) g_sub[i] = 0;
+      g_sub_done = 0;
+    }
+  }
+#endif
+  if (kWarp) tcw_teardown(tc);
+  else tc_teardown(tc);
+}
+
+__global__ void __launch_bounds__(128, 1) walk_kernel_tc(WalkArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  walk_tc_body<false>(a, smem);
+}
+
+__global__ void __launch_bounds__(128) walk_kernel_tcw(WalkArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  walk_tc_body<true>(a, smem);
 }
 
 // GuidingField::eval_batch on the tensor cores: persistent CTAs over 128-point tiles
@@ -341,23 +518,44 @@ __global__ void __launch_bounds__(128) field_eval_tc_kernel(FieldView f, int64_t
   tc_teardown(smem);
 }
 
+// warps per CTA of the warp-independent kernel (0 = lockstep 128-walk CTAs,
+// the default: measured faster on cfg 2, 0.85 vs 1.2 ms per round, because
+// the per-warp M = 128 MMAs quadruple tensor/smem traffic and the waiting
+// warps' mbarrier polling slows the running warps); WOSTGPU_TC_WARPS = 1/2/4
+// selects the warp-independent kernel for experiments
+int walk_tc_warps() {
+  static const int w = [] {
+    const char* e = std::getenv("WOSTGPU_TC_WARPS");
+    int v = e ? std::atoi(e) : 0;
+    return (v == 0 || v == 1 || v == 2 || v == 4) ? v : 0;
+  }();
+  return w;
+}
+
+int walk_tc_block() { return walk_tc_warps() == 0 ? 128 : 32 * walk_tc_warps(); }
+
 int walk_tc_smem(const WalkArgs& a) {
-  return static_cast<int>(al16(TcLayout::BYTES) + (a.scene_smem_bytes > 0 ? al16(a.scene_smem_bytes) : 0));
+  size_t tile = walk_tc_warps() == 0 ? TcLayout::BYTES : TcLayoutW::BYTES;
+  return static_cast<int>(al16(tile) + (a.scene_smem_bytes > 0 ? al16(a.scene_smem_bytes) : 0));
 }
 
 int walk_tc_blocks_per_sm(int smem) {
   int n = 0;
-  cudaFuncSetAttribute(walk_kernel_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, walk_kernel_tc, 128, smem);
-  // 4 x 128 TMEM columns per SM
-  return n < 4 ? n : 4;
+  const int warps = walk_tc_warps();
+  auto k = warps == 0 ? walk_kernel_tc : walk_kernel_tcw;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, walk_tc_block(), smem);
+  // 512 TMEM columns per SM: 128 per lockstep CTA, 64 per warp otherwise
+  const int tmem_cap = warps == 0 ? 4 : 512 / (64 * warps);
+  return n < tmem_cap ? n : tmem_cap;
 }
 
 cudaError_t launch_walks_tc(const WalkArgs& a, int blocks, cudaStream_t st) {
   int smem = walk_tc_smem(a);
-  cudaError_t e = cudaFuncSetAttribute(walk_kernel_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  auto k = walk_tc_warps() == 0 ? walk_kernel_tc : walk_kernel_tcw;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  walk_kernel_tc<<<blocks, 128, smem, st>>>(a);
+  k<<<blocks, walk_tc_block(), smem, st>>>(a);
   return cudaGetLastError();
 }
 
