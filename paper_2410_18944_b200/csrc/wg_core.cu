@@ -471,7 +471,10 @@ int wostgpu_field_set_state(wg_field f, const float* p, const double* m, const d
                             int64_t steps) {
   return guarded([&] {
     CK(cudaDeviceSynchronize());
-    if (p) CK(cudaMemcpy(f->p.p, p, sizeof(float) * f->n_params, cudaMemcpyHostToDevice));
+    if (p) {
+      CK(cudaMemcpy(f->p.p, p, sizeof(float) * f->n_params, cudaMemcpyHostToDevice));
+      f->pack_dirty = true;
+    }
     if (m) CK(cudaMemcpy(f->m.p, m, sizeof(double) * f->n_params, cudaMemcpyHostToDevice));
     if (v) CK(cudaMemcpy(f->v.p, v, sizeof(double) * f->n_params, cudaMemcpyHostToDevice));
     if (steps >= 0) {

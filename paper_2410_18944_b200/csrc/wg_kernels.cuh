@@ -34,7 +34,8 @@ struct __align__(16) DevRecord {
   uint32_t flags;
   uint64_t key;  // deterministic selection key (seed, round, point, depth)
 };
-static_assert(sizeof(DevRecord) == 80, "record layout");
+static_assert(sizeof(DevRecord) == 80 && offsetof(DevRecord, walk) == 56 && offsetof(DevRecord, key) == 64,
+              "record layout (compact_kernel loads walk|flags and key by offset)");
 enum : uint32_t { REC_ON_NEUMANN = 1u, REC_VALID = 2u, REC_USABLE = 4u, REC_WRITTEN = 8u };
 
 struct TrainCtl;  // wg_train.cuh
@@ -67,8 +68,11 @@ struct WalkArgs {
   TrainCtl* ctl;     // round's record counts (collecting rounds)
   // counters: [0] steps, [1] escaped, [2] walks, [3] record overflow, [4] scene error
   unsigned long long* counters;
-  // optional per-CTA phase timing [gridDim][4]: cycles in phase A (begin
-  // step + barrier), B (MLP), C (sample + move), iterations (WOSTGPU_PHASE_PROF)
+  // tensor-core kernel: the field's packed split-fp16 weights (wg_wpack.cuh)
+  const unsigned char* wblob;
+  // optional per-CTA phase timing [gridDim][8]: cycles in phase A (begin
+  // step + barrier), B (MLP), C (sample + move), iterations, MMA windows,
+  // gather, MLP prep (WOSTGPU_PHASE_PROF)
   unsigned long long* phase_prof;
 };
 

@@ -14,6 +14,7 @@
 
 #include "wg_field.cuh"
 #include "wg_umma.cuh"
+#include "wg_wpack.cuh"
 
 namespace wg {
 
@@ -29,10 +30,30 @@ struct TcLayout {
   static constexpr uint32_t B3_LO = B3_HI + NO_PAD * NH * 2;
   static constexpr uint32_t BIAS = B3_LO + NO_PAD * NH * 2;  // 64 + 64 + 48 fp32
   static constexpr uint32_t BAR = BIAS + (NH + NH + NO_PAD) * 4;
-  static constexpr uint32_t TMEM_SLOT = BAR + 8;
+  static constexpr uint32_t BAR_W = BAR + 8;  // weight bulk copy
+  static constexpr uint32_t TMEM_SLOT = BAR + 16;
   static constexpr uint32_t BYTES = TMEM_SLOT + 8;
   static constexpr uint32_t TMEM_COLS = 128;
 };
+// [B1_HI, BAR) is byte-for-byte the forward prefix of the packed blob
+static_assert(TcLayout::B1_HI % 16 == 0 && TcLayout::BAR - TcLayout::B1_HI == wpack::FWD_BYTES,
+              "TcLayout weights must match the packed blob (wg_wpack.cuh)");
+
+// Weights from the field's packed blob: one TMA bulk copy issued by thread 0;
+// every thread waits with tc_wait_weights after the CTA barrier.
+__device__ __forceinline__ void tc_fetch_weights(unsigned char* sm, const unsigned char* blob) {
+  using L = TcLayout;
+  if (threadIdx.x == 0) {
+    uint64_t* wb = reinterpret_cast<uint64_t*>(sm + L::BAR_W);
+    umma::mbar_init(wb, 1);
+    umma::fence_async_smem();
+    umma::mbar_expect_tx(wb, wpack::FWD_BYTES);
+    umma::bulk_g2s(sm + L::B1_HI, blob, wpack::FWD_BYTES, wb);
+  }
+}
+__device__ __forceinline__ void tc_wait_weights(unsigned char* sm) {
+  umma::mbar_wait(reinterpret_cast<uint64_t*>(sm + TcLayout::BAR_W), 0);
+}
 
 
 // Stage B_l = W_l^T as split fp16 in the K-major layout, plus the biases.

@@ -159,4 +159,8 @@ struct wg_field_s {
   wgrt::DBuf p, m, v;
   wgrt::DBuf adam;  // wg::AdamCtl: step count + per-step control, device truth
   wg::FieldView view{};
+  // packed split-fp16 MLP weights (wg_wpack.cuh) for the tensor-core kernels;
+  // dirty after any host write of the parameters, kept current by Adam
+  wgrt::DBuf wpack;
+  bool pack_dirty = true;
 };

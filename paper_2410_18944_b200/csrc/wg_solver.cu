@@ -10,6 +10,7 @@
 #include <cstdlib>
 
 #include "wg_runtime.hpp"
+#include "wg_wpack.cuh"
 
 using namespace wg;
 using namespace wgrt;
@@ -109,6 +110,17 @@ void reset_run(wg_solver_s* s) {
   s->n_walk_ev = s->n_train_ev = 0;
 }
 
+// the field's packed weight blob, repacked on the stream if the host changed
+// the parameters since it was last written
+unsigned char* field_blob(wg_field_s* f, cudaStream_t st) {
+  f->wpack.alloc(wpack::BYTES);
+  if (f->pack_dirty) {
+    CKL(launch_pack_weights(f->view, f->wpack.as<unsigned char>(), st));
+    f->pack_dirty = false;
+  }
+  return f->wpack.as<unsigned char>();
+}
+
 // enqueue solve_batch for `rounds` consecutive wpp indices (no host sync)
 void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t rounds, bool collect,
                     uint64_t key_seed, double pdf_floor) {
@@ -164,7 +176,10 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
   int smem = (s->scene->smem_bytes > 0 ? ((s->scene->smem_bytes + 15) & ~15) : 0) +
              (guided ? ((int)sizeof(float) * s->field->view.mlp_count + 15) / 16 * 16 : 0);
   if (g8) smem = walk_g8_smem(a);
-  if (tc) smem = walk_tc_smem(a);
+  if (tc) {
+    smem = walk_tc_smem(a);
+    a.wblob = field_blob(s->field, s->stream);
+  }
   const int lanes_per_walk = g8 ? 8 : 1;
   const int block = g8 ? 256 : tc ? walk_tc_block() : 128;
   const int per_sm = std::max(1, tc ? walk_tc_blocks_per_sm(smem)
@@ -244,7 +259,10 @@ void enqueue_minibatch(wg_solver_s* s, const wg_train_config& tc, int b, double 
   ta.e_fraction = tc.e_fraction;
   ta.v_floor = tc.v_floor;
   ta.totals = s->totals.as<TrainTotals>();
-  if (s->mlp == WG_MLP_TENSOR && tc_grad_available()) CKL(launch_grad_tc(ta, s->stream));
+  if (s->mlp == WG_MLP_TENSOR && tc_grad_available()) {
+    ta.packed = field_blob(f, s->stream);
+    CKL(launch_grad_tc(ta, s->stream));
+  }
   else CKL(launch_grad_cuda_core(ta, s->stream));
 }
 
@@ -265,13 +283,12 @@ void enqueue_train(wg_solver_s* s, const wg_train_config& tc) {
   AdamCtl* actl = f->adam.as<AdamCtl>();
   for (int b = 0; b < n_mb; ++b) {
     enqueue_minibatch(s, tc, b, 1.0);
-    float* count_slot = s->grad.as<float>() + f->n_params;
     if (s->comm)
       NCK(nccl().allReduce(s->grad.p, s->grad.p, f->n_params + 1, ncclFloat, ncclSum, s->comm,
                         s->stream));
-    CKL(launch_adam_prep(actl, count_slot, tc.beta1, tc.beta2, s->stream));
     CKL(launch_adam(f->p.as<float>(), f->m.as<double>(), f->v.as<double>(), s->grad.as<float>(),
-                    f->n_params, tc.lr, tc.beta1, tc.beta2, tc.eps, actl, s->stream));
+                    f->n_params, tc.lr, tc.beta1, tc.beta2, tc.eps, actl, f->view,
+                    f->wpack.p && !f->pack_dirty ? f->wpack.as<unsigned char>() : nullptr, s->stream));
   }
   CK(cudaEventRecord(pool_event(s->ev_train, s->n_train_ev), s->stream));
 }

@@ -13,6 +13,7 @@
 #include "wg_sphdist.cuh"
 #include "wg_train.cuh"
 #include "wg_loss.cuh"
+#include "wg_wpack.cuh"
 
 namespace wg {
 
@@ -36,15 +37,36 @@ __global__ void compact_kernel(const DevRecord* recs, const unsigned long long* 
     atomicAdd(&totals->seen, ctl->seen);
     atomicAdd(&totals->low_pdf, ctl->low_pdf);
   }
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const DevRecord r = recs[i];
-    if (!(r.flags & REC_VALID) || n_mb == 0) continue;
-    const double u = static_cast<double>(r.key >> 11) * 0x1.0p-53;
-    if (!(u < p) || !(r.flags & REC_USABLE)) continue;
-    int mb = static_cast<int>(u / p * n_mb);
-    mb = mb < n_mb - 1 ? mb : n_mb - 1;
-    unsigned long long slot = atomicAdd(&ctl->mb_count[mb], 1ull);
+  // warp-strided so every lane of a warp takes part in the aggregated slot
+  // allocation; each record contributes one 8-B (walk, flags) and one 8-B key load
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += stride) {
+    const int64_t i = i0 + lane;
+    bool sel = false;
+    int mb = 0;
+    if (i < n && n_mb > 0) {
+      const char* rp = reinterpret_cast<const char*>(recs + i);
+      const uint32_t flags = reinterpret_cast<const uint2*>(rp + 56)->y;
+      if ((flags & (REC_VALID | REC_USABLE)) == (REC_VALID | REC_USABLE)) {
+        const uint64_t key = *reinterpret_cast<const uint64_t*>(rp + 64);
+        const double u = static_cast<double>(key >> 11) * 0x1.0p-53;
+        if (u < p) {
+          sel = true;
+          mb = static_cast<int>(u / p * n_mb);
+          mb = mb < n_mb - 1 ? mb : n_mb - 1;
+        }
+      }
+    }
+    const unsigned act = __ballot_sync(0xffffffffu, sel);
+    if (!sel) continue;
+    // one atomic per (warp, minibatch): lanes with the same minibatch share it
+    const unsigned peers = __match_any_sync(act, mb);
+    const int leader = __ffs(peers) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(&ctl->mb_count[mb], static_cast<unsigned long long>(__popc(peers)));
+    base = __shfl_sync(peers, base, leader);
+    const unsigned long long slot = base + __popc(peers & ((1u << lane) - 1u));
     if (static_cast<int64_t>(slot) < list_cap) lists[mb * list_cap + static_cast<int64_t>(slot)] = static_cast<uint32_t>(i);
     else atomicAdd(&totals->overflow, 1ull);
   }
@@ -336,30 +358,19 @@ cudaError_t launch_grad_cuda_core(const TrainArgs& a, cudaStream_t st) {
 // adam_step (guide_field.cpp:317-331). The minibatch's (global) record count
 // sits in g[n]; a step only happens when it is non-zero, exactly like the
 // reference which never steps on an empty minibatch.
-__global__ void adam_prep_kernel(AdamCtl* c, const float* count_slot, double b1, double b2) {
-  const double cnt = static_cast<double>(*count_slot);
-  if (cnt > 0.0) {
-    c->steps += 1;
-    c->bc1 = 1.0 - pow(b1, static_cast<double>(c->steps));
-    c->bc2 = 1.0 - pow(b2, static_cast<double>(c->steps));
-    c->scale = 1.0 / cnt;
-    c->active = 1;
-    c->norm2[(c->steps - 1) % kNormRing] = 0.0;
-  } else {
-    c->active = 0;
-  }
-}
-
-cudaError_t launch_adam_prep(AdamCtl* ctl, const float* count_slot, double b1, double b2,
-                             cudaStream_t st) {
-  adam_prep_kernel<<<1, 1, 0, st>>>(ctl, count_slot, b1, b2);
-  return cudaGetLastError();
-}
-
-__global__ void adam_kernel(float* p, double* m, double* v, float* g, int64_t n, double lr,
-                            double b1, double b2, double eps, AdamCtl* c) {
-  if (!c->active) return;
-  const double scale = c->scale, bc1 = c->bc1, bc2 = c->bc2;
+// Adam (GuidingField::adam_step, guide_field.cpp:317-331) with fp64 moments
+// and the step control folded in: every block derives the bias corrections
+// from `steps + 1` and the record count g[n]; the last block to finish
+// publishes |g|^2 and advances `steps`.
+__global__ void adam_kernel(float* p, double* m, double* v, const float* g, int64_t n, double lr,
+                            double b1, double b2, double eps, AdamCtl* c, FieldView f,
+                            unsigned char* blob) {
+  const double cnt = static_cast<double>(g[n]);
+  if (!(cnt > 0.0)) return;  // no usable records: no optimizer step
+  const long long step = c->steps + 1;
+  const double bc1 = 1.0 - pow(b1, static_cast<double>(step));
+  const double bc2 = 1.0 - pow(b2, static_cast<double>(step));
+  const double scale = 1.0 / cnt;
   double local = 0.0;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -368,17 +379,55 @@ __global__ void adam_kernel(float* p, double* m, double* v, float* g, int64_t n,
     double mi = m[i] = b1 * m[i] + (1.0 - b1) * gi;
     double vi = v[i] = b2 * v[i] + (1.0 - b2) * gi * gi;
     double up = lr * (mi / bc1) / (sqrt(vi / bc2) + eps);
-    p[i] = static_cast<float>(static_cast<double>(p[i]) - up);
+    const float np = static_cast<float>(static_cast<double>(p[i]) - up);
+    p[i] = np;
+    if (blob != nullptr && i >= f.w1) wpack::pack_param(f, blob, i, np);
   }
+  __shared__ double red[32];
   for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
-  if ((threadIdx.x & 31) == 0) atomicAdd(&c->norm2[(c->steps - 1) % kNormRing], local);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double x = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (threadIdx.x == 0) {
+      atomicAdd(&c->norm_acc, x);
+      __threadfence();
+      if (atomicAdd(&c->done, 1u) == gridDim.x - 1) {  // last block: publish the step
+        __threadfence();
+        c->norm2[(step - 1) % kNormRing] = atomicAdd(&c->norm_acc, 0.0);  // coherent read
+        c->norm_acc = 0.0;
+        c->done = 0u;
+        c->steps = step;
+      }
+    }
+  }
 }
 
-cudaError_t launch_adam(float* p, double* m, double* v, float* g, int64_t n, double lr, double b1,
-                        double b2, double eps, AdamCtl* ctl, cudaStream_t st) {
+cudaError_t launch_adam(float* p, double* m, double* v, const float* g, int64_t n, double lr, double b1,
+                        double b2, double eps, AdamCtl* ctl, const FieldView& f, unsigned char* blob,
+                        cudaStream_t st) {
   int blocks = static_cast<int>((n + 255) / 256);
   if (blocks > 148 * 4) blocks = 148 * 4;
-  adam_kernel<<<blocks, 256, 0, st>>>(p, m, v, g, n, lr, b1, b2, eps, ctl);
+  adam_kernel<<<blocks, 256, 0, st>>>(p, m, v, g, n, lr, b1, b2, eps, ctl, f, blob);
+  return cudaGetLastError();
+}
+
+// the whole packed weight blob (wg_wpack.cuh) from the parameters, including
+// the zero padding of B3 (rows 33..47), C3 (columns 33..47) and b3
+__global__ void pack_weights_kernel(FieldView f, unsigned char* blob) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int64_t i = f.w1 + t; i < static_cast<int64_t>(f.b3) + 33; i += nt) wpack::pack_param(f, blob, i, f.p[i]);
+  for (int e = t; e < 15 * 64; e += nt) {
+    const int n = 33 + e / 64, k = e % 64;
+    wpack::put(blob, wpack::B3H, wpack::B3L, n, k, 64, 0.0f);
+    wpack::put(blob, wpack::C3H, wpack::C3L, k, n, 48, 0.0f);
+  }
+  if (t < 15) reinterpret_cast<float*>(blob + wpack::BIAS)[128 + 33 + t] = 0.0f;
+}
+
+cudaError_t launch_pack_weights(const FieldView& f, unsigned char* blob, cudaStream_t st) {
+  pack_weights_kernel<<<32, 256, 0, st>>>(f, blob);
   return cudaGetLastError();
 }
 

@@ -28,11 +28,14 @@ struct TrainTotals {
   unsigned long long seen, low_pdf, consumed, skipped_v, overflow;
 };
 
-// per-field optimizer control (device truth of GuidingField::adam_steps_)
+// per-field optimizer control (device truth of GuidingField::adam_steps_).
+// adam_kernel reads `steps` when it starts and the last of its blocks to
+// finish advances it, so no separate control launch sits between the
+// gradient and the update.
 struct AdamCtl {
   long long steps;
-  double bc1, bc2, scale;
-  int active;
+  double norm_acc;     // |g|^2 block partials of the running step
+  unsigned int done;   // blocks of the running step that have finished
   int pad;
   double norm2[kNormRing];  // |g|^2 of every step (ring)
 };
@@ -49,6 +52,7 @@ struct TrainArgs {
   int32_t reflect, learn_selection;
   double e_fraction, v_floor;
   TrainTotals* totals;
+  const unsigned char* packed;         // tensor-core tile: split-fp16 weight blob (pack kernel)
 };
 
 cudaError_t launch_compact(const DevRecord* recs, const unsigned long long* rec_count,
@@ -59,11 +63,14 @@ cudaError_t launch_finalize_records(DevRecord* recs, const unsigned long long* r
                                     int64_t capacity, const double* est, const int32_t* esc,
                                     double pdf_floor, TrainCtl* ctl, cudaStream_t st);
 size_t grad_tile_smem();
+size_t grad_tc_pack_bytes();
 cudaError_t launch_grad_cuda_core(const TrainArgs& a, cudaStream_t st);
-cudaError_t launch_adam_prep(AdamCtl* ctl, const float* count_slot, double b1, double b2,
-                             cudaStream_t st);
-cudaError_t launch_adam(float* p, double* m, double* v, float* g, int64_t n, double lr, double b1,
-                        double b2, double eps, AdamCtl* ctl, cudaStream_t st);
+// Adam step on all n parameters with the mean gradient g[0..n) / g[n] (the
+// record count); no step when g[n] == 0. blob != nullptr: the packed weight
+// blob (wg_wpack.cuh) is updated for every MLP parameter written.
+cudaError_t launch_adam(float* p, double* m, double* v, const float* g, int64_t n, double lr, double b1,
+                        double b2, double eps, AdamCtl* ctl, const FieldView& f, unsigned char* blob,
+                        cudaStream_t st);
 cudaError_t launch_import_records(const wg_guide_record* in, int64_t n, DevRecord* out,
                                   cudaStream_t st);
 cudaError_t launch_export_records(const DevRecord* in, int64_t n, wg_guide_record* out,

@@ -22,10 +22,12 @@
 // makes row 16 / 64 of each weight-gradient product the bias gradient. Each
 // tensor gets a tile-wide power-of-two scale (exact, undone in the epilogue)
 // so the fp16 split keeps ~22 bits. Weight / bias gradients leave TMEM once per
-// tile by atomics; dX goes to the grid corners by atomics.
+// tile by atomics; dX goes to the grid corners by atomics. The split weight
+// tiles arrive as the field's packed blob (wg_wpack.cuh) in one bulk copy.
 #include "wg_loss.cuh"
 #include "wg_mlp_tc.cuh"
 #include "wg_train.cuh"
+#include "wg_wpack.cuh"
 
 namespace wg {
 
@@ -34,24 +36,29 @@ namespace {
 constexpr int TM = 128;
 constexpr int KX = 24, KH = 72, KY = 48;  // padded K extents of X|1, H|1, dY
 constexpr uint32_t AX = KX * TM * 2, AH = KH * TM * 2, AY = KY * TM * 2;
-constexpr uint32_t BW1 = 64 * 16 * 2, BW2 = 64 * 64 * 2, BW3F = 48 * 64 * 2, BW3B = 64 * 48 * 2,
-                   BW1B = 16 * 64 * 2;
 // shared-memory carve-up (bytes)
 constexpr uint32_t S_XH = 0, S_XL = S_XH + AX;
 constexpr uint32_t S_H1H = S_XL + AX, S_H1L = S_H1H + AH;  // H1, later dH1
 constexpr uint32_t S_H2H = S_H1L + AH, S_H2L = S_H2H + AH;  // H2, later dH2
 constexpr uint32_t S_YH = S_H2L + AH, S_YL = S_YH + AY;     // dY
-constexpr uint32_t S_B1H = S_YL + AY, S_B1L = S_B1H + BW1;  // forward weights
-constexpr uint32_t S_B2H = S_B1L + BW1, S_B2L = S_B2H + BW2;
-constexpr uint32_t S_B3H = S_B2L + BW2, S_B3L = S_B3H + BW3F;
-constexpr uint32_t S_C3H = S_B3L + BW3F, S_C3L = S_C3H + BW3B;  // backward weights
-constexpr uint32_t S_C2H = S_C3L + BW3B, S_C2L = S_C2H + BW2;
-constexpr uint32_t S_C1H = S_C2L + BW2, S_C1L = S_C1H + BW1B;
-constexpr uint32_t S_BIAS = S_C1L + BW1B;            // b1 64, b2 64, b3 48
-constexpr uint32_t S_MAX = S_BIAS + (64 + 64 + 48) * 4;  // 8 x u32 tile maxima
-constexpr uint32_t S_BAR = S_MAX + 32;
-constexpr uint32_t S_TMEM = S_BAR + 8;
+// the field's packed weight blob (wg_wpack.cuh), one bulk copy
+constexpr uint32_t S_W = S_YL + AY;
+constexpr uint32_t S_B1H = S_W + wpack::B1H, S_B1L = S_W + wpack::B1L;  // forward weights
+constexpr uint32_t S_B2H = S_W + wpack::B2H, S_B2L = S_W + wpack::B2L;
+constexpr uint32_t S_B3H = S_W + wpack::B3H, S_B3L = S_W + wpack::B3L;
+constexpr uint32_t S_BIAS = S_W + wpack::BIAS;                          // b1 64, b2 64, b3 48
+constexpr uint32_t S_C3H = S_W + wpack::C3H, S_C3L = S_W + wpack::C3L;  // backward weights
+constexpr uint32_t S_C2H = S_W + wpack::C2H, S_C2L = S_W + wpack::C2L;
+constexpr uint32_t S_C1H = S_W + wpack::C1H, S_C1L = S_W + wpack::C1L;
+constexpr uint32_t S_MAX = S_W + wpack::BYTES;  // 8 x u32 tile maxima
+constexpr int STG = 65;                                    // staging row stride (floats)
+constexpr uint32_t S_STAGE = S_MAX + 32;                   // 65 x 65 fp32 dW staging
+constexpr uint32_t S_BAR = S_STAGE + (STG * STG * 4 + 15) / 16 * 16;  // mbarrier: 8-B aligned
+constexpr uint32_t S_BAR_W = S_BAR + 8;                     // weight bulk-copy barrier
+constexpr uint32_t S_TMEM = S_BAR_W + 8;
+static_assert(S_W % 16 == 0, "bulk copy destination alignment");
 constexpr uint32_t SMEM_BYTES = S_TMEM + 8;
+static_assert(S_BAR % 8 == 0 && S_STAGE % 16 == 0, "shared-memory carve-up alignment");
 // TMEM columns
 constexpr uint32_t C0 = 0, C64 = 64, C128 = 128, CW3 = 192, CW2 = 256, CW1 = 320;
 
@@ -139,20 +146,37 @@ __device__ __forceinline__ void ld_row(uint32_t taddr, float* v) {
   }
 }
 
-// weight-gradient rows leave TMEM: rows [0, nrow) -> grad[w + i * ldw + j],
-// row `bias_row` -> grad[b + j]; only warps holding those lanes load
+// weight-gradient rows leave TMEM through a shared-memory stage (row stride
+// 65: conflict-free row writes) and then go out as flat, coalesced atomics:
+// the nrow x ncol block is dense in the gradient vector at grad[w], the bias
+// row (TMEM lane `bias_row`) dense at grad[b]. Only warps holding lanes of
+// interest load TMEM (warp-uniform test: tcgen05.ld is warp-collective).
 template <int NC>
-__device__ __forceinline__ void flush_dw(uint32_t trow, int row, int nrow, int bias_row, int ncol,
-                                         float inv_w, float inv_b, float* grad, int w, int ldw, int b) {
+__device__ __forceinline__ void flush_dw(unsigned char* sm, uint32_t trow, int row, int nrow, int bias_row,
+                                         int ncol, float inv_w, float inv_b, float* grad, int w, int b) {
+  float* st = reinterpret_cast<float*>(sm + S_STAGE);
   const int warp = threadIdx.x >> 5;
-  if (warp * 32 > bias_row) return;  // warp-uniform: no lanes of interest
-  float v[NC];
-  ld_row<NC>(trow, v);
-  if (row < nrow) {
-    for (int j = 0; j < ncol; ++j) atomicAdd(grad + w + row * ldw + j, v[j] * inv_w);
-  } else if (row == bias_row) {
-    for (int j = 0; j < ncol; ++j) atomicAdd(grad + b + j, v[j] * inv_b);
+  if (warp * 32 <= bias_row) {
+    float v[NC];
+    ld_row<NC>(trow, v);
+    if (row <= bias_row) {
+      const float sc = row < nrow ? inv_w : inv_b;
+      for (int j = 0; j < ncol; ++j) st[row * STG + j] = v[j] * sc;
+    }
   }
+  __syncthreads();
+  const int nw = nrow * ncol;
+  for (int e = threadIdx.x; e < nw; e += blockDim.x) {
+    const int r = e / ncol;
+    atomicAdd(grad + w + e, st[r * STG + (e - r * ncol)]);
+  }
+  for (int e = threadIdx.x; e < ncol; e += blockDim.x) atomicAdd(grad + b + e, st[bias_row * STG + e]);
+}
+
+// 16-byte vector reduction (the 4 features of one grid corner)
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
 }
 
 }  // namespace
@@ -166,45 +190,19 @@ __global__ void __launch_bounds__(128, 1) grad_tc_kernel(TrainArgs a) {
   if (static_cast<int64_t>(blockIdx.x) >= tiles) return;
   if (blockIdx.x == 0 && t == 0) a.grad[a.n_params] = static_cast<float>(count);
 
-  // ---- stage weights (split fp16) and biases
-  {
-    const float* p = f.p;
-    auto put = [&](uint32_t hi, uint32_t lo, int n, int k, int K, float v) {
-      __half h = __float2half_rn(v), l = __float2half_rn(v - __half2float(h));
-      uint32_t o = umma::kmajor_off(n, k, K);
-      *reinterpret_cast<__half*>(sm + hi + o) = h;
-      *reinterpret_cast<__half*>(sm + lo + o) = l;
-    };
-    for (int e = t; e < 64 * 16; e += TM) {  // B1[n][k] = W1[k][n]
-      int n = e % 64, k = e / 64;
-      put(S_B1H, S_B1L, n, k, 16, p[f.w1 + k * 64 + n]);
-    }
-    for (int e = t; e < 64 * 64; e += TM) {  // B2[n][k] = W2[k][n]; C2[n][k] = W2[n][k]
-      int n = e % 64, k = e / 64;
-      put(S_B2H, S_B2L, n, k, 64, p[f.w2 + k * 64 + n]);
-      put(S_C2H, S_C2L, k, n, 64, p[f.w2 + k * 64 + n]);
-    }
-    for (int e = t; e < 48 * 64; e += TM) {  // B3[n][k] = W3[k][n] (n < 33)
-      int n = e % 48, k = e / 48;
-      float w = n < 33 ? p[f.w3 + k * 33 + n] : 0.0f;
-      put(S_B3H, S_B3L, n, k, 64, w);
-      put(S_C3H, S_C3L, k, n, 48, w);  // C3[n=i][k=j] = W3[i][j]
-    }
-    for (int e = t; e < 16 * 64; e += TM) {  // C1[n=i][k=j] = W1[i][j]
-      int n = e / 64, k = e % 64;
-      put(S_C1H, S_C1L, n, k, 64, p[f.w1 + n * 64 + k]);
-    }
-    float* bias = reinterpret_cast<float*>(sm + S_BIAS);
-    for (int i = t; i < 64; i += TM) {
-      bias[i] = p[f.b1 + i];
-      bias[64 + i] = p[f.b2 + i];
-    }
-    for (int i = t; i < 48; i += TM) bias[128 + i] = i < 33 ? p[f.b3 + i] : 0.0f;
+  // ---- split fp16 weight tiles + biases: one TMA bulk copy of the packed blob
+  if (t == 0) {
+    uint64_t* wb = reinterpret_cast<uint64_t*>(sm + S_BAR_W);
+    umma::mbar_init(wb, 1);
+    umma::fence_async_smem();
+    umma::mbar_expect_tx(wb, wpack::BYTES);
+    umma::bulk_g2s(sm + S_W, a.packed, wpack::BYTES, wb);
   }
   if (warp == 0) umma::tmem_alloc(reinterpret_cast<uint32_t*>(sm + S_TMEM), 512);
   if (t == 0) umma::mbar_init(reinterpret_cast<uint64_t*>(sm + S_BAR), 1);
   publish_smem();
   umma::fence_after();
+  umma::mbar_wait(reinterpret_cast<uint64_t*>(sm + S_BAR_W), 0);  // weights landed
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(sm + S_TMEM);
   const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
   const uint32_t base = umma::smem_u32(sm);
@@ -353,7 +351,7 @@ __global__ void __launch_bounds__(128, 1) grad_tc_kernel(TrainArgs a) {
       umma::commit(reinterpret_cast<uint64_t*>(sm + S_BAR));
     }
     wait_mma(sm, phase);
-    flush_dw<48>(trow + CW3, t, 64, 64, 33, inv_h2 * inv_dy, inv_dy, a.grad, f.w3, 33, f.b3);
+    flush_dw<48>(sm, trow + CW3, t, 64, 64, 33, inv_h2 * inv_dy, inv_dy, a.grad, f.w3, f.b3);
     {
       float d[64];
       ld_row<64>(trow + C0, d);
@@ -377,7 +375,7 @@ __global__ void __launch_bounds__(128, 1) grad_tc_kernel(TrainArgs a) {
       umma::commit(reinterpret_cast<uint64_t*>(sm + S_BAR));
     }
     wait_mma(sm, phase);
-    flush_dw<64>(trow + CW2, t, 64, 64, 64, inv_h1 * inv_d2, inv_d2, a.grad, f.w2, 64, f.b2);
+    flush_dw<64>(sm, trow + CW2, t, 64, 64, 64, inv_h1 * inv_d2, inv_d2, a.grad, f.w2, f.b2);
     {
       float d[64];
       ld_row<64>(trow + C64, d);
@@ -401,7 +399,7 @@ __global__ void __launch_bounds__(128, 1) grad_tc_kernel(TrainArgs a) {
       umma::commit(reinterpret_cast<uint64_t*>(sm + S_BAR));
     }
     wait_mma(sm, phase);
-    flush_dw<64>(trow + CW1, t, 16, 16, 64, inv_x * inv_d1, inv_d1, a.grad, f.w1, 64, f.b1);
+    flush_dw<64>(sm, trow + CW1, t, 16, 16, 64, inv_x * inv_d1, inv_d1, a.grad, f.w1, f.b1);
     {
       float dx[16];
       ld_row<16>(trow + C128, dx);
@@ -409,10 +407,11 @@ __global__ void __launch_bounds__(128, 1) grad_tc_kernel(TrainArgs a) {
 #pragma unroll
         for (int l = 0; l < 4; ++l)
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              atomicAdd(a.grad + cidx[4 * l + c] + q, cw[4 * l + c] * dx[4 * l + q] * inv_d1);
+          for (int c = 0; c < 4; ++c) {
+            const float wc = cw[4 * l + c] * inv_d1;
+            red_add_v4(a.grad + cidx[4 * l + c], wc * dx[4 * l], wc * dx[4 * l + 1], wc * dx[4 * l + 2],
+                       wc * dx[4 * l + 3]);
+          }
       }
     }
     umma::fence_before();
@@ -443,10 +442,13 @@ cudaError_t launch_grad_tc(const TrainArgs& a, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (a.packed == nullptr) return cudaErrorInvalidValue;
   int64_t tiles = (a.list_cap + TM - 1) / TM;
   int blocks = static_cast<int>(tiles < sms ? tiles : sms);
   grad_tc_kernel<<<blocks, TM, SMEM_BYTES, st>>>(a);
   return cudaGetLastError();
 }
+
+size_t grad_tc_pack_bytes() { return wpack::BYTES; }
 
 }  // namespace wg

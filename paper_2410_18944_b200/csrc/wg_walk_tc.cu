@@ -297,12 +297,13 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
   if (kWarp) {
     tcw_stage_weights(tc, a.field);
   } else {
-    tc_stage_weights(tc, a.field);
+    tc_fetch_weights(tc, a.wblob);
     tc_setup(tc);
   }
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
+  if (!kWarp) tc_wait_weights(tc);
 
   const bool collect = a.recs != nullptr;
   const int64_t total = a.n_points * static_cast<int64_t>(a.n_rounds);
