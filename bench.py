@@ -248,11 +248,27 @@ def main():
     peaks, peak_kind = measured_peaks()
     alg_bytes = pr["steps"] * BYTES_PER_STEP + pr["train_steps"] * BYTES_PER_TRAIN_STEP
     achieved = alg_bytes / (pr["walk_ms"] * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "kernel": "walk_kernel", "achieved": achieved,
+    kname = "walk_kernel_tc" if args.mlp == "tensor" else "walk_kernel_g8"
+    rounds = max(1, WPP)
+    roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved,
                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                 "traffic": None, "peak_source": peak_kind,
+                "algorithmic_bytes_per_launch": alg_bytes / rounds,
                 "algorithmic_bytes_per_step": alg_bytes, "walk_ms_per_step": pr["walk_ms"],
                 "train_ms_per_step": pr["train_ms"], "walk_steps_per_step": pr["steps"]}
+    # DRAM / L2 bytes of one launch of the same kernel from the committed ncu
+    # --set full capture (profiles/, tools/ncu_counters.py): the walk state
+    # lives in registers and the records stay in L2, so DRAM traffic is far
+    # below the SoA algorithmic bytes; the kernel is latency-bound
+    ncu_json = os.path.join(ROOT, "profiles", f"ncu_counters_{kname}.json")
+    if os.path.exists(ncu_json):
+        with open(ncu_json) as f:
+            nc = json.load(f)
+        roofline["traffic"] = nc.get("dram_bytes")
+        roofline["traffic_source"] = os.path.relpath(ncu_json, ROOT)
+        roofline["l2_bytes_per_launch"] = nc.get("l2_bytes")
+        roofline["l2_gbs_achieved"] = nc.get("l2_gbs")
+        roofline["tensor_pipe_active_pct"] = nc.get("tensor_pipe_active_pct")
 
     # e2e through the public API with host buffers (points in, statistics out)
     e2e_times = []

@@ -82,13 +82,26 @@ int wostgpu_field_set_state(wg_field field, const float* params, const double* a
 /* GuidingField::eval_batch (guide_field.cpp:178-221, 251-256): row-major
  * [n x output_dim]. mlp = WG_MLP_EXACT reproduces the reference's fp32
  * accumulation order bit for bit (CUDA cores); WG_MLP_TENSOR runs the
- * tcgen05 tensor-core kernel (TF32 inputs, fp32 accumulation). */
+ * tcgen05 tensor-core kernel (fp32 operands split into fp16 hi + lo, three
+ * MMAs per K-step, fp32 accumulation in TMEM: ~1e-6 relative). */
 enum { WG_MLP_EXACT = 0, WG_MLP_TENSOR = 1 };
 int wostgpu_field_eval_batch(wg_field field, int64_t n, const double* xy, double* out, int mlp);
 /* normalize_params(unpack_params(...)) (sphdist.cpp:287-310,
  * guide_field.cpp:424-441) on device for n raw rows */
 int wostgpu_normalize_params(int64_t n, const double* raw, int32_t k, int32_t dim,
                              wg_mixture* out);
+/* Diagnostics of the tensor-core walk path's fp32 mixture math (default
+ * shape: K = 8, dim 2; no reference counterpart, used by the parity tests):
+ * mixture32_pdf decodes raw row i (33 floats) and evaluates the mixture pdf
+ * at nu[i] (unit, fp64): out[2i] = pdf, out[2i+1] = selection probability c;
+ * mixture32_sample draws n directions from the single mixture `raw`, sample
+ * i with its own PCG32 stream (seed, i). */
+/* diagnostic: bytes in which the field's Adam-maintained split-fp16 weight
+ * blob (tensor-core kernels) differs from a fresh pack of its parameters;
+ * -1 when no maintained blob exists yet */
+int wostgpu_field_check_pack(wg_field field, int64_t* mismatched_bytes);
+int wostgpu_mixture32_pdf(int64_t n, const float* raw, const double* nu, double* out);
+int wostgpu_mixture32_sample(const float* raw, int64_t n, uint64_t seed, double* nu_out);
 
 /* ---- solver (solve_batch / Engine) --------------------------------------- */
 /* StepContext{scene, accel, field, cfg} (proj/include/wost/wost.hpp:33-51)

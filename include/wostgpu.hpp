@@ -14,6 +14,9 @@
 #pragma once
 
 #include <cstdint>
+#include <cstring>
+#include <istream>
+#include <ostream>
 #include <optional>
 #include <span>
 #include <stdexcept>
@@ -197,16 +200,22 @@ class Accel {  // geom2d.hpp:38-91, batched on the device
 
 class GuidingField {  // guide_field.hpp:37-96
  public:
-  GuidingField(const FieldConfig& cfg, const Bbox& bbox, uint64_t seed) : cfg_(cfg) {
+  GuidingField(const FieldConfig& cfg, const Bbox& bbox, uint64_t seed) : cfg_(cfg), bbox_(bbox) {
     wg_field_config c = cfg.c();
     double bb[4] = {bbox.min.x, bbox.min.y, bbox.max.x, bbox.max.y};
     check(wostgpu_field_create(&c, bb, seed, &h_));
     check(wostgpu_field_param_count(h_, &n_));
   }
-  ~GuidingField() { wostgpu_field_destroy(h_); }
+  ~GuidingField() {
+    if (h_) wostgpu_field_destroy(h_);
+  }
   GuidingField(const GuidingField&) = delete;
   GuidingField& operator=(const GuidingField&) = delete;
+  GuidingField(GuidingField&& o) noexcept : cfg_(o.cfg_), bbox_(o.bbox_), h_(o.h_), n_(o.n_) {
+    o.h_ = nullptr;
+  }
   const FieldConfig& config() const { return cfg_; }
+  const Bbox& bbox() const { return bbox_; }
   size_t param_count() const { return static_cast<size_t>(n_); }
   std::vector<float> params() const {
     std::vector<float> p(n_);
@@ -224,8 +233,73 @@ class GuidingField {  // guide_field.hpp:37-96
   }
   wg_field handle() const { return h_; }
 
+  // WGF1 checkpoint, byte-compatible with GuidingField::save / load
+  // (guide_field.cpp:333-411): magic, version 1, level count + resolutions,
+  // features, hidden, K, dim (u32), bbox (4 f64), Adam steps (i64), parameter
+  // count (u64), fp32 params, fp64 Adam m, fp64 Adam v
+  void save(std::ostream& out) const {
+    std::vector<float> p(n_);
+    std::vector<double> m(n_), v(n_);
+    int64_t steps = 0;
+    check(wostgpu_field_get_state(h_, p.data(), m.data(), v.data(), &steps));
+    out.write("WGF1", 4);
+    put<uint32_t>(out, 1);
+    put<uint32_t>(out, static_cast<uint32_t>(cfg_.level_res.size()));
+    for (int r : cfg_.level_res) put<uint32_t>(out, static_cast<uint32_t>(r));
+    for (int x : {cfg_.features, cfg_.hidden, cfg_.mixture_k, cfg_.mixture_dim})
+      put<uint32_t>(out, static_cast<uint32_t>(x));
+    for (double x : {bbox_.min.x, bbox_.min.y, bbox_.max.x, bbox_.max.y}) put<double>(out, x);
+    put<int64_t>(out, steps);
+    put<uint64_t>(out, static_cast<uint64_t>(n_));
+    out.write(reinterpret_cast<const char*>(p.data()), static_cast<std::streamsize>(p.size() * 4));
+    out.write(reinterpret_cast<const char*>(m.data()), static_cast<std::streamsize>(m.size() * 8));
+    out.write(reinterpret_cast<const char*>(v.data()), static_cast<std::streamsize>(v.size() * 8));
+  }
+  static GuidingField load(std::istream& in) {
+    char magic[4];
+    in.read(magic, 4);
+    if (!in || std::memcmp(magic, "WGF1", 4) != 0)
+      throw std::runtime_error("guiding field checkpoint: bad magic");
+    if (get<uint32_t>(in) != 1) throw std::runtime_error("guiding field checkpoint: unknown version");
+    FieldConfig cfg;
+    cfg.level_res.resize(get<uint32_t>(in));
+    for (auto& r : cfg.level_res) r = static_cast<int>(get<uint32_t>(in));
+    cfg.features = static_cast<int>(get<uint32_t>(in));
+    cfg.hidden = static_cast<int>(get<uint32_t>(in));
+    cfg.mixture_k = static_cast<int>(get<uint32_t>(in));
+    cfg.mixture_dim = static_cast<int>(get<uint32_t>(in));
+    Bbox bb;
+    bb.min.x = get<double>(in);
+    bb.min.y = get<double>(in);
+    bb.max.x = get<double>(in);
+    bb.max.y = get<double>(in);
+    const int64_t steps = get<int64_t>(in);
+    GuidingField f(cfg, bb, 0);
+    if (get<uint64_t>(in) != static_cast<uint64_t>(f.n_))
+      throw std::runtime_error("guiding field checkpoint: size mismatch");
+    std::vector<float> p(f.n_);
+    std::vector<double> m(f.n_), v(f.n_);
+    in.read(reinterpret_cast<char*>(p.data()), static_cast<std::streamsize>(p.size() * 4));
+    in.read(reinterpret_cast<char*>(m.data()), static_cast<std::streamsize>(m.size() * 8));
+    in.read(reinterpret_cast<char*>(v.data()), static_cast<std::streamsize>(v.size() * 8));
+    if (!in) throw std::runtime_error("guiding field checkpoint: truncated");
+    check(wostgpu_field_set_state(f.h_, p.data(), m.data(), v.data(), steps));
+    return f;
+  }
+
  private:
+  template <typename T>
+  static void put(std::ostream& out, T v) {
+    out.write(reinterpret_cast<const char*>(&v), sizeof(T));
+  }
+  template <typename T>
+  static T get(std::istream& in) {
+    T v{};
+    in.read(reinterpret_cast<char*>(&v), sizeof(T));
+    return v;
+  }
   FieldConfig cfg_;
+  Bbox bbox_;
   wg_field h_ = nullptr;
   int64_t n_ = 0;
 };

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -320,6 +321,93 @@ void ref_field_get_params(void* fp, float* out) {
 void ref_field_set_params(void* fp, const float* in) {
   auto* f = static_cast<GuidingField*>(fp);
   for (size_t i = 0; i < f->param_count(); ++i) f->set_param(i, in[i]);
+}
+// WGF1 checkpoints through the reference's own GuidingField::save / load
+// (proj/src/guide_field.cpp:351-411)
+int ref_field_save(void* fp, const char* path) {
+  return guarded([&] {
+    std::ofstream out(path, std::ios::binary);
+    static_cast<GuidingField*>(fp)->save(out);
+    if (!out) throw std::runtime_error("write failed");
+  });
+}
+void* ref_field_load(const char* path) {
+  GuidingField* f = nullptr;
+  int rc = guarded([&] {
+    std::ifstream in(path, std::ios::binary);
+    f = new GuidingField(GuidingField::load(in));
+  });
+  return rc == WG_OK ? f : nullptr;
+}
+int64_t ref_field_adam_steps(void* fp) { return static_cast<GuidingField*>(fp)->adam_steps(); }
+
+// result formats through the reference's own writers (proj/src/image.cpp,
+// solver.cpp:317-327) for byte-level comparison with the Python harness
+int ref_write_image(int32_t w, int32_t h, const double* bbox, const wg_point_stats* cells,
+                    const char* csv, const char* pfm, const char* png) {
+  return guarded([&] {
+    SolutionImage img = make_image(w, h, Bbox{{bbox[0], bbox[1]}, {bbox[2], bbox[3]}});
+    for (size_t i = 0; i < img.cells.size(); ++i) {
+      img.cells[i].mean = cells[i].mean;
+      img.cells[i].m2 = cells[i].m2;
+      img.cells[i].count = cells[i].count;
+      img.cells[i].escaped = cells[i].escaped;
+    }
+    if (csv && *csv) write_csv(img, csv);
+    if (pfm && *pfm) write_pfm(img, pfm);
+    if (png && *png) write_png(img, png);
+  });
+}
+double ref_compute_relmse(int32_t w, int32_t h, const double* est, const double* refv) {
+  SolutionImage a = make_image(w, h, Bbox{{0, 0}, {1, 1}}), b = a;
+  for (size_t i = 0; i < a.cells.size(); ++i) {
+    a.cells[i].mean = est[i];
+    b.cells[i].mean = refv[i];
+  }
+  return compute_relmse(a, b);
+}
+int ref_write_convergence_log(int32_t n, const int32_t* wpp, const double* relmse, const double* sec,
+                              const char* path) {
+  return guarded([&] {
+    std::vector<LogRow> rows(n);
+    for (int32_t i = 0; i < n; ++i) rows[i] = LogRow{wpp[i], relmse[i], sec[i]};
+    write_convergence_log(rows, path);
+  });
+}
+// write_scene(make_preset(name).scene) into buf (NUL-terminated); returns
+// the JSON length, or -1 (error text in ref_last_error)
+int64_t ref_preset_scene_json(const char* name, char* buf, int64_t cap) {
+  int64_t n = -1;
+  guarded([&] {
+    std::string js = write_scene(make_preset(name).scene);
+    n = static_cast<int64_t>(js.size());
+    if (buf && cap > n) std::memcpy(buf, js.c_str(), js.size() + 1);
+  });
+  return n;
+}
+// load_scene(json) -> geometry back out, for loader parity
+int64_t ref_load_scene_json(const char* text, double* seg, int32_t* kind, int32_t* value_index,
+                            int64_t cap, double* bbox, double* eps) {
+  int64_t n = -1;
+  guarded([&] {
+    Scene sc = load_scene(text);
+    n = static_cast<int64_t>(sc.segments.size());
+    for (int64_t i = 0; i < n && i < cap; ++i) {
+      const auto& s = sc.segments[i];
+      seg[4 * i] = s.a.x;
+      seg[4 * i + 1] = s.a.y;
+      seg[4 * i + 2] = s.b.x;
+      seg[4 * i + 3] = s.b.y;
+      kind[i] = s.kind == BoundaryKind::Dirichlet ? 0 : 1;
+      value_index[i] = s.value_index;
+    }
+    bbox[0] = sc.bbox.min.x;
+    bbox[1] = sc.bbox.min.y;
+    bbox[2] = sc.bbox.max.x;
+    bbox[3] = sc.bbox.max.y;
+    *eps = sc.epsilon_shell;
+  });
+  return n;
 }
 void ref_field_eval_batch(void* fp, int64_t n, const double* xy, double* out) {
   auto* f = static_cast<GuidingField*>(fp);

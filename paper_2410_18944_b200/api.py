@@ -154,6 +154,64 @@ class GuidingField:
         check(load().wostgpu_field_set_state(self.h, p.ctypes.data_as(C.POINTER(C.c_float)),
                                               _d(m), _d(v), steps))
 
+    # WGF1 checkpoints, byte-compatible with GuidingField::save / load
+    # (guide_field.cpp:333-411); see include/wostgpu.hpp for the layout
+    def save(self, path):
+        p, m, v, steps = self.state()
+        c = self.cfg
+        with open(path, "wb") as f:
+            f.write(b"WGF1")
+            hdr = [1, c.n_levels] + [c.level_res[i] for i in range(c.n_levels)]
+            hdr += [c.features, c.hidden, c.mixture_k, c.mixture_dim]
+            f.write(np.array(hdr, dtype="<u4").tobytes())
+            f.write(np.array(self.bbox, dtype="<f8").tobytes())
+            f.write(np.array([steps], dtype="<i8").tobytes())
+            f.write(np.array([len(p)], dtype="<u8").tobytes())
+            f.write(p.astype("<f4").tobytes())
+            f.write(m.astype("<f8").tobytes())
+            f.write(v.astype("<f8").tobytes())
+
+    @classmethod
+    def load(cls, path, device=None):
+        with open(path, "rb") as f:
+            data = f.read()
+        if data[:4] != b"WGF1":
+            raise ValueError("guiding field checkpoint: bad magic")
+        off = 4
+        u32 = lambda k: np.frombuffer(data, "<u4", k, off)  # noqa: E731
+        ver, nl = u32(2)
+        if ver != 1:
+            raise ValueError("guiding field checkpoint: unknown version")
+        off += 8
+        res = [int(r) for r in u32(nl)]
+        off += 4 * int(nl)
+        feat, hid, k, dim = (int(x) for x in u32(4))
+        off += 16
+        bbox = tuple(float(x) for x in np.frombuffer(data, "<f8", 4, off))
+        off += 32
+        steps = int(np.frombuffer(data, "<i8", 1, off)[0])
+        off += 8
+        n = int(np.frombuffer(data, "<u8", 1, off)[0])
+        off += 8
+        field = cls(abi.field_config(tuple(res), features=feat, hidden=hid, mixture_k=k, mixture_dim=dim),
+                    bbox, 0, device)
+        if n != field.n_params:
+            raise ValueError("guiding field checkpoint: size mismatch")
+        if len(data) < off + n * 20:
+            raise ValueError("guiding field checkpoint: truncated")
+        p = np.frombuffer(data, "<f4", n, off)
+        m = np.frombuffer(data, "<f8", n, off + 4 * n)
+        v = np.frombuffer(data, "<f8", n, off + 12 * n)
+        field.set_state(p, m, v, steps)
+        return field
+
+    def check_pack(self):
+        """Bytes in which the Adam-maintained split-fp16 weight blob of the
+        tensor-core kernels differs from a fresh pack (-1: no blob yet)."""
+        m = C.c_int64()
+        check(load().wostgpu_field_check_pack(self.h, C.byref(m)))
+        return m.value
+
     def eval_batch(self, xy, mlp=MLP_EXACT):
         xy = _xy(xy)
         out = np.zeros((len(xy), self.output_dim))
@@ -167,6 +225,27 @@ def normalize_params(raw, k, dim=2):
     out = np.zeros(raw.shape[0], dtype=abi.MIXTURE_DTYPE)
     check(load().wostgpu_normalize_params(raw.shape[0], _d(raw), k, dim,
                                            C.c_void_p(out.ctypes.data)))
+    return out
+
+
+def mixture32_pdf(raw, nu):
+    """Tensor-core walk path's fp32 mixture math (diagnostic): decode each raw
+    row (33 floats, K = 8) and evaluate the mixture pdf at the unit direction
+    nu[i]; returns (pdf [n], c [n])."""
+    raw = np.ascontiguousarray(raw, dtype=np.float32)
+    nu = np.ascontiguousarray(nu, dtype=np.float64)
+    out = np.zeros((raw.shape[0], 2))
+    check(load().wostgpu_mixture32_pdf(raw.shape[0], raw.ctypes.data_as(C.POINTER(C.c_float)), _d(nu),
+                                       _d(out)))
+    return out[:, 0], out[:, 1]
+
+
+def mixture32_sample(raw, n, seed):
+    """n directions drawn by the tensor-core walk path's sampler from the
+    single mixture `raw` (33 floats), sample i on PCG32 stream (seed, i)."""
+    raw = np.ascontiguousarray(raw, dtype=np.float32).reshape(33)
+    out = np.zeros((n, 2))
+    check(load().wostgpu_mixture32_sample(raw.ctypes.data_as(C.POINTER(C.c_float)), n, seed, _d(out)))
     return out
 
 

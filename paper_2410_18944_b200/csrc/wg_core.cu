@@ -517,5 +517,29 @@ int wostgpu_normalize_params(int64_t n, const double* raw, int32_t k, int32_t di
   });
 }
 
+int wostgpu_mixture32_pdf(int64_t n, const float* raw, const double* nu, double* out) {
+  return guarded([&] {
+    if (n == 0) return;
+    DBuf draw, dnu, dout;
+    draw.upload(raw, (size_t)n * 33);
+    dnu.upload(nu, (size_t)n * 2);
+    dout.alloc(sizeof(double) * 2 * n);
+    CKL(launch_mix32_pdf(draw.as<float>(), n, dnu.as<double>(), dout.as<double>(), 0));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(out, dout.p, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost));
+  });
+}
+
+int wostgpu_mixture32_sample(const float* raw, int64_t n, uint64_t seed, double* nu_out) {
+  return guarded([&] {
+    if (n == 0) return;
+    DBuf draw, dout;
+    draw.upload(raw, 33);
+    dout.alloc(sizeof(double) * 2 * n);
+    CKL(launch_mix32_sample(draw.as<float>(), n, seed, dout.as<double>(), 0));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(nu_out, dout.p, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost));
+  });
+}
 
 }  // extern "C"

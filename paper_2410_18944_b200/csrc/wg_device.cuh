@@ -72,6 +72,10 @@ struct Pcg {
     while (u == 0.0);
     return u;
   }
+  // fp32 uniforms from ONE 32-bit output (tensor-core walk path only):
+  // [0, 1) and (0, 1] on the 2^-24 grid
+  WG_HD float unif() { return static_cast<float>(u32() >> 8) * 0x1.0p-24f; }
+  WG_HD float unif_pos() { return static_cast<float>((u32() >> 8) + 1u) * 0x1.0p-24f; }
 };
 
 // ---------------------------------------------------------------- scene

@@ -108,6 +108,8 @@ int walk_tc_smem(const WalkArgs& a);
 int walk_tc_blocks_per_sm(int smem);
 int walk_tc_block();
 cudaError_t launch_walks_tc(const WalkArgs& a, int blocks, cudaStream_t st);
+cudaError_t launch_mix32_pdf(const float* raw, int64_t n, const double* nu, double* out, cudaStream_t st);
+cudaError_t launch_mix32_sample(const float* raw, int64_t n, uint64_t seed, double* out, cudaStream_t st);
 cudaError_t launch_field_eval_tc(const FieldView& f, int64_t n, const double* xy, double* out,
                                  int sm_count, cudaStream_t st);
 cudaError_t launch_welford(const double* est, const int32_t* esc, int64_t n_points,

@@ -28,33 +28,36 @@ struct Mix32 {
   float c;
 };
 
-// log(I0(x)) - x for x >= 0 (A&S 9.8.1 below 3.75, 9.8.2 above)
-WG_D float log_i0e(float x) {
-  if (x < 3.75f) {
-    float t = x * (1.0f / 3.75f);
-    t *= t;
-    float p = 1.0f + t * (3.5156229f + t * (3.0899424f + t * (1.2067492f + t * (0.2659732f +
-              t * (0.0360768f + t * 0.0045813f)))));
-    return __logf(p) - x;
-  }
-  float t = 3.75f / x;
-  float p = 0.39894228f + t * (0.01328592f + t * (0.00225319f + t * (-0.00157565f + t * (0.00916281f +
-            t * (-0.02057706f + t * (0.02635537f + t * (-0.01647633f + t * 0.00392377f)))))));
-  return __logf(p) - 0.5f * __logf(x);
-}
-
-// branch-free log_i0e: both rational forms, one select (lets the unrolled
-// lobes interleave instead of serialising divergent branches)
-WG_D float log_i0e_nb(float x) {
-  float t = x * (1.0f / 3.75f);
-  t *= t;
-  const float p = 1.0f + t * (3.5156229f + t * (3.0899424f + t * (1.2067492f + t * (0.2659732f +
-                  t * (0.0360768f + t * 0.0045813f)))));
-  const float u = __fdividef(3.75f, fmaxf(x, 3.75f));
-  const float q = 0.39894228f + u * (0.01328592f + u * (0.00225319f + u * (-0.00157565f + u * (0.00916281f +
-                  u * (-0.02057706f + u * (0.02635537f + u * (-0.01647633f + u * 0.00392377f)))))));
-  const bool lo = x < 3.75f;
-  return __logf(lo ? p : q) - (lo ? x : 0.5f * __logf(x));
+// log(I0(k)) - k for k = exp(lk), without logarithms: below 3.75 a degree-10
+// Chebyshev-economised polynomial of log I0 in t = (k / 3.75)^2, above it a
+// degree-8 one of log(I0(k) e^-k sqrt(k)) in u = 3.75 / k (fitted to
+// scipy.special.i0 / i0e; |error| < 2.5e-6 resp. 1.2e-7 in fp32). Both are
+// evaluated and one is selected (branch-free, interleaves across lobes); the
+// caller already knows log k, the MLP output the concentration comes from.
+WG_D float log_i0e_k(float k, float lk, float ik) {
+  const float t = k * k * (1.0f / 14.0625f);
+  float ps = -5.958795547e-01f;
+  ps = fmaf(ps, t, 3.533270836e+00f);
+  ps = fmaf(ps, t, -9.344935417e+00f);
+  ps = fmaf(ps, t, 1.470542622e+01f);
+  ps = fmaf(ps, t, -1.564052677e+01f);
+  ps = fmaf(ps, t, 1.233080673e+01f);
+  ps = fmaf(ps, t, -7.950976849e+00f);
+  ps = fmaf(ps, t, 4.742706299e+00f);
+  ps = fmaf(ps, t, -3.085052967e+00f);
+  ps = fmaf(ps, t, 3.515514374e+00f);
+  ps = ps * t;  // log I0(0) = 0
+  const float u = fminf(3.75f * ik, 1.0f);
+  float pl = 7.403874304e-03f;
+  pl = fmaf(pl, u, -3.077054955e-02f);
+  pl = fmaf(pl, u, 4.749890044e-02f);
+  pl = fmaf(pl, u, -3.451954946e-02f);
+  pl = fmaf(pl, u, 1.407056209e-02f);
+  pl = fmaf(pl, u, -1.557706157e-03f);
+  pl = fmaf(pl, u, 4.722106736e-03f);
+  pl = fmaf(pl, u, 3.332294524e-02f);
+  pl = fmaf(pl, u, -9.189384580e-01f);
+  return k < 3.75f ? ps - k : pl - 0.5f * lk;
 }
 
 // I1(x) / I0(x) for x >= 0 (A&S 9.8.1-9.8.4; the e^x / sqrt(x) factors
@@ -118,12 +121,15 @@ WG_D void normalize32(const float* raw, Mix32& m) {
     const bool fb = !(n2 >= 1e-24f);
     m.mux[i] = fb ? fallback_cos(i) : x * r;
     m.muy[i] = fb ? fallback_sin(i) : y * r;
-    const float k = fminf(fmaxf(__expf(raw[16 + i]), 1e-6f), 1e4f);
+    // kappa = clamp(exp(raw), 1e-6, 1e4) = exp(clamp(raw, ln 1e-6, ln 1e4))
+    const float lk = fminf(fmaxf(raw[16 + i], -13.81551056f), 9.210340372f);
+    const float k = __expf(lk);
     m.kappa[i] = k;
+    // kappa / (2 + eps) to O(eps^2) = 1e-14
     const float eps = fmaf(m.mux[i], m.mux[i], fmaf(m.muy[i], m.muy[i], -1.0f));  // |mu|^2 - 1
-    m.hk[i] = __fdividef(k, 2.0f + eps);
+    m.hk[i] = k * fmaf(-0.25f, eps, 0.5f);
     m.lambda[i] = e[i] * iz;
-    m.lne[i] = -log_i0e_nb(k) - 1.8378770664093453f;  // - log(2 pi)
+    m.lne[i] = -log_i0e_k(k, lk, __expf(-lk)) - 1.8378770664093453f;  // - log(2 pi)
   }
 }
 
@@ -154,10 +160,11 @@ WG_D double reflected_pdf32(const Mix32& m, double nx, double ny, double px, dou
   return mixture_pdf32(m, nx, ny) + mixture_pdf32(m, rx, ry);
 }
 
+// Uniforms on this path are fp32 draws from single PCG32 outputs (Pcg::unif).
 // Best-Fisher (sphdist.cpp:120-140) in fp32, returning the sampled angle as
 // (cos th, sin th) directly. Every quantity that the reference forms by
 // cancellation is rewritten exactly:
-//   r - 1 = (1 - rho)^2 / (2 rho),  1 - z = 2 sin^2(pi u1 / 2),
+//   r - 1 = (1 - rho)^2 / (2 rho),  1 -+ z = 2 sin^2 / cos^2(pi u1 / 2),
 //   r - f = (r - 1)(r + 1) / (r + z),  1 - f = (r - 1)(1 - z) / (r + z),
 // so cv = kappa (r - f) and sin th = sqrt((1 - f)(1 + f)) keep full fp32
 // relative accuracy for concentrated lobes (kappa up to 1e4), and no acos /
@@ -168,18 +175,21 @@ WG_D void vm_cos_sin(Pcg& rng, float kappa, float* oc, float* os) {
   const float s = sqrtf(fmaf(4.0f * kappa, kappa, 1.0f));
   const float tau = 1.0f + s;
   const float rho = __fdividef(2.0f * kappa * tau, (s + 1.0f) * (tau + sqrtf(2.0f * tau)));
-  const float rm1 = __fdividef((1.0f - rho) * (1.0f - rho), 2.0f * rho);  // r - 1 > 0
-  const float r = 1.0f + rm1;
+  // r - 1 > 0; r itself is never rounded to fp32 (for kappa = 1e4, r - 1 =
+  // 5e-5 would lose 3 digits in 1 + (r - 1)): every place r appears is
+  // written in terms of rm1, so proposal and test use the same exact r
+  const float rm1 = __fdividef((1.0f - rho) * (1.0f - rho), 2.0f * rho);
   for (;;) {
-    const float u1 = static_cast<float>(rng.uni_pos());
-    const float h = sinpif(0.5f * u1);
-    const float omz = 2.0f * h * h;  // 1 - z
-    const float inv = __frcp_rn(r + 1.0f - omz);  // 1 / (r + z)
-    const float cv = kappa * rm1 * (r + 1.0f) * inv;
-    const float omf = rm1 * omz * inv;  // 1 - f
-    const float u2 = static_cast<float>(rng.uni_pos());
+    const float u1 = rng.unif_pos();
+    float hs, hc;
+    sincospif(0.5f * u1, &hs, &hc);
+    const float omz = 2.0f * hs * hs;                   // 1 - z, z = cos(pi u1)
+    const float inv = __frcp_rn(fmaf(2.0f * hc, hc, rm1));  // 1 / (r + z), r + z = (1 + z) + rm1
+    const float cv = kappa * rm1 * (2.0f + rm1) * inv;  // kappa (r - f)
+    const float omf = rm1 * omz * inv;                   // 1 - f
+    const float u2 = rng.unif_pos();
     if (cv * (2.0f - cv) - u2 > 0.0f || __logf(__fdividef(cv, u2)) + 1.0f - cv >= 0.0f) {
-      const float u3 = static_cast<float>(rng.uni());
+      const float u3 = rng.unif();
       const float sn = sqrtf(fmaxf(omf * (2.0f - omf), 0.0f));
       *oc = fminf(fmaxf(1.0f - omf, -1.0f), 1.0f);
       *os = u3 < 0.5f ? -sn : sn;
@@ -188,16 +198,17 @@ WG_D void vm_cos_sin(Pcg& rng, float kappa, float* oc, float* os) {
   }
 }
 
-// unit fp32 direction -> fp64 with |nu| = 1 to fp64 rounding (see Mix32)
+// unit fp32 direction -> fp64 with |nu| = 1 to ~1e-15 (see Mix32): |v|^2 =
+// 1 + d with |d| < 1e-6, one Newton step of rsqrt about 1 (error 3d^2/8)
 WG_D void unit64(float x, float y, double* ox, double* oy) {
   const double dx = x, dy = y;
-  const double inv = rsqrt(dx * dx + dy * dy);
+  const double inv = fma(-0.5, fma(dx, dx, dy * dy), 1.5);
   *ox = dx * inv;
   *oy = dy * inv;
 }
 
 WG_D void mixture_sample32(Pcg& rng, const Mix32& m, double* ox, double* oy) {
-  const float u = static_cast<float>(rng.uni());
+  const float u = rng.unif();
   float acc = 0.0f;
   float mux = m.mux[7], muy = m.muy[7];
   float kap = m.kappa[7];
@@ -239,7 +250,7 @@ WG_D void reflected_sample32(Pcg& rng, const Mix32& m, double px, double py, dou
 WG_D void uniform_sample32(Pcg& rng, bool on_n, double px, double py, double* ox, double* oy) {
   for (;;) {
     float sn, cs;
-    sincospif(2.0f * static_cast<float>(rng.uni()), &sn, &cs);
+    sincospif(2.0f * rng.unif(), &sn, &cs);
     double nx, ny;
     unit64(cs, sn, &nx, &ny);
     const double d = on_n ? nx * px + ny * py : 1.0;
@@ -251,22 +262,36 @@ WG_D void uniform_sample32(Pcg& rng, bool on_n, double px, double py, double* ox
   }
 }
 
-// mis_sample (sphdist.cpp:254-270) on the fp32 mixture
-WG_D MisOut mis_sample32(Pcg& rng, const Mix32& m, double c, bool on_n, double px, double py,
-                         bool refl) {
-  MisOut o;
-  bool guided = rng.uni() < c;
+// mis_sample (sphdist.cpp:254-270) on the fp32 mixture, in two halves so the
+// walk kernel can time them: the direction draw and the densities at it
+WG_D bool mis_draw32(Pcg& rng, const Mix32& m, double c, bool on_n, double px, double py, bool refl,
+                     double* nx, double* ny) {
+  const bool guided = rng.unif() < static_cast<float>(c);
   if (guided) {
-    if (on_n && refl) reflected_sample32(rng, m, px, py, &o.nx, &o.ny);
-    else mixture_sample32(rng, m, &o.nx, &o.ny);
+    if (on_n && refl) reflected_sample32(rng, m, px, py, nx, ny);
+    else mixture_sample32(rng, m, nx, ny);
   } else {
-    uniform_sample32(rng, on_n, px, py, &o.nx, &o.ny);
+    uniform_sample32(rng, on_n, px, py, nx, ny);
   }
-  o.pg = on_n ? (refl ? reflected_pdf32(m, o.nx, o.ny, px, py) : mixture_pdf32(m, o.nx, o.ny))
-              : mixture_pdf32(m, o.nx, o.ny);
-  o.pu = uniform_pdf(on_n, o.nx, o.ny, px, py);
+  return guided;
+}
+
+WG_D MisOut mis_eval32(const Mix32& m, double c, bool on_n, double px, double py, bool refl, double nx,
+                       double ny) {
+  MisOut o;
+  o.nx = nx;
+  o.ny = ny;
+  o.pg = on_n && refl ? reflected_pdf32(m, nx, ny, px, py) : mixture_pdf32(m, nx, ny);
+  o.pu = uniform_pdf(on_n, nx, ny, px, py);
   o.pmis = c * o.pg + (1.0 - c) * o.pu;
   return o;
+}
+
+WG_D MisOut mis_sample32(Pcg& rng, const Mix32& m, double c, bool on_n, double px, double py,
+                         bool refl) {
+  double nx, ny;
+  mis_draw32(rng, m, c, on_n, px, py, refl, &nx, &ny);
+  return mis_eval32(m, c, on_n, px, py, refl, nx, ny);
 }
 
 }  // namespace wg

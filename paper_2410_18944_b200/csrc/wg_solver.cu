@@ -535,6 +535,25 @@ int wostgpu_train_batch(wg_solver s, const wg_guide_record* recs, int64_t n,
   });
 }
 
+int wostgpu_field_check_pack(wg_field f, int64_t* mismatched_bytes) {
+  return guarded([&] {
+    need(f != nullptr && mismatched_bytes != nullptr, WG_ERR_INVALID, "null argument");
+    *mismatched_bytes = -1;
+    if (!f->wpack.p || f->pack_dirty) return;  // no maintained blob to check
+    DBuf fresh;
+    fresh.alloc(wpack::BYTES);
+    CK(cudaMemset(fresh.p, 0, wpack::BYTES));
+    CKL(launch_pack_weights(f->view, fresh.as<unsigned char>(), 0));
+    CK(cudaDeviceSynchronize());
+    std::vector<unsigned char> a(wpack::BYTES), b(wpack::BYTES);
+    CK(cudaMemcpy(a.data(), f->wpack.p, wpack::BYTES, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(b.data(), fresh.p, wpack::BYTES, cudaMemcpyDeviceToHost));
+    int64_t m = 0;
+    for (size_t i = 0; i < a.size(); ++i) m += a[i] != b[i];
+    *mismatched_bytes = m;
+  });
+}
+
 int wostgpu_field_grad(wg_solver s, const wg_guide_record* recs, int64_t n,
                        const wg_train_config* cfg, double* grad) {
   return guarded([&] {

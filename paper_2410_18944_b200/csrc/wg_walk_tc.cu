@@ -52,59 +52,64 @@ struct TLane {
 
 __host__ __device__ __forceinline__ size_t al16(size_t b) { return (b + 15) & ~size_t(15); }
 
-// Small scenes (the benchmark square has 4 segments): visit every segment in
-// BVH leaf order without the traversal stack. Same per-segment arithmetic as
-// closest_point / ray_first_hit (wg_device.cuh), branch-uniform across the
-// warp (every lane tests the same segment); a one-leaf BVH visits segments in
-// exactly this order, otherwise only exact-distance ties can resolve to a
-// different (equidistant) segment.
+// Small scenes (the benchmark square has 4 segments): no traversal stack.
+// At launch the CTA copies the segments of each kind, in BVH leaf order, into
+// shared-memory lists; a query scans only its kind's list, every segment
+// evaluated with predicated updates so the fp64 divisions of consecutive
+// segments overlap. Same per-segment arithmetic and the same strict-< / <=
+// updates in visiting order as closest_point / ray_first_hit (wg_device.cuh):
+// a one-leaf BVH visits segments in exactly this order, otherwise only
+// exact-distance ties can resolve to a different (equidistant) segment.
 constexpr int kSmallScene = 16;
 
-__device__ __forceinline__ CP cp_small(const SceneView& s, double x, double y, unsigned kinds) {
+struct SmallSegs {
+  const Seg* d;  // Dirichlet segments
+  const Seg* n;  // Neumann segments
+  int nd, nn;
+};
+
+__device__ __forceinline__ CP cp_list(const Seg* segs, int n, double x, double y) {
   CP best{0.0, 0.0, dinf(), -1};
   double bd2 = dinf();
 #pragma unroll 4
-  for (int i = 0; i < s.n_segs; ++i) {
-    const Seg g = s.segs[i];
-    if (!((g.kind == WG_DIRICHLET ? 1u : 2u) & kinds)) continue;
+  for (int i = 0; i < n; ++i) {
+    const Seg g = segs[i];
     double ux = g.bx - g.ax, uy = g.by - g.ay;
     double t = ((x - g.ax) * ux + (y - g.ay) * uy) / (ux * ux + uy * uy);
     t = sclamp(t, 0.0, 1.0);
     double px = g.ax + t * ux, py = g.ay + t * uy;
     double dx = px - x, dy = py - y;
     double d2 = dx * dx + dy * dy;
-    if (d2 < bd2) {
-      bd2 = d2;
-      best.px = px;
-      best.py = py;
-      best.seg = g.id;
-    }
+    const bool take = d2 < bd2;
+    bd2 = take ? d2 : bd2;
+    best.px = take ? px : best.px;
+    best.py = take ? py : best.py;
+    best.seg = take ? g.id : best.seg;
   }
   if (best.seg >= 0) best.d = sqrt(bd2);
   return best;
 }
 
-__device__ __forceinline__ Hit ray_small(const SceneView& s, double ox, double oy, double dx, double dy,
-                                         double t_max, unsigned kinds, int exclude) {
+// the hit normal (normalised perp_left, flipped against the ray) is formed
+// once, for the winner only
+__device__ __forceinline__ Hit ray_list(const Seg* segs, int n, double t_eps, double ox, double oy,
+                                        double dx, double dy, double t_max, int exclude) {
   double bt = t_max, bsp = 0.0;
   int bi = -1;
 #pragma unroll 4
-  for (int i = 0; i < s.n_segs; ++i) {
-    const Seg g = s.segs[i];
-    if (!((g.kind == WG_DIRICHLET ? 1u : 2u) & kinds)) continue;
-    if (g.id == exclude) continue;
+  for (int i = 0; i < n; ++i) {
+    const Seg g = segs[i];
     double ux = g.bx - g.ax, uy = g.by - g.ay;
     double wx = g.ax - ox, wy = g.ay - oy;
     double den = dx * uy - dy * ux;
-    if (den == 0.0) continue;
-    double t = (wx * uy - wy * ux) / den;
-    double sp = (wx * dy - wy * dx) / den;
-    if (sp < 0.0 || sp > 1.0) continue;
-    if (t > s.t_eps && t <= bt) {
-      bt = t;
-      bi = i;
-      bsp = sp;
-    }
+    const bool nz = den != 0.0;
+    const double dd = nz ? den : 1.0;
+    double t = (wx * uy - wy * ux) / dd;
+    double sp = (wx * dy - wy * dx) / dd;
+    const bool take = g.id != exclude && nz && !(sp < 0.0 || sp > 1.0) && t > t_eps && t <= bt;
+    bt = take ? t : bt;
+    bi = take ? i : bi;
+    bsp = take ? sp : bsp;
   }
   Hit h;
   h.seg = -1;
@@ -112,7 +117,7 @@ __device__ __forceinline__ Hit ray_small(const SceneView& s, double ox, double o
   h.t = dinf();
   h.px = h.py = h.nx = h.ny = 0.0;
   if (bi < 0) return h;
-  const Seg g = s.segs[bi];
+  const Seg g = segs[bi];
   h.t = bt;
   double ux = g.bx - g.ax, uy = g.by - g.ay;
   h.px = g.ax + bsp * ux;
@@ -131,15 +136,44 @@ __device__ __forceinline__ Hit ray_small(const SceneView& s, double ox, double o
   return h;
 }
 
-__device__ __forceinline__ CP t_closest(const SceneView& s, double x, double y, unsigned kinds) {
-  return s.n_segs <= kSmallScene ? cp_small(s, x, y, kinds) : closest_point(s, x, y, kinds);
+__device__ __forceinline__ CP t_closest(const SceneView& s, const SmallSegs& ss, double x, double y,
+                                        unsigned kinds) {
+  if (s.n_segs > kSmallScene) return closest_point(s, x, y, kinds);
+  return kinds == WG_KIND_DIRICHLET ? cp_list(ss.d, ss.nd, x, y) : closest_point(s, x, y, kinds);
 }
 
-__device__ __forceinline__ Hit t_ray(const SceneView& s, double ox, double oy, double dx, double dy,
-                                     double t_max, unsigned kinds, int exclude) {
-  return s.n_segs <= kSmallScene ? ray_small(s, ox, oy, dx, dy, t_max, kinds, exclude)
-                                 : ray_first_hit(s, ox, oy, dx, dy, t_max, kinds, exclude);
+__device__ __forceinline__ Hit t_ray(const SceneView& s, const SmallSegs& ss, double ox, double oy, double dx,
+                                     double dy, double t_max, unsigned kinds, int exclude) {
+  if (s.n_segs > kSmallScene || kinds != WG_KIND_NEUMANN)
+    return ray_first_hit(s, ox, oy, dx, dy, t_max, kinds, exclude);
+  return ray_list(ss.n, ss.nn, s.t_eps, ox, oy, dx, dy, t_max, exclude);
 }
+
+// closest_silhouette for small vertex lists: squared distances of all
+// vertices first (independent), then the candidate tests in order
+__device__ __forceinline__ double sil_small(const SceneView& s, double x, double y) {
+  double best = dinf();
+#pragma unroll 4
+  for (int v = 0; v < s.n_sil; ++v) {
+    const SilVertex sv = s.sil[v];
+    const double dx = sv.px - x, dy = sv.py - y;
+    const double d = dx * dx + dy * dy;
+    bool cand = sv.n_count < 2;
+    if (!cand && d < best) {
+      double lo = dinf(), hi = -dinf();
+      for (int k = 0; k < sv.n_count; ++k) {
+        double nx = s.sil_n[2 * (sv.n_begin + k)], ny = s.sil_n[2 * (sv.n_begin + k) + 1];
+        double f = nx * dx + ny * dy;
+        lo = smin(lo, f);
+        hi = smax(hi, f);
+      }
+      cand = lo * hi <= 0.0;
+    }
+    best = (cand && d < best) ? d : best;
+  }
+  return best == dinf() ? best : sqrt(best);
+}
+
 
 __device__ __forceinline__ void t_finish(TLane& w, const WalkArgs& a, bool escaped, double terminal,
                                          bool collect) {
@@ -175,11 +209,11 @@ __device__ double t_greens_radius(double u, double R) {  // wost.cpp:37-65, d = 
 }
 
 // begin_step (wost.cpp:148-216); false when the walk terminated
-__device__ __forceinline__ bool t_begin(TLane& w, const WalkArgs& a, const SceneView& s, bool collect,
-                                        long long* sub) {
+__device__ __forceinline__ bool t_begin(TLane& w, const WalkArgs& a, const SceneView& s,
+                                        const SmallSegs& ss, bool collect, long long* sub) {
   (void)sub;
   SUB_T(t0);
-  CP cd = t_closest(s, w.x, w.y, WG_KIND_DIRICHLET);
+  CP cd = t_closest(s, ss, w.x, w.y, WG_KIND_DIRICHLET);
   SUB_ADD(0, t0);
   if (cd.seg >= 0 && cd.d <= a.sp.eps) {
     double g = eval_value(s.values[s.seg_value[cd.seg]], cd.px, cd.py);
@@ -202,7 +236,7 @@ __device__ __forceinline__ bool t_begin(TLane& w, const WalkArgs& a, const Scene
     w.rr = 1.0 / q;
   }
   SUB_T(t1);
-  double dsil = closest_silhouette(s, w.x, w.y);
+  double dsil = s.n_sil <= kSmallScene ? sil_small(s, w.x, w.y) : closest_silhouette(s, w.x, w.y);
   SUB_ADD(1, t1);
   SUB_T(t2);
   double dd = cd.seg >= 0 ? cd.d : dinf();
@@ -218,7 +252,7 @@ __device__ __forceinline__ bool t_begin(TLane& w, const WalkArgs& a, const Scene
     uniform_sample32(w.rng, w.on_n, w.nx, w.ny, &dx, &dy);
     double r = t_greens_radius(w.rng.uni(), w.R);
     double yx = w.x + dx * r, yy = w.y + dy * r;
-    Hit h = t_ray(s, w.x, w.y, dx, dy, r, WG_KIND_ALL, -1);
+    Hit h = t_ray(s, ss, w.x, w.y, dx, dy, r, WG_KIND_ALL, -1);
     double wt = h.seg >= 0 ? 0.0 : w.R * w.R / 4.0;
     if (wt != 0.0) {
       double f = 0.0;
@@ -229,7 +263,7 @@ __device__ __forceinline__ bool t_begin(TLane& w, const WalkArgs& a, const Scene
   if (s.has_flux) {
     double dx, dy;
     uniform_sample32(w.rng, w.on_n, w.nx, w.ny, &dx, &dy);
-    Hit h = t_ray(s, w.x, w.y, dx, dy, w.R, WG_KIND_NEUMANN, w.seg);
+    Hit h = t_ray(s, ss, w.x, w.y, dx, dy, w.R, WG_KIND_NEUMANN, w.seg);
     double add = 0.0;
     if (h.seg >= 0) {
       double hv = eval_value(s.values[s.seg_value[h.seg]], h.px, h.py);
@@ -294,6 +328,20 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
     s.sil = sil;
     s.sil_n = sn;
   }
+  // per-kind segment lists of small scenes (BVH leaf order)
+  __shared__ Seg seg_lists[2 * kSmallScene];
+  __shared__ int seg_counts[2];
+  if (s.n_segs <= kSmallScene && threadIdx.x == 0) {
+    int nd = 0, nn = 0;
+    for (int i = 0; i < s.n_segs; ++i) {
+      const Seg g = s.segs[i];
+      if (g.kind == WG_DIRICHLET) seg_lists[nd++] = g;
+      else seg_lists[kSmallScene + nn++] = g;
+    }
+    seg_counts[0] = nd;
+    seg_counts[1] = nn;
+  }
+  SmallSegs ss{seg_lists, seg_lists + kSmallScene, 0, 0};
   if (kWarp) {
     tcw_stage_weights(tc, a.field);
   } else {
@@ -304,6 +352,8 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
   __syncthreads();
   umma::fence_after();
   if (!kWarp) tc_wait_weights(tc);
+  ss.nd = seg_counts[0];
+  ss.nn = seg_counts[1];
 
   const bool collect = a.recs != nullptr;
   const int64_t total = a.n_points * static_cast<int64_t>(a.n_rounds);
@@ -351,7 +401,7 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
         next += stride;
         ++walks_done;
       }
-      if (t_begin(w, a, s, collect, sub)) {
+      if (t_begin(w, a, s, ss, collect, sub)) {
         need = true;
         break;
       }
@@ -407,7 +457,12 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
     double sel = m.c;
     if (a.sp.mode == WG_MODE_GUIDING_ONLY) sel = 1.0;
     else if (a.sp.mode == WG_MODE_FIXED_MIS) sel = a.sp.fixed_c;
-    MisOut o = mis_sample32(w.rng, m, sel, w.on_n, w.nx, w.ny, a.sp.reflect != 0);
+    double dnx, dny;
+    mis_draw32(w.rng, m, sel, w.on_n, w.nx, w.ny, a.sp.reflect != 0, &dnx, &dny);
+    SUB_ADD(9, ts);
+    SUB_T(te);
+    MisOut o = mis_eval32(m, sel, w.on_n, w.nx, w.ny, a.sp.reflect != 0, dnx, dny);
+    SUB_ADD(10, te);
     double mult = o.pu / o.pmis;
     SUB_ADD(6, ts);
     SUB_T(tr);
@@ -440,7 +495,7 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
       continue;
     }
     SUB_T(th);
-    Hit h = t_ray(s, w.x, w.y, o.nx, o.ny, w.R, WG_KIND_NEUMANN, w.seg);
+    Hit h = t_ray(s, ss, w.x, w.y, o.nx, o.ny, w.R, WG_KIND_NEUMANN, w.seg);
     SUB_ADD(8, th);
     if (h.seg >= 0) {
       w.x = h.px;
@@ -473,9 +528,9 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
       __threadfence();
       double n = static_cast<double>(g_sub[11] > 0 ? g_sub[11] : 1);
       printf("[sub] steps %.0f cyc/step: cp %.0f sil %.0f begin_rest %.0f gather %.0f mlp %.0f norm %.0f "
-             "sample %.0f rec %.0f ray %.0f\n",
+             "sample %.0f (draw %.0f pdf %.0f) rec %.0f ray %.0f\n",
              n, g_sub[0] / n, g_sub[1] / n, g_sub[2] / n, g_sub[3] / n, g_sub[4] / n, g_sub[5] / n,
-             g_sub[6] / n, g_sub[7] / n, g_sub[8] / n);
+             g_sub[6] / n, g_sub[9] / n, g_sub[10] / n, g_sub[7] / n, g_sub[8] / n);
       for (int i = 0; i < 16; ++i) g_sub[i] = 0;
       g_sub_done = 0;
     }
@@ -534,6 +589,41 @@ int walk_tc_warps() {
 }
 
 int walk_tc_block() { return walk_tc_warps() == 0 ? 128 : 32 * walk_tc_warps(); }
+
+// ---- diagnostics of the fp32 mixture math (wostgpu_mixture32_*)
+__global__ void mix32_pdf_kernel(const float* raw, int64_t n, const double* nu, double* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float r[33];
+  for (int j = 0; j < 33; ++j) r[j] = raw[i * 33 + j];
+  Mix32 m;
+  normalize32(r, m);
+  out[2 * i] = mixture_pdf32(m, nu[2 * i], nu[2 * i + 1]);
+  out[2 * i + 1] = m.c;
+}
+
+__global__ void mix32_sample_kernel(const float* raw, int64_t n, uint64_t seed, double* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float r[33];
+  for (int j = 0; j < 33; ++j) r[j] = raw[j];
+  Mix32 m;
+  normalize32(r, m);
+  Pcg rng = Pcg::walk(seed, static_cast<uint64_t>(i), 0);
+  mixture_sample32(rng, m, &out[2 * i], &out[2 * i + 1]);
+}
+
+cudaError_t launch_mix32_pdf(const float* raw, int64_t n, const double* nu, double* out, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  mix32_pdf_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(raw, n, nu, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mix32_sample(const float* raw, int64_t n, uint64_t seed, double* out, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  mix32_sample_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(raw, n, seed, out);
+  return cudaGetLastError();
+}
 
 int walk_tc_smem(const WalkArgs& a) {
   size_t tile = walk_tc_warps() == 0 ? TcLayout::BYTES : TcLayoutW::BYTES;

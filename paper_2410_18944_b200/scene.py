@@ -83,6 +83,7 @@ class Scene:
     value_index: np.ndarray  # [n] int32
     values: List[Value]
     source: Value = field(default_factory=Value.zero)
+    value_names: Optional[List[str]] = None  # Scene::values keys (scene JSON, scene_io.py)
 
     @property
     def n_segments(self):
@@ -128,9 +129,10 @@ class _Builder:
             self.vidx.append(self.names[ref])
 
     def build(self):
+        names = sorted(self.names, key=self.names.get)
         return Scene(self.bbox, self.eps, np.array(self.segs, dtype=np.float64),
                      np.array(self.kinds, dtype=np.int32), np.array(self.vidx, dtype=np.int32),
-                     self.values, self.source)
+                     self.values, self.source, names)
 
 
 def circle_points(center, radius, n):  # presets.cpp:24-31

@@ -86,6 +86,14 @@ class Oracle:
             f.argtypes = [C.c_char_p, D, I32, I32, D, D, D]
             self.lib.ref_strip_vlin_solution.restype = C.c_double
             self.lib.ref_strip_vlin_solution.argtypes = [C.c_double, C.c_double]
+            # WGF1 checkpoints through the reference's GuidingField::save / load
+            if hasattr(self.lib, "ref_field_save"):
+                self.lib.ref_field_save.restype = C.c_int
+                self.lib.ref_field_save.argtypes = [VP, C.c_char_p]
+                self.lib.ref_field_load.restype = VP
+                self.lib.ref_field_load.argtypes = [C.c_char_p]
+                self.lib.ref_field_adam_steps.restype = C.c_int64
+                self.lib.ref_field_adam_steps.argtypes = [VP]
 
     def fn(self, name):
         return getattr(self.lib, f"{self.p}_{name}")

@@ -1,6 +1,8 @@
 """GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the
 same inputs. Geometry, field evaluation, normalisation and per-walk estimates
 are compared bit for bit or with the tolerance stated in each test."""
+import ctypes as C
+
 import numpy as np
 import pytest
 
@@ -248,6 +250,61 @@ def test_train_round_reduces_kl_and_updates_field(gpu):
     p1 = fg.params()
     assert not np.array_equal(p0, p1)
     assert np.all(np.isfinite(p1))
+
+
+def test_tensor_core_training_keeps_weight_blob_in_sync(gpu):
+    """Adam rewrites the packed split-fp16 weights of every MLP parameter it
+    updates (wg_wpack.cuh); after guided training rounds on the tensor-core
+    path the blob equals a fresh pack of the parameters byte for byte, and a
+    host write marks it for repacking."""
+    p = make_preset("neumann-strip-vlin")
+    fg = api.GuidingField(abi.field_config(), p.scene.bbox, 7)
+    sol = api.Solver(api.Accel(p.scene), fg, abi.solver_config("learnable_mis"), api.MLP_TENSOR)
+    sol.set_points(cell_centers(64, 64, p.eval_bbox))
+    assert fg.check_pack() == -1
+    sol.run(1, 3, 256, abi.train_config(seed=1))
+    assert fg.check_pack() == 0
+    fg.set_params(fg.params() * 1.01)
+    assert fg.check_pack() == -1  # dirty until the next tensor-core launch
+    sol.run(2, 1, 256, abi.train_config(seed=1))
+    assert fg.check_pack() == 0
+
+
+def test_wgf1_checkpoint_interop_with_reference(gpu, ref, tmp_path):
+    """WGF1 checkpoints (guide_field.cpp:333-411) are byte-compatible both
+    ways: a fresh field saved by the reference and by us is the same file; a
+    field trained on the GPU loads into the reference with identical params
+    and Adam step count, and the reference re-saves it byte for byte."""
+    if not hasattr(ref.lib, "ref_field_save"):
+        pytest.skip("oracle/_ref built without the checkpoint shim")
+    p = make_preset("neumann-strip-vlin")
+    cfg = abi.field_config()
+    bbox = p.scene.bbox
+    hr = ref.fn("field_create")(C.byref(cfg), (C.c_double * 4)(*bbox), 9)
+    a, b = tmp_path / "ref.wgf", tmp_path / "ours.wgf"
+    assert ref.lib.ref_field_save(hr, str(a).encode()) == 0
+    fg = api.GuidingField(cfg, bbox, 9)
+    fg.save(b)
+    assert a.read_bytes() == b.read_bytes()
+    # train on the GPU, hand the checkpoint to the reference
+    sol = api.Solver(api.Accel(p.scene), fg, abi.solver_config("learnable_mis"))
+    sol.set_points(cell_centers(64, 64, p.eval_bbox))
+    sol.run(1, 2, 256, abi.train_config(seed=1))
+    c, d = tmp_path / "trained.wgf", tmp_path / "resaved.wgf"
+    fg.save(c)
+    hl = ref.lib.ref_field_load(str(c).encode())
+    assert hl
+    pr = np.zeros(fg.n_params, dtype=np.float32)
+    ref.fn("field_get_params")(hl, pr.ctypes.data_as(C.POINTER(C.c_float)))
+    assert np.array_equal(pr, fg.params())
+    assert ref.lib.ref_field_adam_steps(hl) == fg.state()[3] == 4
+    assert ref.lib.ref_field_save(hl, str(d).encode()) == 0
+    assert d.read_bytes() == c.read_bytes()
+    # and back: our loader reproduces the reference's file
+    f2 = api.GuidingField.load(a)
+    assert np.array_equal(f2.params(), api.GuidingField(cfg, bbox, 9).params())
+    ref.fn("field_destroy")(hr)
+    ref.fn("field_destroy")(hl)
 
 
 # ---------------------------------------------------------------- tensor cores

@@ -1,12 +1,14 @@
 """Estimator-level parity with the reference on cfg 2 (neumann-strip-vlin
 128^2, 256 wpp, seed 1) against the reference's own per-point statistics
 (tests/golden/ref_cfg2_*_seed1.npz, from its run_solve) and its relMSE over
-seeds 1-4 (tests/golden/ref_cfg2_seeds.json):
+seeds 1-8 (tests/golden/ref_cfg2_seeds.json, tests/golden/make_cfg2_seeds.py):
   * uniform WoSt: per-point means equal the reference's to 1e-9 (same PCG32
     streams, fp64 arithmetic in the same order);
   * learnable MIS with online training: per-point means within 3 combined
-    standard errors for >= 99% of points, and the 4-seed mean relMSE and the
-    variance-reduction factor over uniform within 10% of the reference's."""
+    standard errors for >= 99% of points, and the 8-seed mean relMSE and the
+    variance-reduction factor over uniform within 10% of the reference's (a
+    single seed's relMSE scatters by ~10%, dominated by a few rare
+    high-throughput walks, so both sides average 8 seeds)."""
 import json
 import os
 
@@ -60,7 +62,9 @@ def test_guided_cfg2_per_point_within_3_se(gpu, mlp):
 def test_guided_relmse_and_variance_reduction_within_10_percent(gpu):
     ref = json.load(open(os.path.join(G, "ref_cfg2_seeds.json")))
     ours_g, ours_u = [], []
-    for seed in (1, 2, 3, 4):
+    seeds = sorted(int(k) for k in ref["learnable_mis"])
+    assert len(seeds) == 8
+    for seed in seeds:
         st, img = _run("learnable_mis", seed)
         ours_g.append(relmse(st["mean"], img))
         st, img = _run("uniform", seed)
