@@ -294,6 +294,30 @@ def main():
     _, ums = usolver.run(SEED, WPP, 0, None)
     rel_uniform = relmse(usolver.stats()["mean"], ref_img)
 
+    # estimator quality over 8 seeds (a single seed's relMSE scatters by ~10%):
+    # guided (this arm's MLP path) and uniform at equal samples, and uniform at
+    # equal device time (as many wpp as fit in the guided run's time)
+    quality_seeds = []
+    if world == 1:
+        acc = api.Accel(preset.scene)
+        for sd in range(1, 9):
+            f = api.GuidingField(abi.field_config(), preset.scene.bbox, sd)
+            gs = api.Solver(acc, f, abi.solver_config("learnable_mis"),
+                            api.MLP_TENSOR if args.mlp == "tensor" else api.MLP_EXACT)
+            gs.set_points(pts, offset)
+            _, gms = gs.run(sd, WPP, TRAIN_UNTIL, abi.train_config(seed=sd))
+            us = api.Solver(acc, None, abi.solver_config("uniform"))
+            us.set_points(pts, offset)
+            _, ums_s = us.run(sd, WPP, 0, None)
+            quality_seeds.append((relmse(gs.stats()["mean"], ref_img), relmse(us.stats()["mean"], ref_img),
+                                  gms, ums_s))
+        q = np.array(quality_seeds)
+        wpp_eq = int(WPP * q[:, 2].mean() / q[:, 3].mean())
+        us = api.Solver(api.Accel(preset.scene), None, abi.solver_config("uniform"))
+        us.set_points(pts, offset)
+        _, ums_eq = us.run(SEED, wpp_eq, 0, None)
+        rel_uniform_eq_time = relmse(us.stats()["mean"], ref_img)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r = cpu_reference_rate(args.ref_rounds, os.cpu_count() or 1)
@@ -322,6 +346,21 @@ def main():
                 "quality": {"relmse_guided": rel_guided, "relmse_uniform_equal_wpp": rel_uniform,
                             "vr_factor": rel_uniform / rel_guided if rel_guided > 0 else None,
                             "uniform_ms": ums, "escaped": pr["escaped"]}}
+        if quality_seeds:
+            # reference side: tests/golden/ref_cfg2_seeds.json (its run_solve, seeds 1-8)
+            q = np.array(quality_seeds)
+            with open(os.path.join(ROOT, "tests", "golden", "ref_cfg2_seeds.json")) as f:
+                rs = json.load(f)
+            ref_g = float(np.mean(list(rs["learnable_mis"].values())))
+            ref_u = float(np.mean(list(rs["uniform"].values())))
+            line["quality"].update({
+                "seeds": 8, "relmse_guided_mean": float(q[:, 0].mean()),
+                "relmse_uniform_mean": float(q[:, 1].mean()),
+                "vr_factor_mean": float(q[:, 1].mean() / q[:, 0].mean()),
+                "reference_relmse_guided_mean_8seeds": ref_g, "reference_vr_factor_8seeds": ref_u / ref_g,
+                "guided_ms_mean": float(q[:, 2].mean()), "uniform_ms_mean": float(q[:, 3].mean()),
+                "uniform_equal_time_wpp": wpp_eq, "relmse_uniform_equal_time": rel_uniform_eq_time,
+                "vr_factor_equal_time": rel_uniform_eq_time / float(q[:, 0].mean())})
         print(json.dumps(line))
     if dist:
         dist.barrier()

@@ -8,6 +8,7 @@
 // when a caller asks for results (statistics, records, TrainStats, timings).
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "wg_runtime.hpp"
 #include "wg_wpack.cuh"
@@ -259,7 +260,13 @@ void enqueue_minibatch(wg_solver_s* s, const wg_train_config& tc, int b, double 
   ta.e_fraction = tc.e_fraction;
   ta.v_floor = tc.v_floor;
   ta.totals = s->totals.as<TrainTotals>();
-  if (s->mlp == WG_MLP_TENSOR && tc_grad_available()) {
+  // WOSTGPU_GRAD=cuda: CUDA-core fp64-loss gradient tile under tensor-core walks
+  // (experiments separating walk-side and training-side numerics)
+  static const bool force_cuda_grad = [] {
+    const char* e = std::getenv("WOSTGPU_GRAD");
+    return e && std::string(e) == "cuda";
+  }();
+  if (s->mlp == WG_MLP_TENSOR && tc_grad_available() && !force_cuda_grad) {
     ta.packed = field_blob(f, s->stream);
     CKL(launch_grad_tc(ta, s->stream));
   }
