@@ -108,6 +108,11 @@ int walk_tc_smem(const WalkArgs& a);
 int walk_tc_blocks_per_sm(int smem);
 int walk_tc_block();
 cudaError_t launch_walks_tc(const WalkArgs& a, int blocks, cudaStream_t st);
+// warp-per-walk guided kernel for the default field shape (wg_walk_coop.cu)
+int walk_coop_smem(const WalkArgs& a);
+int walk_coop_block();
+int walk_coop_blocks_per_sm(int smem);
+cudaError_t launch_walks_coop(const WalkArgs& a, int blocks, cudaStream_t st);
 cudaError_t launch_mix32_pdf(const float* raw, int64_t n, const double* nu, double* out, cudaStream_t st);
 cudaError_t launch_mix32_sample(const float* raw, int64_t n, uint64_t seed, double* out, cudaStream_t st);
 cudaError_t launch_field_eval_tc(const FieldView& f, int64_t n, const double* xy, double* out,

@@ -172,8 +172,13 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
 
   // guided walks on the default field shape: tcgen05 MLP tile kernel, or the
   // bit-faithful CUDA-core MLP with 8 lanes per walk; otherwise generic
-  const bool tc = dflt && s->mlp == WG_MLP_TENSOR;
-  const bool g8 = dflt && !tc;
+  static const bool coop_env = [] {
+    const char* e = std::getenv("WOSTGPU_WALK");
+    return e && std::string(e) == "coop";
+  }();
+  const bool coop = dflt && s->mlp == WG_MLP_TENSOR && coop_env;
+  const bool tc = dflt && s->mlp == WG_MLP_TENSOR && !coop;
+  const bool g8 = dflt && !tc && !coop;
   int smem = (s->scene->smem_bytes > 0 ? ((s->scene->smem_bytes + 15) & ~15) : 0) +
              (guided ? ((int)sizeof(float) * s->field->view.mlp_count + 15) / 16 * 16 : 0);
   if (g8) smem = walk_g8_smem(a);
@@ -181,11 +186,13 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
     smem = walk_tc_smem(a);
     a.wblob = field_blob(s->field, s->stream);
   }
-  const int lanes_per_walk = g8 ? 8 : 1;
-  const int block = g8 ? 256 : tc ? walk_tc_block() : 128;
-  const int per_sm = std::max(1, tc ? walk_tc_blocks_per_sm(smem)
-                                    : g8 ? walk_g8_blocks_per_sm(smem)
-                                         : walk_blocks_per_sm(dflt, guided && !dflt, smem));
+  if (coop) smem = walk_coop_smem(a);
+  const int lanes_per_walk = g8 ? 8 : coop ? 32 : 1;
+  const int block = g8 ? 256 : tc ? walk_tc_block() : coop ? walk_coop_block() : 128;
+  const int per_sm = std::max(1, tc     ? walk_tc_blocks_per_sm(smem)
+                                 : coop ? walk_coop_blocks_per_sm(smem)
+                                 : g8   ? walk_g8_blocks_per_sm(smem)
+                                        : walk_blocks_per_sm(dflt, guided && !dflt, smem));
   for (int32_t r0 = 0; r0 < rounds; r0 += chunk) {
     int32_t n = std::min(chunk, rounds - r0);
     a.wpp_first = wpp_first + r0;
@@ -215,7 +222,8 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
                    worst, it, q[0] / it, q[1] / it, q[5] / it, q[6] / it, q[4] / it, q[2] / it);
     }
     if (tc) {
-    } else if (g8) CKL(launch_walks_g8(a, std::max(1, blocks), s->stream));
+    } else if (coop) CKL(launch_walks_coop(a, std::max(1, blocks), s->stream));
+    else if (g8) CKL(launch_walks_g8(a, std::max(1, blocks), s->stream));
     else CKL(launch_walks(a, dflt, guided && !dflt, std::max(1, blocks), s->stream));
     CK(cudaEventRecord(pool_event(s->ev_walk, s->n_walk_ev), s->stream));
     CKL(launch_welford(a.est, a.esc, s->n_points, n, s->stats.as<wg_point_stats>(), s->stream));

@@ -53,11 +53,12 @@ def samples(rep):
         try:
             addr = int(r["Address"], 16)
             s = int(r["Warp Stall Sampling (All Samples)"] or 0)
+            ex = int(r.get("Instructions Executed") or 0)
         except (KeyError, ValueError):
             continue
-        res.append((addr, s, r["Source"]))
-    base = min(a for a, _, _ in res) if res else 0  # runtime addresses -> section offsets
-    return [(a - base, s, src) for a, s, src in res]
+        res.append((addr, s, r["Source"], ex))
+    base = min(r[0] for r in res) if res else 0  # runtime addresses -> section offsets
+    return [(a - base, s, src, ex) for a, s, src, ex in res]
 
 
 def main():
@@ -66,12 +67,16 @@ def main():
     table = line_table(obj, kernel)
     per_line = collections.Counter()
     per_file = collections.Counter()
+    inst_line = collections.Counter()
     total = 0
-    for addr, s, _ in samples(rep):
+    tinst = 0
+    for addr, s, _, ex in samples(rep):
         total += s
+        tinst += ex
         key = table.get(addr, ("?", 0))
         per_line[key] += s
         per_file[key[0]] += s
+        inst_line[key] += ex
     src_cache = {}
     root = os.path.dirname(os.path.abspath(obj))
     csrc = os.path.join(os.path.dirname(root), "paper_2410_18944_b200", "csrc")
@@ -81,6 +86,13 @@ def main():
             src_cache[f] = open(p).read().splitlines() if os.path.exists(p) else []
         text = src_cache[f][n - 1].strip() if 0 < n <= len(src_cache[f]) else ""
         print(f"{100.0 * s / max(total, 1):5.1f}%  {f}:{n}  {text[:90]}")
+    print("-- top lines by executed warp instructions")
+    for (f, n), c in inst_line.most_common(top // 2):
+        if f not in src_cache:
+            p = os.path.join(csrc, f)
+            src_cache[f] = open(p).read().splitlines() if os.path.exists(p) else []
+        text = src_cache[f][n - 1].strip() if 0 < n <= len(src_cache[f]) else ""
+        print(f"{100.0 * c / max(tinst, 1):5.1f}%  {f}:{n}  {text[:90]}")
     print("-- per file")
     for f, s in per_file.most_common():
         print(f"{100.0 * s / max(total, 1):5.1f}%  {f}")
