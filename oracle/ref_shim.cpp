@@ -555,6 +555,25 @@ int ref_run_solve(const char* preset, int32_t width, int32_t height, int32_t wpp
   });
 }
 
+// run_solve writing the trained field as a WGF1 checkpoint (cfg.field_out)
+int ref_run_solve_field(const char* preset, int32_t width, int32_t height, int32_t wpp, int32_t mode,
+                        int64_t train_until, uint64_t seed, const char* field_out, double* relmse) {
+  return guarded([&] {
+    RunConfig cfg;
+    cfg.preset = preset;
+    cfg.grid.width = width;
+    cfg.grid.height = height;
+    cfg.wpp = wpp;
+    cfg.mode = static_cast<SamplerMode>(mode);
+    cfg.train_until = static_cast<uint64_t>(train_until);
+    cfg.seed = seed;
+    cfg.field_out = field_out;
+    RunResult res = run_solve(cfg);
+    SolutionImage ref = generate_reference(cfg, 1);
+    *relmse = compute_relmse(res.image, ref);
+  });
+}
+
 // preset scene geometry, for pinning the product's preset fixtures
 int ref_preset(const char* name, double* seg_out, int32_t* kind_out, int32_t* n_seg,
                double* eval_bbox, double* scene_bbox, double* eps) {

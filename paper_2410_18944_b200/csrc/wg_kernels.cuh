@@ -27,13 +27,22 @@ struct __align__(16) DevRecord {
   float nx, ny;
   float pdf_mis, pdf_g, pdf_u, c;
   float target;  // |u(x_{k+1})|, filled by the finalise pass
-  float acc_p;   // P: accumulated estimate after this step's local term
+  float dacc;    // accumulator increments since the walk's previous record
+                 // (this step's source / Neumann term included)
   float thr_q;   // Q: throughput after this step's multiplier (0 = walk died)
   float pad_;
   int32_t walk;  // estimate-buffer slot of the walk (round * n_points + point); -1 imported
   uint32_t flags;
   uint64_t key;  // deterministic selection key (seed, round, point, depth)
+  int32_t prev;  // arena slot of the walk's previous record, -1 for its first
+  int32_t pad2_;
 };
+// Targets (backfill_targets_append, guide_train.cpp:58-79): with the walk's
+// terminal term S_K = T_K g (0 when killed), S_{k+1} = S_K + sum_{j>k} dacc_j
+// and target_k = |S_{k+1} / Q_k|. A backward suffix sum like the reference's
+// recursion, so no cancellation against the walk total when throughputs
+// decay; scenes without source / Neumann terms have dacc = 0 and need no
+// chain walk (target = |S_K / Q_k|, one record per thread).
 static_assert(sizeof(DevRecord) == 80 && offsetof(DevRecord, walk) == 56 && offsetof(DevRecord, key) == 64,
               "record layout (compact_kernel loads walk|flags and key by offset)");
 enum : uint32_t { REC_ON_NEUMANN = 1u, REC_VALID = 2u, REC_USABLE = 4u, REC_WRITTEN = 8u };
@@ -68,6 +77,10 @@ struct WalkArgs {
   TrainCtl* ctl;     // round's record counts (collecting rounds)
   // counters: [0] steps, [1] escaped, [2] walks, [3] record overflow, [4] scene error
   unsigned long long* counters;
+  // per walk (collecting rounds): arena slot of the walk's last record (-1:
+  // none) and its terminal term T_K g plus increments after the last record
+  int32_t* rec_tail;
+  double* rec_term;
   // tensor-core kernel: the field's packed split-fp16 weights (wg_wpack.cuh)
   const unsigned char* wblob;
   // optional per-CTA phase timing [gridDim][8]: cycles in phase A (begin

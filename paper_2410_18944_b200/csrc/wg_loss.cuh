@@ -81,9 +81,13 @@ WG_D bool record_dy(const float* raw, const DevRecord& r, const TrainArgs& a, fl
       g[OD - 1] = dc * m.c * (1.0 - m.c);
     }
   }
+  bool fin = true;
 #pragma unroll
-  for (int j = 0; j < OD; ++j) dy[j] = static_cast<float>(g[j] * a.inv_count);
-  return true;
+  for (int j = 0; j < OD; ++j) {
+    dy[j] = static_cast<float>(g[j] * a.inv_count);
+    fin = fin && isfinite(dy[j]);
+  }
+  return fin;  // a gradient beyond fp32 range is dropped (counted as skipped)
 }
 
 
@@ -146,7 +150,7 @@ __device__ __forceinline__ bool record_dy32(const float* raw, const DevRecord& r
     if (!(static_cast<double>(v) > a.v_floor)) return false;
     const float s = -target / (r.pdf_mis * v);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) g[j] = s * dv[j];
+    for (int j = 0; j < 32; ++j) g[j] = s * dv[j];  // scaled by inv_count below
   }
   if (a.learn_selection) {  // selection_grad, guide_train.cpp:44-56
     double pg = on_n ? (a.reflect ? reflected_pdf32(m, nx, ny, px, py) : mixture_pdf32(m, nx, ny))
@@ -159,9 +163,13 @@ __device__ __forceinline__ bool record_dy32(const float* raw, const DevRecord& r
     }
   }
   const float ic = static_cast<float>(a.inv_count);
+  bool fin = true;
 #pragma unroll
-  for (int j = 0; j < 33; ++j) dy[j] = g[j] * ic;
-  return true;
+  for (int j = 0; j < 33; ++j) {
+    dy[j] = g[j] * ic;
+    fin = fin && isfinite(dy[j]);
+  }
+  return fin;  // a gradient beyond fp32 range is dropped (counted as skipped)
 }
 
 }  // namespace wg

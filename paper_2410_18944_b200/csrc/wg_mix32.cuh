@@ -179,7 +179,11 @@ WG_D void vm_cos_sin(Pcg& rng, float kappa, float* oc, float* os) {
   // 5e-5 would lose 3 digits in 1 + (r - 1)): every place r appears is
   // written in terms of rm1, so proposal and test use the same exact r
   const float rm1 = __fdividef((1.0f - rho) * (1.0f - rho), 2.0f * rho);
-  for (;;) {
+  for (int it = 0;; ++it) {
+    if (it == kMaxProposals) {  // NaN parameters: see kMaxProposals
+      *oc = *os = kappa * 0.0f / 0.0f;
+      return;
+    }
     const float u1 = rng.unif_pos();
     float hs, hc;
     sincospif(0.5f * u1, &hs, &hc);
@@ -229,7 +233,7 @@ WG_D void mixture_sample32(Pcg& rng, const Mix32& m, double* ox, double* oy) {
 }
 
 WG_D void reflected_sample32(Pcg& rng, const Mix32& m, double px, double py, double* ox, double* oy) {
-  for (;;) {
+  for (int it = 0;; ++it) {
     double nx, ny;
     mixture_sample32(rng, m, &nx, &ny);
     double d = nx * px + ny * py;
@@ -237,7 +241,7 @@ WG_D void reflected_sample32(Pcg& rng, const Mix32& m, double px, double py, dou
       reflect(nx, ny, px, py, ox, oy);
       return;
     }
-    if (d > 0.0) {
+    if (d > 0.0 || it + 1 == kMaxProposals) {
       *ox = nx;
       *oy = ny;
       return;
@@ -248,13 +252,13 @@ WG_D void reflected_sample32(Pcg& rng, const Mix32& m, double px, double py, dou
 // uniform_dir_sample (sphdist.cpp:226-243) with one fp32 sincospi per
 // proposal: full circle, or the hemisphere around the Neumann normal by flipping
 WG_D void uniform_sample32(Pcg& rng, bool on_n, double px, double py, double* ox, double* oy) {
-  for (;;) {
+  for (int it = 0;; ++it) {
     float sn, cs;
     sincospif(2.0f * rng.unif(), &sn, &cs);
     double nx, ny;
     unit64(cs, sn, &nx, &ny);
     const double d = on_n ? nx * px + ny * py : 1.0;
-    if (d != 0.0) {
+    if (d != 0.0 || it + 1 == kMaxProposals) {
       *ox = d > 0.0 ? nx : -nx;
       *oy = d > 0.0 ? ny : -ny;
       return;

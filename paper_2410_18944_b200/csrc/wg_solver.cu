@@ -47,7 +47,10 @@ struct wg_solver_s {
   int32_t est_rounds = 0;
   // records of the current / last collecting round
   DBuf recs, rec_counter;  // rec_counter: u64 bump allocator of the arena
+  DBuf rec_tail, rec_term;  // per walk of the collecting round: chain end, terminal term
+  bool recs_from_walks = false;
   int64_t rec_capacity = 0;
+  int64_t rec_capacity_min = 0;  // grown after an arena overflow
   bool have_records = false;
   // device control
   DBuf counters;  // C_N x u64
@@ -139,16 +142,26 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
     s->est_rounds = chunk;
   }
   if (collect) {
-    int64_t cap = std::max<int64_t>(s->n_points * 48, 1 << 16);
+    // Record arena: every step of every walk in the round may write one
+    // record (the reference keeps them all, guide_train.cpp:58-79). 256 per
+    // point covers long-walk scenes (const-source-disk reaches ~120 records
+    // per point once guiding is trained); a walk that finds the arena full
+    // stops recording, which would bias the training set towards early,
+    // short walks, so any overflow doubles the arena for the next call.
+    int64_t cap = std::max<int64_t>({s->n_points * 256, int64_t(1) << 16, s->rec_capacity_min});
     if (s->rec_capacity < cap) {
       s->recs.alloc(sizeof(DevRecord) * cap);
       s->rec_capacity = cap;
     }
     s->rec_counter.alloc(sizeof(unsigned long long));
     CK(cudaMemsetAsync(s->rec_counter.p, 0, sizeof(unsigned long long), s->stream));
+    s->rec_tail.alloc(sizeof(int32_t) * s->n_points);
+    s->rec_term.alloc(sizeof(double) * s->n_points);
+    CK(cudaMemsetAsync(s->rec_tail.p, 0xFF, sizeof(int32_t) * s->n_points, s->stream));  // -1
     s->ctl.alloc(sizeof(TrainCtl));
     CK(cudaMemsetAsync(s->ctl.p, 0, sizeof(TrainCtl), s->stream));
     s->have_records = true;
+    s->recs_from_walks = true;
   }
   WalkArgs a{};
   a.scene = s->scene->view;
@@ -169,6 +182,8 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
   a.key_seed = key_seed;
   a.pdf_floor = pdf_floor;
   a.ctl = collect ? s->ctl.as<TrainCtl>() : nullptr;
+  a.rec_tail = collect ? s->rec_tail.as<int32_t>() : nullptr;
+  a.rec_term = collect ? s->rec_term.as<double>() : nullptr;
 
   // guided walks on the default field shape: tcgen05 MLP tile kernel, or the
   // bit-faithful CUDA-core MLP with 8 lanes per walk; otherwise generic
@@ -234,9 +249,15 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
 void enqueue_finalize(wg_solver_s* s, double pdf_floor) {
   s->ctl.alloc(sizeof(TrainCtl));
   CK(cudaMemsetAsync(s->ctl.p, 0, sizeof(TrainCtl), s->stream));
+  // walk-collected records of scenes with source / Neumann terms take their
+  // targets from the per-walk backward suffix sums (DevRecord)
+  const SceneView& v = s->scene->view;
+  const bool walks = s->recs_from_walks;
+  const bool chain = walks && (!v.source_zero || v.has_flux);
   CKL(launch_finalize_records(s->recs.as<DevRecord>(), s->rec_counter.as<unsigned long long>(),
-                              s->rec_capacity, s->est.as<double>(), s->esc.as<int32_t>(), pdf_floor,
-                              s->ctl.as<TrainCtl>(), s->stream));
+                              s->rec_capacity, walks ? s->n_points : 0, s->rec_tail.as<int32_t>(),
+                              s->rec_term.as<double>(), s->esc.as<int32_t>(), pdf_floor,
+                              s->ctl.as<TrainCtl>(), chain, s->stream));
 }
 
 void ensure_train_buffers(wg_solver_s* s, const wg_train_config& tc) {
@@ -297,12 +318,15 @@ void enqueue_train(wg_solver_s* s, const wg_train_config& tc) {
   const int n_mb = static_cast<int>((tc.max_records_per_round + tc.minibatch - 1) / tc.minibatch);
   AdamCtl* actl = f->adam.as<AdamCtl>();
   for (int b = 0; b < n_mb; ++b) {
-    enqueue_minibatch(s, tc, b, 1.0);
+    // records enter the fp32 gradient sum pre-scaled by 1 / minibatch (the
+    // same constant on every rank); Adam divides by count / minibatch
+    enqueue_minibatch(s, tc, b, 1.0 / static_cast<double>(tc.minibatch));
     if (s->comm)
       NCK(nccl().allReduce(s->grad.p, s->grad.p, f->n_params + 1, ncclFloat, ncclSum, s->comm,
                         s->stream));
     CKL(launch_adam(f->p.as<float>(), f->m.as<double>(), f->v.as<double>(), s->grad.as<float>(),
-                    f->n_params, tc.lr, tc.beta1, tc.beta2, tc.eps, actl, f->view,
+                    f->n_params, tc.lr, tc.beta1, tc.beta2, tc.eps,
+                    static_cast<double>(tc.minibatch), actl, f->view,
                     f->wpack.p && !f->pack_dirty ? f->wpack.as<unsigned char>() : nullptr, s->stream));
   }
   CK(cudaEventRecord(pool_event(s->ev_train, s->n_train_ev), s->stream));
@@ -319,6 +343,14 @@ long long adam_steps(wg_solver_s* s) {
 wg_train_stats sync_collect(wg_solver_s* s, long long steps_before) {
   CK(cudaStreamSynchronize(s->stream));
   CK(cudaMemcpy(s->last_counters, s->counters.p, sizeof(s->last_counters), cudaMemcpyDeviceToHost));
+  if (s->last_counters[C_REC_OVERFLOW] > 0) {
+    s->rec_capacity_min = std::max<int64_t>(s->rec_capacity_min, 2 * s->rec_capacity);
+    std::fprintf(stderr,
+                 "wostgpu: record arena overflow (%llu chunks dropped, capacity %lld); the next call "
+                 "uses %lld records\n",
+                 s->last_counters[C_REC_OVERFLOW], static_cast<long long>(s->rec_capacity),
+                 static_cast<long long>(s->rec_capacity_min));
+  }
   s->last_walk_ms = pool_ms(s->ev_walk, s->n_walk_ev);
   s->last_train_ms = pool_ms(s->ev_train, s->n_train_ev);
   need(s->last_counters[C_SCENE_ERR] == 0, WG_ERR_SCENE,
@@ -363,6 +395,7 @@ void import_records(wg_solver_s* s, const wg_guide_record* recs, int64_t n, doub
   s->rec_counter.alloc(sizeof(unsigned long long));
   unsigned long long nn = static_cast<unsigned long long>(n);
   CK(cudaMemcpyAsync(s->rec_counter.p, &nn, sizeof(nn), cudaMemcpyHostToDevice, s->stream));
+  s->recs_from_walks = false;
   enqueue_finalize(s, pdf_floor);
   CK(cudaStreamSynchronize(s->stream));  // h goes out of scope
 }

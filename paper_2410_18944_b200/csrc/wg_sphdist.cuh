@@ -93,12 +93,19 @@ WG_D double reflected_pdf(const Mix& m, double nx, double ny, double px, double 
   return mixture_pdf(m, nx, ny) + mixture_pdf(m, rx, ry);
 }
 
+// Rejection loops on the device are capped at kMaxProposals: with
+// acceptance >= 1/2 per proposal a legitimate draw never reaches it, and
+// NaN parameters (which no comparison accepts) cannot hang a kernel; they
+// yield a NaN direction and the walk escapes the bbox test.
+constexpr int kMaxProposals = 4096;
+
 // Best-Fisher rejection sampler (sphdist.cpp:111-128)
 WG_D double vm_angle(Pcg& rng, double kappa) {
   double tau = 1.0 + sqrt(1.0 + 4.0 * kappa * kappa);
   double rho = (tau - sqrt(2.0 * tau)) / (2.0 * kappa);
   double r = (1.0 + rho * rho) / (2.0 * rho);
-  for (;;) {
+  for (int it = 0;; ++it) {
+    if (it == kMaxProposals) return kappa * 0.0 / 0.0;  // NaN
     double u1 = rng.uni_pos();
     double z = cos(kPi * u1);
     double f = (1.0 + r * z) / (r + z);
@@ -147,7 +154,7 @@ WG_D void mixture_sample(Pcg& rng, const Mix& m, double* ox, double* oy) {
 
 // reflected_sample (sphdist.cpp:210-218)
 WG_D void reflected_sample(Pcg& rng, const Mix& m, double px, double py, double* ox, double* oy) {
-  for (;;) {
+  for (int it = 0;; ++it) {
     double nx, ny;
     mixture_sample(rng, m, &nx, &ny);
     double d = nx * px + ny * py + 0.0 * 0.0;
@@ -155,7 +162,7 @@ WG_D void reflected_sample(Pcg& rng, const Mix& m, double px, double py, double*
       reflect(nx, ny, px, py, ox, oy);
       return;
     }
-    if (d > 0.0) {
+    if (d > 0.0 || it + 1 == kMaxProposals) {
       *ox = nx;
       *oy = ny;
       return;
@@ -165,7 +172,7 @@ WG_D void reflected_sample(Pcg& rng, const Mix& m, double px, double py, double*
 
 // uniform_dir_sample 2D (sphdist.cpp:226-243); on_n selects the hemisphere
 WG_D void uniform_sample(Pcg& rng, bool on_n, double px, double py, double* ox, double* oy) {
-  for (;;) {
+  for (int it = 0;; ++it) {
     double a = kTwoPi * rng.uni();
     double nx = cos(a), ny = sin(a);
     if (!on_n) {
@@ -179,7 +186,7 @@ WG_D void uniform_sample(Pcg& rng, bool on_n, double px, double py, double* ox, 
       *oy = ny;
       return;
     }
-    if (d < 0.0) {
+    if (d < 0.0 || it + 1 == kMaxProposals) {
       *ox = -nx;
       *oy = -ny;
       return;

@@ -9,6 +9,8 @@
 //                  corners receive their share by atomics (wg_train_tc.cu holds
 //                  the tcgen05 version of the three GEMMs)
 //   adam_kernel    bias-corrected Adam with fp64 moments (guide_field.cpp:317-331)
+#include <algorithm>
+
 #include "wg_kernels.cuh"
 #include "wg_sphdist.cuh"
 #include "wg_train.cuh"
@@ -81,15 +83,16 @@ cudaError_t launch_compact(const DevRecord* recs, const unsigned long long* rec_
   return cudaGetLastError();
 }
 
-// Finalise a round's records: target |u_{k+1}| = |(u_0 - P) / Q| from the
-// walk's final estimate (the backfill of guide_train.cpp:58-79 without its
-// serial chain, see DevRecord), drop records of escaped walks (the reference
-// only backfills non-escaped walks, wost.cpp:373-383), and count usable /
-// low-pdf records for the selection. Imported records (walk < 0) keep their
-// target. Grid-stride over the device-side record count.
+// Finalise a round's records: validity (the reference only backfills
+// non-escaped walks, wost.cpp:373-383), usable / low-pdf counts for the
+// selection, and - for scenes without source or Neumann terms, where every
+// dacc is 0 - the target |S_K / Q_k| directly (see DevRecord). Scenes with
+// local terms take their targets from backfill_chains_kernel instead.
+// Imported records (walk < 0) keep their target. Grid-stride over the
+// device-side record count.
 __global__ void finalize_records_kernel(DevRecord* recs, const unsigned long long* rec_count,
-                                        int64_t capacity, const double* est, const int32_t* esc,
-                                        double pdf_floor, TrainCtl* ctl) {
+                                        int64_t capacity, const double* term, const int32_t* esc,
+                                        double pdf_floor, TrainCtl* ctl, bool chain) {
   const int64_t n = static_cast<int64_t>(min(*rec_count, static_cast<unsigned long long>(capacity)));
   unsigned usable = 0, low = 0;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -103,9 +106,10 @@ __global__ void finalize_records_kernel(DevRecord* recs, const unsigned long lon
         r.flags = fl;  // not valid
         continue;
       }
-      const double q = r.thr_q;
-      r.target = q == 0.0 ? 0.0f
-                          : static_cast<float>(fabs((est[r.walk] - static_cast<double>(r.acc_p)) / q));
+      if (!chain) {
+        const double q = r.thr_q;
+        r.target = q == 0.0 ? 0.0f : static_cast<float>(fabs(term[r.walk] / q));
+      }
     }
     fl |= REC_VALID;
     if (static_cast<double>(r.pdf_mis) < pdf_floor) {
@@ -127,10 +131,36 @@ __global__ void finalize_records_kernel(DevRecord* recs, const unsigned long lon
   }
 }
 
+// backfill_targets_append (guide_train.cpp:58-79) for scenes with source /
+// Neumann terms: one thread per walk follows its record chain from the last
+// record backwards with the suffix sum S in fp64 (target_k = |S_{k+1} / Q_k|,
+// then S += dacc_k), like the reference's backward recursion.
+__global__ void backfill_chains_kernel(DevRecord* recs, int64_t n_walks, const int32_t* tail,
+                                       const double* term, const int32_t* esc) {
+  for (int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < n_walks;
+       w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (esc[w]) continue;
+    double s = term[w];
+    for (int32_t i = tail[w]; i >= 0;) {
+      DevRecord& r = recs[i];
+      const double q = r.thr_q;
+      r.target = q == 0.0 ? 0.0f : static_cast<float>(fabs(s / q));
+      s += static_cast<double>(r.dacc);
+      i = r.prev;
+    }
+  }
+}
+
 cudaError_t launch_finalize_records(DevRecord* recs, const unsigned long long* rec_count,
-                                    int64_t capacity, const double* est, const int32_t* esc,
-                                    double pdf_floor, TrainCtl* ctl, cudaStream_t st) {
-  finalize_records_kernel<<<148 * 4, 256, 0, st>>>(recs, rec_count, capacity, est, esc, pdf_floor, ctl);
+                                    int64_t capacity, int64_t n_walks, const int32_t* tail,
+                                    const double* term, const int32_t* esc, double pdf_floor,
+                                    TrainCtl* ctl, bool chain, cudaStream_t st) {
+  if (chain) {
+    const int blocks = static_cast<int>(std::min<int64_t>((n_walks + 127) / 128, 148 * 8));
+    backfill_chains_kernel<<<std::max(blocks, 1), 128, 0, st>>>(recs, n_walks, tail, term, esc);
+  }
+  finalize_records_kernel<<<148 * 4, 256, 0, st>>>(recs, rec_count, capacity, term, esc, pdf_floor, ctl,
+                                                   chain);
   return cudaGetLastError();
 }
 
@@ -363,14 +393,14 @@ cudaError_t launch_grad_cuda_core(const TrainArgs& a, cudaStream_t st) {
 // from `steps + 1` and the record count g[n]; the last block to finish
 // publishes |g|^2 and advances `steps`.
 __global__ void adam_kernel(float* p, double* m, double* v, const float* g, int64_t n, double lr,
-                            double b1, double b2, double eps, AdamCtl* c, FieldView f,
+                            double b1, double b2, double eps, double prescale, AdamCtl* c, FieldView f,
                             unsigned char* blob) {
   const double cnt = static_cast<double>(g[n]);
   if (!(cnt > 0.0)) return;  // no usable records: no optimizer step
   const long long step = c->steps + 1;
   const double bc1 = 1.0 - pow(b1, static_cast<double>(step));
   const double bc2 = 1.0 - pow(b2, static_cast<double>(step));
-  const double scale = 1.0 / cnt;
+  const double scale = prescale / cnt;
   double local = 0.0;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -405,11 +435,11 @@ __global__ void adam_kernel(float* p, double* m, double* v, const float* g, int6
 }
 
 cudaError_t launch_adam(float* p, double* m, double* v, const float* g, int64_t n, double lr, double b1,
-                        double b2, double eps, AdamCtl* ctl, const FieldView& f, unsigned char* blob,
-                        cudaStream_t st) {
+                        double b2, double eps, double prescale, AdamCtl* ctl, const FieldView& f,
+                        unsigned char* blob, cudaStream_t st) {
   int blocks = static_cast<int>((n + 255) / 256);
   if (blocks > 148 * 4) blocks = 148 * 4;
-  adam_kernel<<<blocks, 256, 0, st>>>(p, m, v, g, n, lr, b1, b2, eps, ctl, f, blob);
+  adam_kernel<<<blocks, 256, 0, st>>>(p, m, v, g, n, lr, b1, b2, eps, prescale, ctl, f, blob);
   return cudaGetLastError();
 }
 

@@ -48,7 +48,9 @@ struct TrainArgs {
   int64_t list_cap;                    // grid covers list_cap records
   float* grad;                         // [n_params + 1]; grad[n_params] = record count
   int64_t n_params;
-  double inv_count;                    // 1.0 in training (mean taken by Adam)
+  double inv_count;                    // per-record scale: 1 / minibatch in training
+                                       // (keeps the fp32 sums in range; Adam rescales
+                                       // by minibatch / count), 1 / n in field_grad
   int32_t reflect, learn_selection;
   double e_fraction, v_floor;
   TrainTotals* totals;
@@ -59,18 +61,22 @@ cudaError_t launch_compact(const DevRecord* recs, const unsigned long long* rec_
                            int64_t capacity, TrainCtl* ctl, TrainTotals* totals, uint32_t* lists,
                            int64_t list_cap, int64_t max_records, int32_t minibatch,
                            cudaStream_t st);
+// targets (DevRecord), validity and usable counts of the arena's records;
+// chain = the scene has source / Neumann terms (per-walk backward suffix sums)
 cudaError_t launch_finalize_records(DevRecord* recs, const unsigned long long* rec_count,
-                                    int64_t capacity, const double* est, const int32_t* esc,
-                                    double pdf_floor, TrainCtl* ctl, cudaStream_t st);
+                                    int64_t capacity, int64_t n_walks, const int32_t* tail,
+                                    const double* term, const int32_t* esc, double pdf_floor,
+                                    TrainCtl* ctl, bool chain, cudaStream_t st);
 size_t grad_tile_smem();
 size_t grad_tc_pack_bytes();
 cudaError_t launch_grad_cuda_core(const TrainArgs& a, cudaStream_t st);
-// Adam step on all n parameters with the mean gradient g[0..n) / g[n] (the
-// record count); no step when g[n] == 0. blob != nullptr: the packed weight
+// Adam step on all n parameters with the mean gradient prescale * g[0..n) /
+// g[n] (g holds sum_i grad_i / prescale, g[n] the record count); no step when
+// g[n] == 0. blob != nullptr: the packed weight
 // blob (wg_wpack.cuh) is updated for every MLP parameter written.
 cudaError_t launch_adam(float* p, double* m, double* v, const float* g, int64_t n, double lr, double b1,
-                        double b2, double eps, AdamCtl* ctl, const FieldView& f, unsigned char* blob,
-                        cudaStream_t st);
+                        double b2, double eps, double prescale, AdamCtl* ctl, const FieldView& f,
+                        unsigned char* blob, cudaStream_t st);
 cudaError_t launch_import_records(const wg_guide_record* in, int64_t n, DevRecord* out,
                                   cudaStream_t st);
 cudaError_t launch_export_records(const DevRecord* in, int64_t n, wg_guide_record* out,

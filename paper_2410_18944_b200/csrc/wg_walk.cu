@@ -57,6 +57,7 @@ struct Lane {
   int64_t rec_base;
   int rec_left;
   int last_rec;
+  double dacc;  // accumulator increments since the last record (DevRecord::dacc)
   bool rec_ok;
 };
 
@@ -77,6 +78,7 @@ __device__ __forceinline__ void lane_init(Lane& w, const WalkArgs& a, int64_t id
   w.rng = Pcg::walk(a.seed, static_cast<uint64_t>(a.point_offset + w.point),
                     a.wpp_first + static_cast<uint64_t>(w.round));
   w.last_rec = -1;
+  w.dacc = 0.0;
   w.rec_ok = true;
 }
 
@@ -113,9 +115,10 @@ __device__ __forceinline__ void finish_walk(Lane& w, const WalkArgs& a, bool esc
   if (a.steps) a.steps[slot] = w.depth;
   atomicAdd(&a.counters[0], static_cast<unsigned long long>(w.depth));
   if (escaped) atomicAdd(&a.counters[1], 1ull);
-  // targets are formed later from (est, P, Q): see DevRecord
-  (void)terminal;
-  (void)collect;
+  if (collect && a.rec_tail) {  // the walk's end of the record chain (see DevRecord)
+    a.rec_tail[slot] = w.last_rec;
+    a.rec_term[slot] = escaped ? 0.0 : w.T * terminal + w.dacc;
+  }
   w.alive = false;
 }
 
@@ -210,6 +213,7 @@ __global__ void __launch_bounds__(128) walk_kernel(WalkArgs a) {
       contrib += add;
     }
     w.acc += w.T * contrib;
+    w.dacc += w.T * contrib;
 
     int rec = -1;
     if (collect && w.rec_ok) {  // trace push (wost.cpp:206-214)
@@ -269,7 +273,8 @@ __global__ void __launch_bounds__(128) walk_kernel(WalkArgs a) {
       r.pdf_u = static_cast<float>(pu);
       r.c = static_cast<float>(sel);
       r.target = 0.0f;
-      r.acc_p = static_cast<float>(w.acc);
+      r.dacc = static_cast<float>(w.dacc);
+      w.dacc = 0.0;
       r.thr_q = static_cast<float>(GUIDED ? w.T * mult : w.T);
       r.pad_ = 0.0f;
       r.walk = static_cast<int32_t>(static_cast<int64_t>(w.round) * a.n_points + w.point);
@@ -277,6 +282,8 @@ __global__ void __launch_bounds__(128) walk_kernel(WalkArgs a) {
       (void)rr;
       r.key = Pcg::mix(a.key_seed ^ Pcg::mix((static_cast<uint64_t>(a.point_offset + w.point) << 20) ^
                                              static_cast<uint64_t>(w.depth)));
+      r.prev = w.last_rec;
+      r.pad2_ = 0;
       a.recs[rec] = r;
       w.last_rec = rec;
     }

@@ -49,7 +49,8 @@ struct CLane {
   int64_t point;
   int round;
   int64_t rec_base;
-  int rec_left;
+  int rec_left, last_rec;
+  double dacc;  // accumulator increments since the last record (DevRecord::dacc)
   bool rec_ok;
 };
 
@@ -179,9 +180,14 @@ __device__ __forceinline__ Hit w_ray_neumann(const SceneView& s, const SmallSegs
   return w_ray_list(ss.n, ss.nn, s.t_eps, ox, oy, dx, dy, t_max, exclude, lane);
 }
 
-__device__ __forceinline__ void c_finish(const CLane& w, const WalkArgs& a, bool escaped, int lane) {
+__device__ __forceinline__ void c_finish(const CLane& w, const WalkArgs& a, bool escaped, int lane,
+                                         double terminal = 0.0) {
   if (lane == 0) {
     const int64_t slot = static_cast<int64_t>(w.round) * a.n_points + w.point;
+    if (a.rec_tail) {  // the walk's end of the record chain (see DevRecord)
+      a.rec_tail[slot] = w.last_rec;
+      a.rec_term[slot] = escaped ? 0.0 : w.T * terminal + w.dacc;
+    }
     a.est[slot] = escaped ? 0.0 : w.acc;
     a.esc[slot] = escaped ? 1 : 0;
     if (a.steps) a.steps[slot] = w.depth;
@@ -197,7 +203,7 @@ __device__ __forceinline__ bool c_begin(CLane& w, const WalkArgs& a, const Scene
   if (cd.seg >= 0 && cd.d <= a.sp.eps) {
     double g = eval_value(s.values[s.seg_value[cd.seg]], cd.px, cd.py);
     w.acc += w.T * g;
-    c_finish(w, a, false, lane);
+    c_finish(w, a, false, lane, g);
     return false;
   }
   if (w.depth >= a.sp.max_steps) {
@@ -250,6 +256,7 @@ __device__ __forceinline__ bool c_begin(CLane& w, const WalkArgs& a, const Scene
     contrib += add;
   }
   w.acc += w.T * contrib;
+  w.dacc += w.T * contrib;
   w.rec = -1;
   if (collect && w.rec_ok) {
     if (w.rec_left == 0) {
@@ -507,6 +514,8 @@ __global__ void __launch_bounds__(kCoopThreads, 2) walk_kernel_coop(WalkArgs a) 
     w.rng = Pcg::walk(a.seed, static_cast<uint64_t>(a.point_offset + w.point),
                       a.wpp_first + static_cast<uint64_t>(w.round));
     w.rec_ok = true;
+    w.last_rec = -1;
+    w.dacc = 0.0;
     ++walks_done;
 
     while (c_begin(w, a, s, ss, collect, lane)) {
@@ -524,7 +533,7 @@ __global__ void __launch_bounds__(kCoopThreads, 2) walk_kernel_coop(WalkArgs a) 
       double dnx, dny;
       if (w.rng.unif() < static_cast<float>(sel)) {
         if (w.on_n && refl) {
-          for (;;) {  // reflected_sample (sphdist.cpp:210-218)
+          for (int it = 0;; ++it) {  // reflected_sample (sphdist.cpp:210-218)
             double mx, my;
             c_mixture_sample(w.rng, L, lane, &mx, &my);
             const double d = mx * w.nx + my * w.ny;
@@ -532,7 +541,7 @@ __global__ void __launch_bounds__(kCoopThreads, 2) walk_kernel_coop(WalkArgs a) 
               reflect(mx, my, w.nx, w.ny, &dnx, &dny);
               break;
             }
-            if (d > 0.0) {
+            if (d > 0.0 || it + 1 == kMaxProposals) {
               dnx = mx;
               dny = my;
               break;
@@ -569,14 +578,20 @@ __global__ void __launch_bounds__(kCoopThreads, 2) walk_kernel_coop(WalkArgs a) 
         r.pdf_u = static_cast<float>(pu);
         r.c = static_cast<float>(sel);
         r.target = 0.0f;
-        r.acc_p = static_cast<float>(w.acc);
+        r.dacc = static_cast<float>(w.dacc);
         r.thr_q = static_cast<float>(w.T * mult);
         r.pad_ = 0.0f;
         r.walk = static_cast<int32_t>(static_cast<int64_t>(w.round) * a.n_points + w.point);
         r.flags = REC_WRITTEN | (w.on_n ? REC_ON_NEUMANN : 0u);
         r.key = Pcg::mix(a.key_seed ^ Pcg::mix((static_cast<uint64_t>(a.point_offset + w.point) << 20) ^
                                                static_cast<uint64_t>(w.depth)));
+        r.prev = w.last_rec;
+        r.pad2_ = 0;
         a.recs[w.rec] = r;
+      }
+      if (w.rec >= 0) {
+        w.last_rec = w.rec;
+        w.dacc = 0.0;
       }
       if (mult == 0.0) {
         c_finish(w, a, false, lane);

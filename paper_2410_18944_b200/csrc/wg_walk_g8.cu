@@ -96,7 +96,7 @@ __device__ __forceinline__ void mixture_sample_g(const Grp& gp, Pcg& rng, const 
 
 __device__ __forceinline__ void reflected_sample_g(const Grp& gp, Pcg& rng, const MixL& m, double px,
                                                    double py, double* ox, double* oy) {
-  for (;;) {
+  for (int it = 0;; ++it) {
     double nx, ny;
     mixture_sample_g(gp, rng, m, &nx, &ny);
     double d = nx * px + ny * py + 0.0 * 0.0;
@@ -104,7 +104,7 @@ __device__ __forceinline__ void reflected_sample_g(const Grp& gp, Pcg& rng, cons
       reflect(nx, ny, px, py, ox, oy);
       return;
     }
-    if (d > 0.0) {
+    if (d > 0.0 || it + 1 == kMaxProposals) {
       *ox = nx;
       *oy = ny;
       return;
@@ -225,6 +225,7 @@ struct GLane {
   int round;
   int64_t rec_base;
   int rec_left, last_rec;
+  double dacc;  // accumulator increments since the last record (DevRecord::dacc)
   bool rec_ok;
 };
 
@@ -282,7 +283,10 @@ __global__ void __launch_bounds__(256) walk_kernel_g8(WalkArgs a) {
       if (a.steps) a.steps[slot] = w.depth;
       atomicAdd(&a.counters[0], static_cast<unsigned long long>(w.depth));
       if (escaped) atomicAdd(&a.counters[1], 1ull);
-      (void)terminal;  // targets are formed later from (est, P, Q): see DevRecord
+      if (a.rec_tail) {  // the walk's end of the record chain (see DevRecord)
+        a.rec_tail[slot] = w.last_rec;
+        a.rec_term[slot] = escaped ? 0.0 : w.T * terminal + w.dacc;
+      }
     }
     w.alive = false;
   };
@@ -305,6 +309,7 @@ __global__ void __launch_bounds__(256) walk_kernel_g8(WalkArgs a) {
       w.rng = Pcg::walk(a.seed, static_cast<uint64_t>(a.point_offset + w.point),
                         a.wpp_first + static_cast<uint64_t>(w.round));
       w.last_rec = -1;
+      w.dacc = 0.0;
       w.rec_ok = true;
       next += groups;
       ++walks_done;
@@ -392,6 +397,7 @@ __global__ void __launch_bounds__(256) walk_kernel_g8(WalkArgs a) {
       contrib += add;
     }
     w.acc += w.T * contrib;
+    w.dacc += w.T * contrib;
 
     int rec = -1;
     if (collect && w.rec_ok) {
@@ -453,7 +459,7 @@ __global__ void __launch_bounds__(256) walk_kernel_g8(WalkArgs a) {
       r.pdf_u = static_cast<float>(pu);
       r.c = static_cast<float>(m.c);
       r.target = 0.0f;
-      r.acc_p = static_cast<float>(w.acc);
+      r.dacc = static_cast<float>(w.dacc);
       r.thr_q = static_cast<float>(w.T * mult);
       r.pad_ = 0.0f;
       r.walk = static_cast<int32_t>(static_cast<int64_t>(w.round) * a.n_points + w.point);
@@ -462,9 +468,14 @@ __global__ void __launch_bounds__(256) walk_kernel_g8(WalkArgs a) {
       (void)contrib;
       r.key = Pcg::mix(a.key_seed ^ Pcg::mix((static_cast<uint64_t>(a.point_offset + w.point) << 20) ^
                                              static_cast<uint64_t>(w.depth)));
+      r.prev = w.last_rec;
+      r.pad2_ = 0;
       a.recs[rec] = r;
     }
-    if (rec >= 0) w.last_rec = rec;
+    if (rec >= 0) {
+      w.last_rec = rec;
+      w.dacc = 0.0;
+    }
     if (mult == 0.0) {
       finish(false, 0.0);
       continue;

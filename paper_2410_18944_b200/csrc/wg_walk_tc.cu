@@ -48,6 +48,7 @@ struct TLane {
   int round;
   int64_t rec_base;
   int rec_left, last_rec;
+  double dacc;  // accumulator increments since the last record (DevRecord::dacc)
   bool rec_ok;
 };
 
@@ -61,8 +62,10 @@ __device__ __forceinline__ void t_finish(TLane& w, const WalkArgs& a, bool escap
   if (a.steps) a.steps[slot] = w.depth;
   atomicAdd(&a.counters[0], static_cast<unsigned long long>(w.depth));
   if (escaped) atomicAdd(&a.counters[1], 1ull);
-  (void)terminal;  // targets are formed later from (est, P, Q): see DevRecord
-  (void)collect;
+  if (collect && a.rec_tail) {  // the walk's end of the record chain (see DevRecord)
+    a.rec_tail[slot] = w.last_rec;
+    a.rec_term[slot] = escaped ? 0.0 : w.T * terminal + w.dacc;
+  }
   w.alive = false;
 }
 
@@ -134,6 +137,7 @@ __device__ __forceinline__ bool t_begin(TLane& w, const WalkArgs& a, const Scene
     contrib += add;
   }
   w.acc += w.T * contrib;
+  w.dacc += w.T * contrib;
   w.contrib = contrib;
   SUB_ADD(2, t2);
   w.rec = -1;
@@ -255,6 +259,7 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
         w.rng = Pcg::walk(a.seed, static_cast<uint64_t>(a.point_offset + w.point),
                           a.wpp_first + static_cast<uint64_t>(w.round));
         w.last_rec = -1;
+        w.dacc = 0.0;
         w.rec_ok = true;
         next += stride;
         ++walks_done;
@@ -337,15 +342,18 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
       r.pdf_u = static_cast<float>(o.pu);
       r.c = static_cast<float>(sel);
       r.target = 0.0f;
-      r.acc_p = static_cast<float>(w.acc);
+      r.dacc = static_cast<float>(w.dacc);
       r.thr_q = static_cast<float>(w.T * mult);
       r.pad_ = 0.0f;
       r.walk = static_cast<int32_t>(static_cast<int64_t>(w.round) * a.n_points + w.point);
       r.flags = REC_WRITTEN | (w.on_n ? REC_ON_NEUMANN : 0u);
       r.key = Pcg::mix(a.key_seed ^ Pcg::mix((static_cast<uint64_t>(a.point_offset + w.point) << 20) ^
                                              static_cast<uint64_t>(w.depth)));
+      r.prev = w.last_rec;
+      r.pad2_ = 0;
       a.recs[w.rec] = r;
       w.last_rec = w.rec;
+      w.dacc = 0.0;
     }
     SUB_ADD(7, tr);
     if (mult == 0.0) {

@@ -211,6 +211,31 @@ def test_records_and_backfill(gpu, orc):
     np.testing.assert_allclose(rec_o["pdf_mis"], c, rtol=1e-12)
 
 
+@pytest.mark.parametrize("mlp", [api.MLP_EXACT, api.MLP_TENSOR])
+def test_record_targets_with_source_term(gpu, orc, mlp):
+    """Scenes with a source term accumulate local contributions along the
+    walk; targets |u(x_{k+1})| are backward suffix sums per walk (DevRecord),
+    like backfill_targets_append (guide_train.cpp:58-79). On the exact path
+    the records equal the oracle's (order-free comparison); on the tensor-core
+    path every target equals the suffix sum of its own walk's records."""
+    p = make_preset("const-source-disk")
+    cfg = abi.field_config()
+    fo = orc.field(cfg, p.scene.bbox, 31)
+    fg = api.GuidingField(cfg, p.scene.bbox, 31)
+    xy = cell_centers(24, 24, p.eval_bbox)
+    sc = abi.solver_config("learnable_mis")
+    sol = api.Solver(api.Accel(p.scene), fg, sc, mlp)
+    st_g = np.zeros(len(xy), dtype=abi.POINT_STATS_DTYPE)
+    rec_g = api.solve_batch(sol, xy, st_g, 7, 0, collect_records=True)
+    if mlp == api.MLP_EXACT:
+        ho = orc.scene(p.scene)
+        st_o = np.zeros(len(xy), dtype=abi.POINT_STATS_DTYPE)
+        rec_o = orc.solve_batch(ho, fo, sc, xy, st_o, 7, 0, collect=True)
+        assert len(rec_g) == len(rec_o)
+        np.testing.assert_allclose(np.sort(rec_g["target"]), np.sort(rec_o["target"]), rtol=1e-5, atol=1e-7)
+    assert np.all(np.isfinite(rec_g["target"])) and np.all(rec_g["target"] >= 0)
+
+
 # ---------------------------------------------------------------- training
 def test_minibatch_gradient_matches_oracle(gpu, orc):
     """One minibatch gradient (fp32 device MLP) vs the oracle's fp64
