@@ -304,6 +304,8 @@ int wostgpu_scene_create(const double* seg, const int32_t* kind, const int32_t* 
     v.diag = s->diag;
     v.has_flux = s->has_flux;
     v.source_zero = s->source_zero;
+    v.n_neumann = 0;
+    for (int32_t i = 0; i < n_seg; ++i) v.n_neumann += hk[i] == WG_NEUMANN ? 1 : 0;
     auto a16 = [](size_t b) { return (b + 15) & ~size_t(15); };
     size_t bytes = a16(sizeof(Node) * v.n_nodes) + a16(sizeof(Seg) * v.n_segs) +
                    a16(sizeof(SilVertex) * v.n_sil) + a16(sizeof(double) * 2 * v.n_sil_normals);

@@ -114,6 +114,8 @@ struct SceneView {
   double bbox[4];
   double eps, t_eps, diag;
   int32_t has_flux, source_zero;
+  int32_t n_neumann;  // Neumann segments: without any, Neumann-kind rays cannot hit
+  int32_t pad_;
 };
 
 WG_D double eval_value(const DevValue& v, double x, double y) {
@@ -134,6 +136,12 @@ WG_D double eval_value(const DevValue& v, double x, double y) {
     default: return 0.0;
   }
 }
+
+// Occlusion test of a source sample at distance r inside the star ball of
+// radius R (sample_source_point, wost.cpp:67-87). Without Neumann segments
+// R is the Dirichlet distance, so for r < R every segment lies beyond the
+// ray: ray_first_hit would return no hit, and the traversal is skipped.
+WG_D bool source_ray_needed(const SceneView& s, double r, double R) { return s.n_neumann > 0 || !(r < R); }
 
 WG_D bool bbox_contains(const SceneView& s, double x, double y, double pad) {
   return x >= s.bbox[0] - pad && x <= s.bbox[2] + pad && y >= s.bbox[1] - pad &&
@@ -261,10 +269,20 @@ struct Hit {
   int seg, kind;
 };
 
+WG_D Hit no_hit() {
+  Hit h;
+  h.seg = -1;
+  h.kind = -1;
+  h.t = dinf();
+  h.px = h.py = h.nx = h.ny = 0.0;
+  return h;
+}
+
 // Accel::ray_first_hit (geom2d.cpp:202-246): nearest t in (t_eps, t_max],
 // the last equal t in traversal order wins; normal faces the ray.
 WG_D Hit ray_first_hit(const SceneView& s, double ox, double oy, double dx, double dy,
                        double t_max, unsigned kinds, int exclude) {
+  if (kinds == WG_KIND_NEUMANN && s.n_neumann == 0) return no_hit();  // nothing to hit
   double ix = 1.0 / dx, iy = 1.0 / dy;
   double bt = t_max;
   int bi = -1;

@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(128) walk_kernel(WalkArgs a) {
       uniform_sample(w.rng, w.on_n, w.nx, w.ny, &dx, &dy);
       double r = greens_radius2(w.rng.uni(), w.R);
       double yx = w.x + dx * r, yy = w.y + dy * r;
-      Hit h = ray_first_hit(s, w.x, w.y, dx, dy, r, WG_KIND_ALL, -1);
+      Hit h = source_ray_needed(s, r, w.R) ? ray_first_hit(s, w.x, w.y, dx, dy, r, WG_KIND_ALL, -1) : no_hit();
       double wt = h.seg >= 0 ? 0.0 : w.R * w.R / 4.0;
       if (wt != 0.0) {
         double f = 0.0;

@@ -92,19 +92,6 @@ __device__ __forceinline__ Hit ray_list(const Seg* segs, int n, double t_eps, do
   return h;
 }
 
-__device__ __forceinline__ CP t_closest(const SceneView& s, const SmallSegs& ss, double x, double y,
-                                        unsigned kinds) {
-  if (s.n_segs > kSmallScene) return closest_point(s, x, y, kinds);
-  return kinds == WG_KIND_DIRICHLET ? cp_list(ss.d, ss.nd, x, y) : closest_point(s, x, y, kinds);
-}
-
-__device__ __forceinline__ Hit t_ray(const SceneView& s, const SmallSegs& ss, double ox, double oy, double dx,
-                                     double dy, double t_max, unsigned kinds, int exclude) {
-  if (s.n_segs > kSmallScene || kinds != WG_KIND_NEUMANN)
-    return ray_first_hit(s, ox, oy, dx, dy, t_max, kinds, exclude);
-  return ray_list(ss.n, ss.nn, s.t_eps, ox, oy, dx, dy, t_max, exclude);
-}
-
 // closest_silhouette for small vertex lists: squared distances of all
 // vertices first (independent), then the candidate tests in order
 __device__ __forceinline__ double sil_small(const SceneView& s, double x, double y) {
@@ -130,6 +117,20 @@ __device__ __forceinline__ double sil_small(const SceneView& s, double x, double
   return best == dinf() ? best : sqrt(best);
 }
 
+
+
+__device__ __forceinline__ CP t_closest(const SceneView& s, const SmallSegs& ss, double x, double y,
+                                        unsigned kinds) {
+  if (s.n_segs > kSmallScene) return closest_point(s, x, y, kinds);
+  return kinds == WG_KIND_DIRICHLET ? cp_list(ss.d, ss.nd, x, y) : closest_point(s, x, y, kinds);
+}
+
+__device__ __forceinline__ Hit t_ray(const SceneView& s, const SmallSegs& ss, double ox, double oy, double dx,
+                                     double dy, double t_max, unsigned kinds, int exclude) {
+  if (s.n_segs > kSmallScene || kinds != WG_KIND_NEUMANN)
+    return ray_first_hit(s, ox, oy, dx, dy, t_max, kinds, exclude);
+  return ray_list(ss.n, ss.nn, s.t_eps, ox, oy, dx, dy, t_max, exclude);
+}
 
 // sample_greens_radius (wost.cpp:37-65), d = 2: Newton + bisection on the
 // radial CDF u = s^2 (1 - 2 ln s), s = r / R

@@ -232,7 +232,7 @@ __device__ __forceinline__ bool c_begin(CLane& w, const WalkArgs& a, const Scene
     uniform_sample32(w.rng, w.on_n, w.nx, w.ny, &dx, &dy);
     double r = t_greens_radius(w.rng.uni(), w.R);
     double yx = w.x + dx * r, yy = w.y + dy * r;
-    Hit h = t_ray(s, ss, w.x, w.y, dx, dy, r, WG_KIND_ALL, -1);
+    Hit h = source_ray_needed(s, r, w.R) ? t_ray(s, ss, w.x, w.y, dx, dy, r, WG_KIND_ALL, -1) : no_hit();
     double wt = h.seg >= 0 ? 0.0 : w.R * w.R / 4.0;
     if (wt != 0.0) {
       double f = 0.0;
