@@ -233,8 +233,13 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
         if (tot(b) > tot(worst)) worst = b;
       const unsigned long long* q = &h[8 * worst];
       double it = static_cast<double>(std::max<unsigned long long>(q[3], 1));
-      std::fprintf(stderr, "[phase] cta %d iters %.0f cycles/iter A %.0f B %.0f (gather %.0f prep %.0f mma %.0f) C %.0f\n",
-                   worst, it, q[0] / it, q[1] / it, q[5] / it, q[6] / it, q[4] / it, q[2] / it);
+      const double small_it = static_cast<double>(q[6] >> 40);
+      const double prep = static_cast<double>(q[6] & ((1ull << 40) - 1));
+      std::fprintf(stderr,
+                   "[phase] cta %d iters %.0f cycles/iter A %.0f B %.0f (gather %.0f prep %.0f mma %.0f) C %.0f; "
+                   "small-MLP iters %.0f at %.0f cycles\n",
+                   worst, it, q[0] / it, q[1] / it, q[5] / it, prep / it, q[4] / it, q[2] / it, small_it,
+                   small_it > 0 ? q[7] / small_it : 0.0);
     }
     if (tc) {
     } else if (coop) CKL(launch_walks_coop(a, std::max(1, blocks), s->stream));

@@ -54,6 +54,111 @@ struct TLane {
 
 __host__ __device__ __forceinline__ size_t al16(size_t b) { return (b + 15) & ~size_t(15); }
 
+// Tail iterations: once at most kSmallRows slots of a CTA still need a
+// direction (the longest walks of a round; most of a round's iterations),
+// the CTA evaluates their MLP rows on CUDA cores instead of an M = 128 tile:
+// ~1-1.5k cycles against ~6.5k for the three tensor-core layer round trips.
+// fp32 weights staged once per launch; layers 1-2 map thread t to hidden unit
+// t % 64 for every second row (each weight load reused across rows).
+constexpr int kSmallRows = 16;
+
+struct SmallMlp {
+  float w1[16][64], b1[64];
+  float w2[64][64], b2[64];
+  float w3[64][33], b3[36];
+  float x[kSmallRows][16];
+  float h1[kSmallRows][64], h2[kSmallRows][64];
+  float r[kSmallRows][33];
+  int slot_count;
+};
+
+__device__ __forceinline__ void small_stage(SmallMlp& M, const FieldView& f) {
+  for (int e = threadIdx.x; e < 16 * 64; e += blockDim.x) M.w1[e / 64][e % 64] = f.p[f.w1 + e];
+  for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) M.w2[e / 64][e % 64] = f.p[f.w2 + e];
+  for (int e = threadIdx.x; e < 64 * 33; e += blockDim.x) M.w3[e / 33][e % 33] = f.p[f.w3 + e];
+  for (int e = threadIdx.x; e < 64; e += blockDim.x) {
+    M.b1[e] = f.p[f.b1 + e];
+    M.b2[e] = f.p[f.b2 + e];
+  }
+  for (int e = threadIdx.x; e < 33; e += blockDim.x) M.b3[e] = f.p[f.b3 + e];
+}
+
+// layers 1-2: thread t -> hidden unit t % 64, rows h, h + 2, ... (h = t / 64)
+// up to 2Q rows per pass; Q is chosen from the live row count so no
+// predicated-off row costs issue slots
+template <int K, int Q>
+__device__ __forceinline__ void small_layer(const float (*w)[64], const float* b, const float* in, int in_stride,
+                                            float* out, int n) {
+  const int j = threadIdx.x & 63, h = threadIdx.x >> 6;  // 128 threads: 2 row groups
+  for (int r0 = 0; r0 < n; r0 += 2 * Q) {
+    float acc[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) acc[q] = b[j];
+#pragma unroll 8
+    for (int k = 0; k < K; ++k) {
+      const float wk = w[k][j];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) acc[q] = fmaf(wk, in[(r0 + h + 2 * q) * in_stride + k], acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+      if (r0 + h + 2 * q < n) out[(r0 + h + 2 * q) * 64 + j] = fmaxf(acc[q], 0.0f);
+  }
+}
+
+// layer 3: thread t -> output t / 4 (0..31) over K quarter t % 4 (shuffle
+// reduced), Q rows per pass; output 32 by warp 0 with a warp reduction
+template <int Q>
+__device__ __forceinline__ void small_layer3(SmallMlp& M, int n) {
+  const int t = threadIdx.x, o = t >> 2, p = t & 3;
+  for (int r0 = 0; r0 < n; r0 += Q) {
+    float acc[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) acc[q] = 0.0f;
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      const int k = 16 * p + kk;
+      const float wk = M.w3[k][o];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) acc[q] = fmaf(wk, M.h2[r0 + q][k], acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 1);
+      acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 2);
+      if (p == 0 && r0 + q < n) M.r[r0 + q][o] = acc[q] + M.b3[o];
+    }
+  }
+  if (t < 32) {
+    for (int r = 0; r < n; ++r) {
+      float v = fmaf(M.w3[t][32], M.h2[r][t], M.w3[t + 32][32] * M.h2[r][t + 32]);
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o2);
+      if (t == 0) M.r[r][32] = v + M.b3[32];
+    }
+  }
+}
+
+template <int Q>
+__device__ __forceinline__ void small_mlp_q(SmallMlp& M, int n) {
+  small_layer<16, Q>(M.w1, M.b1, &M.x[0][0], 16, &M.h1[0][0], n);
+  __syncthreads();
+  small_layer<64, Q>(M.w2, M.b2, &M.h1[0][0], 64, &M.h2[0][0], n);
+  __syncthreads();
+  small_layer3<2 * Q>(M, n);
+  __syncthreads();
+}
+
+// MLP rows 0..n-1 of M.x -> M.r (raw outputs); all threads, barriers inside.
+// Rows n..kSmallRows-1 of x / h1 / h2 may hold stale values: they are read
+// by the unrolled row loops but never written back.
+__device__ __forceinline__ void small_mlp(SmallMlp& M, int n) {
+  if (n <= 2) small_mlp_q<1>(M, n);
+  else if (n <= 4) small_mlp_q<2>(M, n);
+  else if (n <= 8) small_mlp_q<4>(M, n);
+  else small_mlp_q<8>(M, n);
+}
+
 __device__ __forceinline__ void t_finish(TLane& w, const WalkArgs& a, bool escaped, double terminal,
                                          bool collect) {
   const int64_t slot = static_cast<int64_t>(w.round) * a.n_points + w.point;
@@ -170,7 +275,7 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
   unsigned char* tc = smem;  // TcLayout block first (128-B aligned)
   SceneView s = a.scene;
   if (a.scene_smem_bytes > 0) {
-    unsigned char* p = smem + al16(kWarp ? TcLayoutW::BYTES : TcLayout::BYTES);
+    unsigned char* p = smem + al16(kWarp ? TcLayoutW::BYTES : TcLayout::BYTES + sizeof(SmallMlp));
     size_t off = 0;
     auto carve = [&](size_t bytes) {
       unsigned char* q = p + off;
@@ -204,11 +309,13 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
     seg_counts[1] = nn;
   }
   SmallSegs ss{seg_lists, seg_lists + kSmallScene, 0, 0};
+  SmallMlp& small = *reinterpret_cast<SmallMlp*>(smem + TcLayout::BYTES);  // lockstep kernel only
   if (kWarp) {
     tcw_stage_weights(tc, a.field);
   } else {
     tc_fetch_weights(tc, a.wblob);
     tc_setup(tc);
+    small_stage(small, a.field);
   }
   umma::fence_before();
   __syncthreads();
@@ -239,6 +346,7 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
       if (threadIdx.x == 0) a.phase_prof[8 * blockIdx.x + 2] += static_cast<unsigned long long>(t_top - t_iter);
       t_iter = t_top;
     }
+    if (!kWarp && threadIdx.x == 0) small.slot_count = 0;  // consumed after the phase-A barrier
     // ---- phase A: every slot advances to a walk that needs a direction
     bool need = false;
     for (;;) {
@@ -269,10 +377,12 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
         break;
       }
     }
+    int active = 0;
     if (kWarp) {
       if (!__any_sync(0xffffffffu, need)) break;
     } else {
-      if (!__syncthreads_or(need)) break;
+      active = __syncthreads_count(need);
+      if (active == 0) break;
     }
     long long t_b = a.phase_prof ? clock64() : 0;
     if (a.phase_prof && threadIdx.x == 0) {
@@ -294,8 +404,28 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
     SUB_ADD(3, tg);
     SUB_T(tb);
     float raw[TcLayout::NO];
-    if (kWarp) tcw_forward(tc, phase, xin, raw, a.phase_prof ? &bpa[0] : nullptr);
-    else tc_forward(tc, phase, xin, raw, a.phase_prof ? bpa : nullptr);
+    if (!kWarp && active <= kSmallRows) {  // tail iteration: CUDA-core rows (SmallMlp)
+      int slot = -1;
+      if (need) {
+        slot = atomicAdd(&small.slot_count, 1);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) small.x[slot][i] = xin[i];
+      }
+      __syncthreads();
+      long long t_s = a.phase_prof ? clock64() : 0;
+      small_mlp(small, active);
+      if (a.phase_prof && threadIdx.x == 0) {
+        a.phase_prof[8 * blockIdx.x + 7] += static_cast<unsigned long long>(clock64() - t_s);
+        a.phase_prof[8 * blockIdx.x + 6] += 1ull << 40;  // small-path iteration count (high bits)
+      }
+      if (need)
+#pragma unroll
+        for (int i = 0; i < TcLayout::NO; ++i) raw[i] = small.r[slot][i];
+    } else if (kWarp) {
+      tcw_forward(tc, phase, xin, raw, a.phase_prof ? &bpa[0] : nullptr);
+    } else {
+      tc_forward(tc, phase, xin, raw, a.phase_prof ? bpa : nullptr);
+    }
     if (a.phase_prof && threadIdx.x == 0) {
       a.phase_prof[8 * blockIdx.x + 4] += static_cast<unsigned long long>(bpa[0]);
       a.phase_prof[8 * blockIdx.x + 6] += static_cast<unsigned long long>(bpa[1]);
@@ -492,7 +622,7 @@ cudaError_t launch_mix32_sample(const float* raw, int64_t n, uint64_t seed, doub
 }
 
 int walk_tc_smem(const WalkArgs& a) {
-  size_t tile = walk_tc_warps() == 0 ? TcLayout::BYTES : TcLayoutW::BYTES;
+  size_t tile = walk_tc_warps() == 0 ? TcLayout::BYTES + sizeof(SmallMlp) : TcLayoutW::BYTES;
   return static_cast<int>(al16(tile) + (a.scene_smem_bytes > 0 ? al16(a.scene_smem_bytes) : 0));
 }
 
