@@ -37,7 +37,10 @@ clean:
 
 # diagnostic build: per-sub-phase clock64 totals of the tensor-core walk kernel
 # (overwrites the library; rebuild with `make` afterwards)
+# (the instrumented library is written over the normal one and its timestamp
+# is backdated, so a later plain `make` relinks the normal library)
 subprof: $(OBJ)
 	$(NVCC) $(NVFLAGS) -fmad=true -DWG_SUBPROF -c $(PKG)/csrc/wg_walk_tc.cu -o build/wg_walk_tc_sub.o
 	$(NVCC) $(ARCH) -shared -o $(PKG)/libwostgpu.so $(filter-out build/wg_walk_tc.o,$(OBJ)) build/wg_walk_tc_sub.o -lcudart -ldl
+	touch -d '2000-01-01' $(PKG)/libwostgpu.so
 .PHONY: subprof
