@@ -9,7 +9,7 @@ import os
 from . import abi
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwostgpu.so")
+LIB_PATH = os.environ.get("WOSTGPU_LIB") or os.path.join(_HERE, "libwostgpu.so")  # override: A/B builds
 
 D = C.POINTER(C.c_double)
 F32 = C.POINTER(C.c_float)

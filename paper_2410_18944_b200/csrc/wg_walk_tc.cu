@@ -63,8 +63,8 @@ __host__ __device__ __forceinline__ size_t al16(size_t b) { return (b + 15) & ~s
 constexpr int kSmallRows = 16;
 
 struct SmallMlp {
-  float w1[16][64], b1[64];
-  float w2[64][64], b2[64];
+  float w1[16][80], b1[64];  // row stride = 16 mod 32: lane pairs read rows k, k+1 conflict-free
+  float w2[64][80], b2[64];
   float w3[64][33], b3[36];
   float x[kSmallRows][16];
   float h1[kSmallRows][64], h2[kSmallRows][64];
@@ -83,54 +83,43 @@ __device__ __forceinline__ void small_stage(SmallMlp& M, const FieldView& f) {
   for (int e = threadIdx.x; e < 33; e += blockDim.x) M.b3[e] = f.p[f.b3 + e];
 }
 
-// layers 1-2: thread t -> hidden unit t % 64, rows h, h + 2, ... (h = t / 64)
-// up to 2Q rows per pass; Q is chosen from the live row count so no
-// predicated-off row costs issue slots
-template <int K, int Q>
-__device__ __forceinline__ void small_layer(const float (*w)[64], const float* b, const float* in, int in_stride,
+// layers 1-2: thread t -> hidden unit t / 2 over K half t % 2 (interleaved,
+// k = 2i + t % 2), halves combined by one shuffle: all 128 threads work on
+// every live row with two accumulator chains
+template <int K>
+__device__ __forceinline__ void small_layer(const float (*w)[80], const float* b, const float* in, int in_stride,
                                             float* out, int n) {
-  const int j = threadIdx.x & 63, h = threadIdx.x >> 6;  // 128 threads: 2 row groups
-  for (int r0 = 0; r0 < n; r0 += 2 * Q) {
-    float acc[Q];
+  const int j = threadIdx.x >> 1, s = threadIdx.x & 1;
+  for (int r = 0; r < n; ++r) {
+    const float* x = in + r * in_stride;
+    float a0 = 0.0f, a1 = 0.0f;
 #pragma unroll
-    for (int q = 0; q < Q; ++q) acc[q] = b[j];
-#pragma unroll 8
-    for (int k = 0; k < K; ++k) {
-      const float wk = w[k][j];
-#pragma unroll
-      for (int q = 0; q < Q; ++q) acc[q] = fmaf(wk, in[(r0 + h + 2 * q) * in_stride + k], acc[q]);
+    for (int i = 0; i < K; i += 4) {
+      a0 = fmaf(w[i + s][j], x[i + s], a0);
+      a1 = fmaf(w[i + 2 + s][j], x[i + 2 + s], a1);
     }
-#pragma unroll
-    for (int q = 0; q < Q; ++q)
-      if (r0 + h + 2 * q < n) out[(r0 + h + 2 * q) * 64 + j] = fmaxf(acc[q], 0.0f);
+    float acc = a0 + a1;
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (s == 0) out[r * 64 + j] = fmaxf(acc + b[j], 0.0f);
   }
 }
 
 // layer 3: thread t -> output t / 4 (0..31) over K quarter t % 4 (shuffle
-// reduced), Q rows per pass; output 32 by warp 0 with a warp reduction
-template <int Q>
+// reduced); output 32 by warp 0 with a warp reduction
 __device__ __forceinline__ void small_layer3(SmallMlp& M, int n) {
-  const int t = threadIdx.x, o = t >> 2, p = t & 3;
-  for (int r0 = 0; r0 < n; r0 += Q) {
-    float acc[Q];
+  const int t = threadIdx.x, o = t >> 2, q = t & 3;
+  for (int r = 0; r < n; ++r) {
+    float a0 = 0.0f, a1 = 0.0f;
 #pragma unroll
-    for (int q = 0; q < Q; ++q) acc[q] = 0.0f;
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      const int k = 16 * p + kk;
-      const float wk = M.w3[k][o];
-#pragma unroll
-      for (int q = 0; q < Q; ++q) acc[q] = fmaf(wk, M.h2[r0 + q][k], acc[q]);
+    for (int kk = 0; kk < 16; kk += 2) {
+      a0 = fmaf(M.w3[16 * q + kk][o], M.h2[r][16 * q + kk], a0);
+      a1 = fmaf(M.w3[16 * q + kk + 1][o], M.h2[r][16 * q + kk + 1], a1);
     }
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 1);
-      acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 2);
-      if (p == 0 && r0 + q < n) M.r[r0 + q][o] = acc[q] + M.b3[o];
-    }
-  }
-  if (t < 32) {
-    for (int r = 0; r < n; ++r) {
+    float acc = a0 + a1;
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (q == 0) M.r[r][o] = acc + M.b3[o];
+    if (t < 32) {
       float v = fmaf(M.w3[t][32], M.h2[r][t], M.w3[t + 32][32] * M.h2[r][t + 32]);
 #pragma unroll
       for (int o2 = 16; o2 > 0; o2 >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o2);
@@ -139,24 +128,16 @@ __device__ __forceinline__ void small_layer3(SmallMlp& M, int n) {
   }
 }
 
-template <int Q>
-__device__ __forceinline__ void small_mlp_q(SmallMlp& M, int n) {
-  small_layer<16, Q>(M.w1, M.b1, &M.x[0][0], 16, &M.h1[0][0], n);
-  __syncthreads();
-  small_layer<64, Q>(M.w2, M.b2, &M.h1[0][0], 64, &M.h2[0][0], n);
-  __syncthreads();
-  small_layer3<2 * Q>(M, n);
-  __syncthreads();
-}
-
 // MLP rows 0..n-1 of M.x -> M.r (raw outputs); all threads, barriers inside.
 // Rows n..kSmallRows-1 of x / h1 / h2 may hold stale values: they are read
 // by the unrolled row loops but never written back.
 __device__ __forceinline__ void small_mlp(SmallMlp& M, int n) {
-  if (n <= 2) small_mlp_q<1>(M, n);
-  else if (n <= 4) small_mlp_q<2>(M, n);
-  else if (n <= 8) small_mlp_q<4>(M, n);
-  else small_mlp_q<8>(M, n);
+  small_layer<16>(M.w1, M.b1, &M.x[0][0], 16, &M.h1[0][0], n);
+  __syncthreads();
+  small_layer<64>(M.w2, M.b2, &M.h1[0][0], 64, &M.h2[0][0], n);
+  __syncthreads();
+  small_layer3(M, n);
+  __syncthreads();
 }
 
 __device__ __forceinline__ void t_finish(TLane& w, const WalkArgs& a, bool escaped, double terminal,
