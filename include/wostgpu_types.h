@@ -146,6 +146,27 @@ typedef struct wg_mixture {
   int32_t dim;
 } wg_mixture;
 
+/* ---- 3D (no reference counterpart; SURVEY.md §8 a', configs 4-5) ------ */
+/* Dirichlet value of a 3D triangle: Constant c0 or Linear c0 + cx x + cy y +
+ * cz z (the 3D analogue of ValueSpec, scene.hpp:31-67); Neumann triangles
+ * carry the constant 0 (no flux in 3D scenes) */
+typedef struct wg_value3_spec {
+  int32_t type; /* WG_VALUE_CONSTANT or WG_VALUE_LINEAR */
+  int32_t pad_;
+  double c0, cx, cy, cz;
+} wg_value3_spec;
+
+/* GuideRecord with 3D position and normal */
+typedef struct wg_guide_record3 {
+  double x[3];
+  double nu[3];
+  double target;
+  double pdf_mis, pdf_g, pdf_u, c;
+  int32_t on_neumann;
+  int32_t pad_;
+  double normal[3];
+} wg_guide_record3;
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,6 +82,40 @@ extern "C" {
 WG_ORACLE_DECLS(ref)
 WG_ORACLE_DECLS(orc)
 
+/* 3D contract (oracle/wost3d.inc): restatement only, no reference code */
+void* orc3_scene_create(const double* tri, const int32_t* kind, const int32_t* value_index,
+                        int32_t n_tri, const wg_value3_spec* values, int32_t n_values,
+                        const double* bbox, double epsilon_shell);
+void orc3_scene_destroy(void* scene);
+double orc3_t_epsilon(void* scene);
+void orc3_silhouette_info(void* scene, int64_t* n_always, int64_t* n_crease);
+int orc3_closest_point(void* scene, int64_t n, const double* xyz, uint32_t kinds, double* pt,
+                       double* dist, int32_t* tri);
+int orc3_closest_silhouette(void* scene, int64_t n, const double* xyz, double* dist);
+int orc3_ray_first_hit(void* scene, int64_t n, const double* origin, const double* dir,
+                       const double* t_max, uint32_t kinds, const int32_t* exclude, double* t,
+                       double* pt, double* normal, int32_t* tri, int32_t* kind);
+int orc3_star_radius(void* scene, int64_t n, const double* xyz, double r_min, double* r);
+void* orc3_field_create(const wg_field_config* cfg, const double* bbox, uint64_t seed);
+void orc3_field_destroy(void* field);
+int64_t orc3_field_param_count(void* field);
+void orc3_field_get_params(void* field, float* out);
+void orc3_field_set_params(void* field, const float* in);
+void orc3_field_eval_batch(void* field, int64_t n, const double* xyz, double* out);
+int orc3_walks(void* scene, void* field, const wg_solver_config* cfg, int64_t n, const double* xyz,
+               const int64_t* point_index, uint64_t seed, uint64_t wpp_index, double* estimate,
+               int32_t* escaped, int32_t* steps);
+int orc3_walk_records(void* scene, void* field, const wg_solver_config* cfg, int64_t n,
+                      const double* xyz, const int64_t* point_index, uint64_t seed,
+                      uint64_t wpp_index, wg_guide_record3** records, int64_t* n_records);
+int orc3_field_grad(void* field, const wg_guide_record3* recs, int64_t n,
+                    const wg_train_config* cfg, double* grad_out);
+int orc3_train_batch(void* field, const wg_guide_record3* recs, int64_t n,
+                     const wg_train_config* cfg, uint64_t round, wg_train_stats* stats);
+int orc3_run(void* scene, void* field, const wg_solver_config* cfg, int64_t n, const double* xyz,
+             int64_t point_offset, uint64_t seed, int32_t wpp, int64_t train_until,
+             const wg_train_config* train_cfg, wg_point_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,7 @@
 // strict build of the reference (oracle/_ref/libwost_ref.so).
 // ============================================================================
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -1667,3 +1668,6 @@ int orc_field_grad(void* fp, const wg_guide_record* recs, int64_t n, const wg_tr
 }
 
 }  // extern "C"
+
+// 3D contract (SURVEY.md §8 a′): same translation unit, shares orc::
+#include "wost3d.inc"

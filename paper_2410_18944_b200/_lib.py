@@ -79,6 +79,32 @@ _SIGS = {
     "wostgpu_comm_unique_id": (C.c_int, [C.c_char_p]),
     "wostgpu_solver_attach_comm": (C.c_int, [VP, C.c_char_p, C.c_int32, C.c_int32]),
     "wostgpu_solver_timing": (C.c_int, [VP, D, D]),
+    # ---- 3D path (include/wostgpu3.h)
+    "wostgpu_scene3_create": (C.c_int, [D, I32, I32, C.c_int32, C.POINTER(abi.Value3Spec), C.c_int32, D,
+                                        C.c_double, C.POINTER(VP)]),
+    "wostgpu_scene3_destroy": (C.c_int, [VP]),
+    "wostgpu_scene3_info": (C.c_int, [VP, D, I64, I64, I64]),
+    "wostgpu_closest_point3": (C.c_int, [VP, C.c_int64, D, C.c_uint32, D, D, I32]),
+    "wostgpu_closest_silhouette3": (C.c_int, [VP, C.c_int64, D, D]),
+    "wostgpu_ray_first_hit3": (C.c_int, [VP, C.c_int64, D, D, D, C.c_uint32, I32, D, D, D, I32, I32]),
+    "wostgpu_star_radius3": (C.c_int, [VP, C.c_int64, D, C.c_double, D]),
+    "wostgpu_field3_create": (C.c_int, [C.POINTER(abi.FieldConfig), D, C.c_uint64, C.POINTER(VP)]),
+    "wostgpu_field3_eval_batch": (C.c_int, [VP, C.c_int64, D, D]),
+    "wostgpu_solver3_create": (C.c_int, [VP, VP, C.POINTER(abi.SolverConfig), C.POINTER(VP)]),
+    "wostgpu_solver3_destroy": (C.c_int, [VP]),
+    "wostgpu_solver3_set_points": (C.c_int, [VP, C.c_int64, D, C.c_int64]),
+    "wostgpu_solver3_get_stats": (C.c_int, [VP, VP]),
+    "wostgpu_solver3_solve_rounds": (C.c_int, [VP, C.c_uint64, C.c_uint64, C.c_int32, C.c_int32]),
+    "wostgpu_solver3_fetch_walks": (C.c_int, [VP, D, I32, I32]),
+    "wostgpu_solver3_fetch_records": (C.c_int, [VP, VP, C.c_int64, I64]),
+    "wostgpu_solver3_counters": (C.c_int, [VP, I64, I64, I64, I64]),
+    "wostgpu_solver3_train_round": (C.c_int, [VP, C.POINTER(abi.TrainConfig), C.c_uint64,
+                                              C.POINTER(abi.TrainStats)]),
+    "wostgpu_solver3_field_grad": (C.c_int, [VP, VP, C.c_int64, C.POINTER(abi.TrainConfig), D]),
+    "wostgpu_solver3_run": (C.c_int, [VP, C.c_uint64, C.c_int32, C.c_int64, C.POINTER(abi.TrainConfig),
+                                      C.POINTER(abi.TrainStats), D]),
+    "wostgpu_solver3_run_profile": (C.c_int, [VP, D, D, I64, I64, I64, I64]),
+    "wostgpu_solver3_attach_comm": (C.c_int, [VP, C.c_char_p, C.c_int32, C.c_int32]),
 }
 
 EXPORTED_SYMBOLS = sorted(_SIGS)

@@ -79,6 +79,47 @@ def field_param_count(cfg):
     return emb + i * h + h + h * h + h + h * o + o
 
 
+class Value3Spec(C.Structure):
+    """wg_value3_spec (include/wostgpu_types.h): 3D Dirichlet value."""
+    _fields_ = [
+        ("type", C.c_int32),
+        ("pad_", C.c_int32),
+        ("c0", C.c_double),
+        ("cx", C.c_double),
+        ("cy", C.c_double),
+        ("cz", C.c_double),
+    ]
+
+
+class GuideRecord3(C.Structure):
+    """wg_guide_record3: GuideRecord with 3D position and normal."""
+    _fields_ = [
+        ("x", C.c_double * 3),
+        ("nu", C.c_double * 3),
+        ("target", C.c_double),
+        ("pdf_mis", C.c_double),
+        ("pdf_g", C.c_double),
+        ("pdf_u", C.c_double),
+        ("c", C.c_double),
+        ("on_neumann", C.c_int32),
+        ("pad_", C.c_int32),
+        ("normal", C.c_double * 3),
+    ]
+
+
+def field_config3(level_res=(8, 16, 32, 64), features=4, hidden=64, mixture_k=8):
+    """3D field: dense D^3 x F grids per level (no reference counterpart; the
+    finest level is 64^3 so the 3D grid, 1.2M parameters, stays L2-resident)."""
+    return field_config(level_res, features, hidden, mixture_k, 3)
+
+
+def field_param_count3(cfg):
+    emb = sum(r * r * r * cfg.features for r in cfg.level_res[: cfg.n_levels])
+    i, h = cfg.n_levels * cfg.features, cfg.hidden
+    o = (2 + cfg.mixture_dim) * cfg.mixture_k + 1
+    return emb + i * h + h + h * h + h + h * o + o
+
+
 class TrainConfig(C.Structure):
     _fields_ = [
         ("minibatch", C.c_int32),
@@ -122,6 +163,11 @@ POINT_STATS_DTYPE = np.dtype([("mean", "<f8"), ("m2", "<f8"), ("count", "<i8"), 
 GUIDE_RECORD_DTYPE = np.dtype([
     ("x", "<f8", 2), ("nu", "<f8", 3), ("target", "<f8"), ("pdf_mis", "<f8"), ("pdf_g", "<f8"),
     ("pdf_u", "<f8"), ("c", "<f8"), ("on_neumann", "<i4"), ("pad_", "<i4"), ("normal", "<f8", 2),
+])
+
+GUIDE_RECORD3_DTYPE = np.dtype([
+    ("x", "<f8", 3), ("nu", "<f8", 3), ("target", "<f8"), ("pdf_mis", "<f8"), ("pdf_g", "<f8"),
+    ("pdf_u", "<f8"), ("c", "<f8"), ("on_neumann", "<i4"), ("pad_", "<i4"), ("normal", "<f8", 3),
 ])
 
 MIXTURE_DTYPE = np.dtype([

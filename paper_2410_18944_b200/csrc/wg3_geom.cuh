@@ -1,0 +1,339 @@
+// 3D scene queries on device (SURVEY.md §8 a′, configs 4-5): closest point
+// on a triangle mesh, closest silhouette edge, first ray hit, star radius.
+//
+// The reference has no 3D code; the contract is oracle/wost3d.inc (the 3D
+// analogue of proj/src/geom2d.cpp:142-255). Every selection rule is
+// order-independent (minimum of (d^2, id) / (t, id)), so these BVH traversals
+// return exactly what the oracle's own structure returns. Arithmetic is fp64
+// in the oracle's operation order; translation units including this header
+// compile with -fmad=false (Makefile), so results are bit-identical.
+//
+// HBM layout (per kind: Dirichlet, Neumann; plus the silhouette-edge index):
+//   Node3  32 B  {lo.xyz f32, a i32 | hi.xyz f32, b i32}: one 16-B load per
+//          half; bounds rounded outward from fp64 so pruning is conservative.
+//          Internal: children a, b. Leaf: b = -count, primitives [a, a+count).
+//   Tri3   88 B  vertices (fp64), original id, value index, kind; stored in
+//          leaf order so a leaf's triangles are contiguous.
+//   Edge3 104 B  endpoints, the two incident Neumann normals, type.
+// A 100k-triangle scene is ~10 MB: L2-resident (126 MB) on B200.
+#pragma once
+
+#include <cstdint>
+
+#include "../../include/wostgpu_types.h"
+#include "wg_device.cuh"
+
+namespace wg3 {
+
+using wg::dinf;
+
+struct D3 {
+  double x, y, z;
+};
+__host__ __device__ __forceinline__ D3 add(D3 a, D3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+__host__ __device__ __forceinline__ D3 sub(D3 a, D3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__host__ __device__ __forceinline__ D3 scl(D3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+__host__ __device__ __forceinline__ double dot(D3 a, D3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__host__ __device__ __forceinline__ D3 cross(D3 a, D3 b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+
+struct __align__(16) Node3 {
+  float lo[3];
+  int32_t a;
+  float hi[3];
+  int32_t b;
+};
+struct __align__(8) Tri3 {
+  double a[3], b[3], c[3];
+  int32_t id, value, kind, pad_;
+};
+struct __align__(8) Edge3 {
+  double a[3], b[3], n0[3], n1[3];
+  int32_t type, pad_;  // 0: always a silhouette, 1: crease (facing test)
+};
+static_assert(sizeof(Node3) == 32, "Node3 layout");
+static_assert(sizeof(Tri3) == 88, "Tri3 layout");
+static_assert(sizeof(Edge3) == 104, "Edge3 layout");
+
+struct Scene3View {
+  const Node3* node[3];  // Dirichlet, Neumann, silhouette edges (nullptr if empty)
+  const Tri3* tri[2];    // leaf-ordered triangles per kind
+  const Edge3* edge;     // leaf-ordered edges
+  const wg_value3_spec* values;
+  double bbox[6];
+  double t_eps, diag, eps;
+};
+
+__device__ __forceinline__ D3 ld3(const double* p) { return {p[0], p[1], p[2]}; }
+
+__device__ __forceinline__ void ld_node(const Node3* n, float4& lo, float4& hi) {
+  const float4* q = reinterpret_cast<const float4*>(n);
+  lo = __ldg(q);
+  hi = __ldg(q + 1);
+}
+
+__device__ __forceinline__ double box_d2(const float4& lo, const float4& hi, D3 p) {
+  double dx = fmax(fmax((double)lo.x - p.x, 0.0), p.x - (double)hi.x);
+  double dy = fmax(fmax((double)lo.y - p.y, 0.0), p.y - (double)hi.y);
+  double dz = fmax(fmax((double)lo.z - p.z, 0.0), p.z - (double)hi.z);
+  return dx * dx + dy * dy + dz * dz;
+}
+
+// closest point on triangle abc (oracle/wost3d.inc closest_on_tri)
+__device__ __forceinline__ D3 closest_on_tri(D3 p, D3 a, D3 b, D3 c) {
+  D3 ab = sub(b, a), ac = sub(c, a), ap = sub(p, a);
+  double d1 = dot(ab, ap), d2 = dot(ac, ap);
+  if (d1 <= 0.0 && d2 <= 0.0) return a;
+  D3 bp = sub(p, b);
+  double d3 = dot(ab, bp), d4 = dot(ac, bp);
+  if (d3 >= 0.0 && d4 <= d3) return b;
+  double vc = d1 * d4 - d3 * d2;
+  if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {
+    double v = d1 / (d1 - d3);
+    return add(a, scl(ab, v));
+  }
+  D3 cp = sub(p, c);
+  double d5 = dot(ab, cp), d6 = dot(ac, cp);
+  if (d6 >= 0.0 && d5 <= d6) return c;
+  double vb = d5 * d2 - d1 * d6;
+  if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
+    double w = d2 / (d2 - d6);
+    return add(a, scl(ac, w));
+  }
+  double va = d3 * d6 - d5 * d4;
+  if (va <= 0.0 && (d4 - d3) >= 0.0 && (d5 - d6) >= 0.0) {
+    double w = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+    return add(b, scl(sub(c, b), w));
+  }
+  double den = 1.0 / (va + vb + vc);
+  double v = vb * den, w = vc * den;
+  return add(add(a, scl(ab, v)), scl(ac, w));
+}
+
+__device__ __forceinline__ D3 closest_on_seg(D3 p, D3 a, D3 b) {
+  D3 ab = sub(b, a);
+  double l2 = dot(ab, ab);
+  double t = l2 > 0.0 ? wg::sclamp(dot(sub(p, a), ab) / l2, 0.0, 1.0) : 0.0;
+  return add(a, scl(ab, t));
+}
+
+// Moller-Trumbore (oracle ray_tri); miss -> false
+__device__ __forceinline__ bool ray_tri(D3 o, D3 d, D3 a, D3 b, D3 c, double* t) {
+  D3 e1 = sub(b, a), e2 = sub(c, a);
+  D3 p = cross(d, e2);
+  double det = dot(e1, p);
+  if (det == 0.0) return false;
+  double inv = 1.0 / det;
+  D3 s = sub(o, a);
+  double u = dot(s, p) * inv;
+  if (u < 0.0 || u > 1.0) return false;
+  D3 q = cross(s, e1);
+  double v = dot(d, q) * inv;
+  if (v < 0.0 || u + v > 1.0) return false;
+  *t = dot(e2, q) * inv;
+  return true;
+}
+
+// slab test against [0, t_hi] with precomputed inverse direction
+__device__ __forceinline__ bool ray_box(D3 o, D3 inv, const bool* dz, const float4& lo,
+                                        const float4& hi, double t_hi) {
+  double t0 = 0.0, t1 = t_hi;
+  const double oo[3] = {o.x, o.y, o.z}, iv[3] = {inv.x, inv.y, inv.z};
+  const double l[3] = {lo.x, lo.y, lo.z}, h[3] = {hi.x, hi.y, hi.z};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (dz[a]) {
+      if (oo[a] < l[a] || oo[a] > h[a]) return false;
+      continue;
+    }
+    double ta = (l[a] - oo[a]) * iv[a], tb = (h[a] - oo[a]) * iv[a];
+    if (ta > tb) {
+      double s = ta;
+      ta = tb;
+      tb = s;
+    }
+    t0 = fmax(t0, ta);
+    t1 = fmin(t1, tb);
+    if (t0 > t1) return false;
+  }
+  return true;
+}
+
+struct CP3 {
+  D3 p;
+  double d2;
+  int tri;    // original id, -1 if none
+  int local;  // leaf-order index within its kind's triangle array
+};
+
+__device__ __forceinline__ void cp_bvh(const Node3* nodes, const Tri3* tris, D3 x, CP3& best) {
+  if (!nodes) return;
+  int stack[64];
+  int sp = 0;
+  stack[sp++] = 0;
+  while (sp) {
+    float4 lo, hi;
+    ld_node(nodes + stack[--sp], lo, hi);
+    if (box_d2(lo, hi, x) > best.d2) continue;
+    int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
+    if (b < 0) {
+      for (int i = a; i < a - b; ++i) {
+        const Tri3& t = tris[i];
+        D3 q = closest_on_tri(x, ld3(t.a), ld3(t.b), ld3(t.c));
+        D3 dq = sub(x, q);
+        double d2 = dot(dq, dq);
+        int id = t.id;
+        if (d2 < best.d2 || (d2 == best.d2 && id < best.tri)) {
+          best.d2 = d2;
+          best.p = q;
+          best.tri = id;
+          best.local = i;
+        }
+      }
+      continue;
+    }
+    float4 alo, ahi, blo, bhi;
+    ld_node(nodes + a, alo, ahi);
+    ld_node(nodes + b, blo, bhi);
+    double da = box_d2(alo, ahi, x), db = box_d2(blo, bhi, x);
+    if (da <= db) {  // nearer child on top
+      stack[sp++] = b;
+      stack[sp++] = a;
+    } else {
+      stack[sp++] = a;
+      stack[sp++] = b;
+    }
+  }
+}
+
+// Accel::closest_point analogue: (point, distance, triangle id) or id -1, d = inf
+__device__ __forceinline__ CP3 closest_point(const Scene3View& s, D3 x, unsigned kinds) {
+  CP3 best{{0.0, 0.0, 0.0}, dinf(), -1, -1};
+  if (kinds & WG_KIND_DIRICHLET) cp_bvh(s.node[0], s.tri[0], x, best);
+  if (kinds & WG_KIND_NEUMANN) cp_bvh(s.node[1], s.tri[1], x, best);
+  return best;
+}
+
+__device__ __forceinline__ bool is_silhouette(const Edge3& e, D3 x) {
+  if (e.type == 0) return true;
+  D3 ax = sub(ld3(e.a), x);
+  return dot(ld3(e.n0), ax) * dot(ld3(e.n1), ax) <= 0.0;
+}
+
+// squared distance to the nearest silhouette edge (inf if none)
+__device__ __forceinline__ double closest_silhouette_d2(const Scene3View& s, D3 x) {
+  const Node3* nodes = s.node[2];
+  if (!nodes) return dinf();
+  double best = dinf();
+  int stack[64];
+  int sp = 0;
+  stack[sp++] = 0;
+  while (sp) {
+    float4 lo, hi;
+    ld_node(nodes + stack[--sp], lo, hi);
+    if (box_d2(lo, hi, x) >= best) continue;
+    int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
+    if (b < 0) {
+      for (int i = a; i < a - b; ++i) {
+        const Edge3& e = s.edge[i];
+        if (!is_silhouette(e, x)) continue;
+        D3 dq = sub(x, closest_on_seg(x, ld3(e.a), ld3(e.b)));
+        best = fmin(best, dot(dq, dq));
+      }
+      continue;
+    }
+    float4 alo, ahi, blo, bhi;
+    ld_node(nodes + a, alo, ahi);
+    ld_node(nodes + b, blo, bhi);
+    double da = box_d2(alo, ahi, x), db = box_d2(blo, bhi, x);
+    if (da <= db) {
+      stack[sp++] = b;
+      stack[sp++] = a;
+    } else {
+      stack[sp++] = a;
+      stack[sp++] = b;
+    }
+  }
+  return best;
+}
+
+__device__ __forceinline__ double closest_silhouette(const Scene3View& s, D3 x) {
+  double b = closest_silhouette_d2(s, x);
+  return b == dinf() ? dinf() : sqrt(b);
+}
+
+struct Hit3 {
+  double t;
+  int tri;    // original id, -1 on a miss
+  int local;  // leaf-order index within its kind's array
+  int kind;
+};
+
+__device__ __forceinline__ void ray_bvh(const Node3* nodes, const Tri3* tris, int kind, D3 o, D3 d,
+                                        double t_max, double t_eps, int exclude, Hit3& h) {
+  if (!nodes) return;
+  D3 inv;
+  bool dz[3] = {d.x == 0.0, d.y == 0.0, d.z == 0.0};
+  inv.x = dz[0] ? 0.0 : 1.0 / d.x;
+  inv.y = dz[1] ? 0.0 : 1.0 / d.y;
+  inv.z = dz[2] ? 0.0 : 1.0 / d.z;
+  int stack[64];
+  int sp = 0;
+  stack[sp++] = 0;
+  while (sp) {
+    float4 lo, hi;
+    ld_node(nodes + stack[--sp], lo, hi);
+    if (!ray_box(o, inv, dz, lo, hi, fmin(t_max, h.t))) continue;
+    int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
+    if (b < 0) {
+      for (int i = a; i < a - b; ++i) {
+        const Tri3& t = tris[i];
+        int id = t.id;
+        if (id == exclude) continue;
+        double th;
+        if (!ray_tri(o, d, ld3(t.a), ld3(t.b), ld3(t.c), &th)) continue;
+        if (!(th > t_eps && th <= t_max)) continue;
+        if (th < h.t || (th == h.t && id < h.tri)) {
+          h.t = th;
+          h.tri = id;
+          h.local = i;
+          h.kind = kind;
+        }
+      }
+      continue;
+    }
+    stack[sp++] = b;
+    stack[sp++] = a;
+  }
+}
+
+__device__ __forceinline__ Hit3 ray_first_hit(const Scene3View& s, D3 o, D3 d, double t_max,
+                                              unsigned kinds, int exclude) {
+  Hit3 h{dinf(), -1, -1, -1};
+  if (kinds & WG_KIND_DIRICHLET) ray_bvh(s.node[0], s.tri[0], 0, o, d, t_max, s.t_eps, exclude, h);
+  if (kinds & WG_KIND_NEUMANN) ray_bvh(s.node[1], s.tri[1], 1, o, d, t_max, s.t_eps, exclude, h);
+  return h;
+}
+
+// unit geometric normal of the hit triangle, facing the incoming ray
+__device__ __forceinline__ D3 hit_normal(const Scene3View& s, const Hit3& h, D3 d) {
+  const Tri3& t = s.tri[h.kind][h.local];
+  D3 a = ld3(t.a);
+  D3 n = cross(sub(ld3(t.b), a), sub(ld3(t.c), a));
+  n = scl(n, 1.0 / sqrt(dot(n, n)));
+  if (dot(n, d) > 0.0) n = scl(n, -1.0);
+  return n;
+}
+
+__device__ __forceinline__ double value_at(const wg_value3_spec& v, D3 p) {
+  if (v.type == WG_VALUE_CONSTANT) return v.c0;
+  return v.c0 + v.cx * p.x + v.cy * p.y + v.cz * p.z;
+}
+
+__device__ __forceinline__ bool bbox_contains(const Scene3View& s, D3 p, double pad) {
+  return p.x >= s.bbox[0] - pad && p.x <= s.bbox[3] + pad && p.y >= s.bbox[1] - pad &&
+         p.y <= s.bbox[4] + pad && p.z >= s.bbox[2] - pad && p.z <= s.bbox[5] + pad;
+}
+
+}  // namespace wg3

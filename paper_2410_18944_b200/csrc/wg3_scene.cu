@@ -1,0 +1,448 @@
+// 3D scenes: host BVH build (per-kind triangle BVHs + the silhouette-edge
+// index of the Neumann set), batched query kernels and their C-ABI
+// (include/wostgpu3.h). Contract: oracle/wost3d.inc (the 3D analogue of
+// proj/src/geom2d.cpp:80-255).
+//
+// BVH: binary, median split of the primitive centroids along the longest
+// axis of their bounds (ties by primitive index), leaves of <= 4, depth-first
+// preorder so a node's first child follows it. Built once per scene on the
+// host (not hot); node boxes are fp32 rounded outward from the fp64 bounds.
+#include <array>
+#include <cfloat>
+#include <cmath>
+#include <map>
+#include <utility>
+
+#include "wg3_runtime.hpp"
+
+namespace wg3 {
+namespace {
+
+using wgrt::need;
+
+float round_down(double d) {
+  float f = static_cast<float>(d);
+  if (static_cast<double>(f) > d) f = std::nextafter(f, -INFINITY);
+  return f;
+}
+float round_up(double d) {
+  float f = static_cast<float>(d);
+  if (static_cast<double>(f) < d) f = std::nextafter(f, INFINITY);
+  return f;
+}
+
+struct HBox {
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  void grow(const double* p) {
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = std::min(lo[a], p[a]);
+      hi[a] = std::max(hi[a], p[a]);
+    }
+  }
+  void grow(const HBox& b) {
+    grow(b.lo);
+    grow(b.hi);
+  }
+};
+
+struct Builder {
+  const std::vector<HBox>& box;
+  std::vector<double> cen;  // 3 per primitive
+  std::vector<int> order;
+  std::vector<Node3> nodes;
+  explicit Builder(const std::vector<HBox>& b) : box(b), cen(3 * b.size()), order(b.size()) {
+    for (size_t i = 0; i < b.size(); ++i) {
+      order[i] = static_cast<int>(i);
+      for (int a = 0; a < 3; ++a) cen[3 * i + a] = 0.5 * (b[i].lo[a] + b[i].hi[a]);
+    }
+    if (!b.empty()) build(0, static_cast<int>(b.size()));
+  }
+  int build(int lo, int hi) {
+    const int id = static_cast<int>(nodes.size());
+    nodes.emplace_back();
+    HBox bb, cb;
+    for (int i = lo; i < hi; ++i) {
+      bb.grow(box[order[i]]);
+      cb.grow(&cen[3 * order[i]]);
+    }
+    Node3 n;
+    for (int a = 0; a < 3; ++a) {
+      n.lo[a] = round_down(bb.lo[a]);
+      n.hi[a] = round_up(bb.hi[a]);
+    }
+    if (hi - lo <= 4) {
+      n.a = lo;
+      n.b = -(hi - lo);
+      nodes[id] = n;
+      return id;
+    }
+    double ext[3] = {cb.hi[0] - cb.lo[0], cb.hi[1] - cb.lo[1], cb.hi[2] - cb.lo[2]};
+    const int ax = ext[0] >= ext[1] && ext[0] >= ext[2] ? 0 : (ext[1] >= ext[2] ? 1 : 2);
+    const int mid = (lo + hi) / 2;
+    std::nth_element(order.begin() + lo, order.begin() + mid, order.begin() + hi, [&](int p, int q) {
+      double kp = cen[3 * p + ax], kq = cen[3 * q + ax];
+      return kp < kq || (kp == kq && p < q);
+    });
+    n.a = build(lo, mid);
+    n.b = build(mid, hi);
+    nodes[id] = n;
+    return id;
+  }
+};
+
+void cross3(const double* a, const double* b, double* o) {
+  o[0] = a[1] * b[2] - a[2] * b[1];
+  o[1] = a[2] * b[0] - a[0] * b[2];
+  o[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+// unit normal of triangle abc: cross(b - a, c - a) * (1 / |.|)
+void tri_normal(const double* a, const double* b, const double* c, double* n) {
+  double e1[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+  double e2[3] = {c[0] - a[0], c[1] - a[1], c[2] - a[2]};
+  cross3(e1, e2, n);
+  double inv = 1.0 / std::sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+  for (int i = 0; i < 3; ++i) n[i] = n[i] * inv;
+}
+
+// silhouette candidates: edges of Neumann triangles keyed by the exact bits
+// of their endpoints; one (or > 2) incident triangles -> always, two
+// non-coplanar -> crease (facing test at query time), coplanar -> dropped
+std::vector<Edge3> silhouette_edges(const std::vector<Tri3>& tris, int64_t* n_always, int64_t* n_crease) {
+  using VK = std::array<uint64_t, 3>;
+  auto key = [](const double* p) {
+    VK k;
+    std::memcpy(k.data(), p, 24);
+    return k;
+  };
+  struct E {
+    double a[3], b[3];
+    std::vector<std::array<double, 3>> n;
+  };
+  std::map<std::pair<VK, VK>, E> m;
+  for (const Tri3& t : tris) {
+    if (t.kind != WG_NEUMANN) continue;
+    std::array<double, 3> n;
+    tri_normal(t.a, t.b, t.c, n.data());
+    const double* v[3] = {t.a, t.b, t.c};
+    for (int i = 0; i < 3; ++i) {
+      const double* p = v[i];
+      const double* q = v[(i + 1) % 3];
+      VK kp = key(p), kq = key(q);
+      if (kq < kp) {
+        std::swap(kp, kq);
+        std::swap(p, q);
+      }
+      E& e = m[{kp, kq}];
+      std::memcpy(e.a, p, 24);
+      std::memcpy(e.b, q, 24);
+      e.n.push_back(n);
+    }
+  }
+  std::vector<Edge3> out;
+  *n_always = *n_crease = 0;
+  for (auto& kv : m) {
+    const E& e = kv.second;
+    Edge3 g{};
+    std::memcpy(g.a, e.a, 24);
+    std::memcpy(g.b, e.b, 24);
+    if (e.n.size() == 2) {
+      const auto &n0 = e.n[0], &n1 = e.n[1];
+      if (n0[0] * n1[0] + n0[1] * n1[1] + n0[2] * n1[2] > 1.0 - 1e-9) continue;  // coplanar
+      g.type = 1;
+      std::memcpy(g.n0, n0.data(), 24);
+      std::memcpy(g.n1, n1.data(), 24);
+      ++*n_crease;
+    } else {
+      g.type = 0;
+      ++*n_always;
+    }
+    out.push_back(g);
+  }
+  return out;
+}
+
+// ---------------------------------------------------------------- kernels
+__global__ void cp3_kernel(Scene3View s, int64_t n, const double* x, uint32_t kinds, double* pt,
+                           double* dist, int32_t* tri) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    CP3 c = closest_point(s, {x[3 * i], x[3 * i + 1], x[3 * i + 2]}, kinds);
+    pt[3 * i] = c.p.x;
+    pt[3 * i + 1] = c.p.y;
+    pt[3 * i + 2] = c.p.z;
+    dist[i] = c.tri >= 0 ? sqrt(c.d2) : dinf();
+    tri[i] = c.tri;
+  }
+}
+
+__global__ void sil3_kernel(Scene3View s, int64_t n, const double* x, double* dist) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dist[i] = closest_silhouette(s, {x[3 * i], x[3 * i + 1], x[3 * i + 2]});
+}
+
+__global__ void ray3_kernel(Scene3View s, int64_t n, const double* o, const double* d,
+                            const double* t_max, uint32_t kinds, const int32_t* exclude, double* t,
+                            double* pt, double* nrm, int32_t* tri, int32_t* kind) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    D3 oo{o[3 * i], o[3 * i + 1], o[3 * i + 2]}, dd{d[3 * i], d[3 * i + 1], d[3 * i + 2]};
+    Hit3 h = ray_first_hit(s, oo, dd, t_max[i], kinds, exclude ? exclude[i] : -1);
+    D3 p{0.0, 0.0, 0.0}, nn{0.0, 0.0, 0.0};
+    if (h.tri >= 0) {
+      p = add(oo, scl(dd, h.t));
+      nn = hit_normal(s, h, dd);
+    }
+    t[i] = h.tri >= 0 ? h.t : dinf();
+    pt[3 * i] = p.x;
+    pt[3 * i + 1] = p.y;
+    pt[3 * i + 2] = p.z;
+    nrm[3 * i] = nn.x;
+    nrm[3 * i + 1] = nn.y;
+    nrm[3 * i + 2] = nn.z;
+    tri[i] = h.tri;
+    kind[i] = h.tri >= 0 ? h.kind : -1;
+  }
+}
+
+__global__ void star3_kernel(Scene3View s, int64_t n, const double* x, double r_min, double* r,
+                             int* unbounded) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    D3 p{x[3 * i], x[3 * i + 1], x[3 * i + 2]};
+    CP3 c = closest_point(s, p, WG_KIND_DIRICHLET);
+    double dd = c.tri >= 0 ? sqrt(c.d2) : dinf();
+    double ds = closest_silhouette(s, p);
+    if (dd == dinf() && ds == dinf()) {
+      atomicOr(unbounded, 1);
+      r[i] = dinf();
+      continue;
+    }
+    r[i] = fmin(dd, fmax(ds, r_min));
+  }
+}
+
+int grid_for(int64_t n) {
+  int64_t b = (n + 127) / 128;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16)));
+}
+
+// device copies of host input arrays for one batched query
+struct Staged {
+  std::vector<std::unique_ptr<wgrt::DBuf>> bufs;
+  template <class T>
+  T* in(const T* h, size_t n) {
+    if (!h) return nullptr;
+    bufs.push_back(std::make_unique<wgrt::DBuf>());
+    bufs.back()->upload(h, n);
+    return bufs.back()->as<T>();
+  }
+  template <class T>
+  T* out(size_t n) {
+    bufs.push_back(std::make_unique<wgrt::DBuf>());
+    bufs.back()->alloc(sizeof(T) * (n ? n : 1));
+    return bufs.back()->as<T>();
+  }
+};
+
+template <class T>
+void down(T* h, const T* d, size_t n) {
+  if (n) CK(cudaMemcpy(h, d, sizeof(T) * n, cudaMemcpyDeviceToHost));
+}
+
+}  // namespace
+}  // namespace wg3
+
+using namespace wgrt;
+using namespace wg3;
+
+extern "C" {
+
+int wostgpu_scene3_create(const double* tri, const int32_t* kind, const int32_t* value_index,
+                          int32_t n_tri, const wg_value3_spec* values, int32_t n_values,
+                          const double bbox[6], double eps, wg_scene3* out) {
+  return guarded([&] {
+    check_device();
+    need(n_tri > 0, WG_ERR_SCENE, "Accel: empty scene");
+    auto s = std::make_unique<wg_scene3_s>();
+    CK(cudaGetDevice(&s->device));
+    for (int i = 0; i < 6; ++i) s->bbox[i] = bbox[i];
+    s->eps = eps > 0.0 ? eps : 1e-3;
+    for (int i = 0; i < n_values; ++i)
+      need(values[i].type == WG_VALUE_CONSTANT || values[i].type == WG_VALUE_LINEAR, WG_ERR_INVALID,
+           "3D scene: values must be constant or linear");
+    std::vector<Tri3> tris(static_cast<size_t>(n_tri));
+    HBox root;
+    std::vector<HBox> boxes[2];
+    std::vector<int> ids[2];
+    for (int i = 0; i < n_tri; ++i) {
+      Tri3& t = tris[i];
+      std::memcpy(t.a, tri + 9 * i, 24);
+      std::memcpy(t.b, tri + 9 * i + 3, 24);
+      std::memcpy(t.c, tri + 9 * i + 6, 24);
+      t.id = i;
+      t.kind = kind[i];
+      t.value = value_index[i];
+      t.pad_ = 0;
+      need(t.kind == WG_DIRICHLET || t.kind == WG_NEUMANN, WG_ERR_SCENE, "3D scene: bad kind");
+      need(t.value >= 0 && t.value < n_values, WG_ERR_SCENE, "3D scene: value not defined");
+      double nn[3], e1[3], e2[3];
+      for (int a = 0; a < 3; ++a) {
+        e1[a] = t.b[a] - t.a[a];
+        e2[a] = t.c[a] - t.a[a];
+      }
+      cross3(e1, e2, nn);
+      need(std::sqrt(nn[0] * nn[0] + nn[1] * nn[1] + nn[2] * nn[2]) != 0.0, WG_ERR_SCENE,
+           "3D scene: degenerate triangle");
+      if (eps > 0.0) {
+        for (const double* p : {t.a, t.b, t.c})
+          for (int a = 0; a < 3; ++a)
+            need(p[a] >= bbox[a] && p[a] <= bbox[3 + a], WG_ERR_SCENE, "3D scene: vertex outside scene bbox");
+      }
+      if (t.kind == WG_NEUMANN)
+        need(values[t.value].type == WG_VALUE_CONSTANT && values[t.value].c0 == 0.0, WG_ERR_INVALID,
+             "3D scene: Neumann flux must be zero");
+      HBox b;
+      b.grow(t.a);
+      b.grow(t.b);
+      b.grow(t.c);
+      root.grow(b);
+      boxes[t.kind].push_back(b);
+      ids[t.kind].push_back(i);
+    }
+    double rd = 0.0, sd = 0.0;
+    for (int a = 0; a < 3; ++a) {
+      rd += (root.hi[a] - root.lo[a]) * (root.hi[a] - root.lo[a]);
+      sd += (bbox[3 + a] - bbox[a]) * (bbox[3 + a] - bbox[a]);
+    }
+    s->t_eps = 1e-6 * std::sqrt(rd);
+    s->diag = std::sqrt(sd);
+    s->n_tri = n_tri;
+    Scene3View& v = s->view;
+    v = Scene3View{};
+    for (int k = 0; k < 2; ++k) {
+      Builder b(boxes[k]);
+      std::vector<Tri3> leaf(b.order.size());
+      for (size_t i = 0; i < b.order.size(); ++i) leaf[i] = tris[ids[k][b.order[i]]];
+      s->n_node[k] = static_cast<int64_t>(b.nodes.size());
+      if (!b.nodes.empty()) {
+        s->node[k].upload(b.nodes.data(), b.nodes.size());
+        s->tri[k].upload(leaf.data(), leaf.size());
+        v.node[k] = s->node[k].as<Node3>();
+        v.tri[k] = s->tri[k].as<Tri3>();
+      }
+    }
+    std::vector<Edge3> edges = silhouette_edges(tris, &s->n_always, &s->n_crease);
+    if (!edges.empty()) {
+      std::vector<HBox> eb(edges.size());
+      for (size_t i = 0; i < edges.size(); ++i) {
+        eb[i].grow(edges[i].a);
+        eb[i].grow(edges[i].b);
+      }
+      Builder b(eb);
+      std::vector<Edge3> leaf(edges.size());
+      for (size_t i = 0; i < edges.size(); ++i) leaf[i] = edges[b.order[i]];
+      s->n_node[2] = static_cast<int64_t>(b.nodes.size());
+      s->node[2].upload(b.nodes.data(), b.nodes.size());
+      s->edge.upload(leaf.data(), leaf.size());
+      v.node[2] = s->node[2].as<Node3>();
+      v.edge = s->edge.as<Edge3>();
+    }
+    s->values.upload(values, static_cast<size_t>(n_values));
+    v.values = s->values.as<wg_value3_spec>();
+    for (int i = 0; i < 6; ++i) v.bbox[i] = bbox[i];
+    v.t_eps = s->t_eps;
+    v.diag = s->diag;
+    v.eps = s->eps;
+    *out = s.release();
+  });
+}
+
+int wostgpu_scene3_destroy(wg_scene3 s) {
+  return guarded([&] { delete s; });
+}
+
+int wostgpu_scene3_info(wg_scene3 s, double* t_eps, int64_t n_nodes[3], int64_t* n_always,
+                        int64_t* n_crease) {
+  return guarded([&] {
+    if (t_eps) *t_eps = s->t_eps;
+    if (n_nodes)
+      for (int k = 0; k < 3; ++k) n_nodes[k] = s->n_node[k];
+    if (n_always) *n_always = s->n_always;
+    if (n_crease) *n_crease = s->n_crease;
+  });
+}
+
+int wostgpu_closest_point3(wg_scene3 s, int64_t n, const double* x, uint32_t kinds, double* pt,
+                           double* dist, int32_t* tri) {
+  return guarded([&] {
+    if (n <= 0) return;
+    Staged g;
+    const double* dx = g.in(x, 3 * n);
+    double* dp = g.out<double>(3 * n);
+    double* dd = g.out<double>(n);
+    int32_t* dt = g.out<int32_t>(n);
+    cp3_kernel<<<grid_for(n), 128>>>(s->view, n, dx, kinds, dp, dd, dt);
+    CKL(cudaGetLastError());
+    down(pt, dp, 3 * n);
+    down(dist, dd, n);
+    down(tri, dt, n);
+  });
+}
+
+int wostgpu_closest_silhouette3(wg_scene3 s, int64_t n, const double* x, double* dist) {
+  return guarded([&] {
+    if (n <= 0) return;
+    Staged g;
+    const double* dx = g.in(x, 3 * n);
+    double* dd = g.out<double>(n);
+    sil3_kernel<<<grid_for(n), 128>>>(s->view, n, dx, dd);
+    CKL(cudaGetLastError());
+    down(dist, dd, n);
+  });
+}
+
+int wostgpu_ray_first_hit3(wg_scene3 s, int64_t n, const double* o, const double* d,
+                           const double* t_max, uint32_t kinds, const int32_t* exclude, double* t,
+                           double* pt, double* nrm, int32_t* tri, int32_t* kind) {
+  return guarded([&] {
+    if (n <= 0) return;
+    Staged g;
+    const double* dO = g.in(o, 3 * n);
+    const double* dD = g.in(d, 3 * n);
+    const double* dT = g.in(t_max, n);
+    const int32_t* dE = g.in(exclude, n);
+    double* ot = g.out<double>(n);
+    double* op = g.out<double>(3 * n);
+    double* on = g.out<double>(3 * n);
+    int32_t* otri = g.out<int32_t>(n);
+    int32_t* okind = g.out<int32_t>(n);
+    ray3_kernel<<<grid_for(n), 128>>>(s->view, n, dO, dD, dT, kinds, dE, ot, op, on, otri, okind);
+    CKL(cudaGetLastError());
+    down(t, ot, n);
+    down(pt, op, 3 * n);
+    down(nrm, on, 3 * n);
+    down(tri, otri, n);
+    down(kind, okind, n);
+  });
+}
+
+int wostgpu_star_radius3(wg_scene3 s, int64_t n, const double* x, double r_min, double* r) {
+  return guarded([&] {
+    if (n <= 0) return;
+    Staged g;
+    const double* dx = g.in(x, 3 * n);
+    double* dr = g.out<double>(n);
+    int* flag = g.out<int>(1);
+    CK(cudaMemset(flag, 0, sizeof(int)));
+    star3_kernel<<<grid_for(n), 128>>>(s->view, n, dx, r_min, dr, flag);
+    CKL(cudaGetLastError());
+    int h = 0;
+    down(&h, flag, 1);
+    need(h == 0, WG_ERR_SCENE, "star_radius: unbounded star region");
+    down(r, dr, n);
+  });
+}
+
+}  // extern "C"

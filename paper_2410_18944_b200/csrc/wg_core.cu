@@ -488,6 +488,7 @@ int wostgpu_field_set_state(wg_field f, const float* p, const double* m, const d
 
 int wostgpu_field_eval_batch(wg_field f, int64_t n, const double* xy, double* out, int mlp) {
   return guarded([&] {
+    need(f->sdim == 2, WG_ERR_INVALID, "field_eval_batch: 3D field (use wostgpu_field3_eval_batch)");
     need(mlp == WG_MLP_EXACT || default_shape(f->view), WG_ERR_NOT_BUILT,
          "tensor-core field evaluation is built for the default field shape");
     if (n == 0) return;

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "../../include/wostgpu.h"
+#include "wg3_field.cuh"
 #include "wg_kernels.cuh"
 #include "wg_train.cuh"
 
@@ -163,4 +164,9 @@ struct wg_field_s {
   // dirty after any host write of the parameters, kept current by Adam
   wgrt::DBuf wpack;
   bool pack_dirty = true;
+  // spatial dimension: 2 (GuidingField) or 3 (wostgpu_field3_create; view3
+  // and bbox3 describe it, view is unused)
+  int sdim = 2;
+  wg3::Field3View view3{};
+  double bbox3[6] = {0, 0, 0, 0, 0, 0};
 };

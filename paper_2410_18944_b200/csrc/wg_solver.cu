@@ -414,6 +414,8 @@ int wostgpu_solver_create(wg_scene scene, wg_field field, const wg_solver_config
   return guarded([&] {
     check_device();
     need(scene != nullptr, WG_ERR_INVALID, "solver needs a scene");
+    need(field == nullptr || field->sdim == 2, WG_ERR_INVALID,
+         "2D solver: the field is 3D (use wostgpu_solver3_create)");
     bool has_dirichlet = false;
     for (const Seg& g : scene->h_segs) has_dirichlet |= g.kind == WG_DIRICHLET;
     need(has_dirichlet, WG_ERR_SCENE, "solver: scene has no Dirichlet boundary; walks cannot terminate");

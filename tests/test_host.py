@@ -56,8 +56,9 @@ def test_strip_vlin_matches_reference(ref):
 
 
 def test_library_exports_every_header_symbol():
-    """libwostgpu.so exports exactly the entry points include/wostgpu.h declares."""
-    hdr = open(os.path.join(ROOT, "include", "wostgpu.h")).read()
+    """libwostgpu.so exports exactly the entry points include/wostgpu.h and
+    include/wostgpu3.h declare."""
+    hdr = "".join(open(os.path.join(ROOT, "include", h)).read() for h in ("wostgpu.h", "wostgpu3.h"))
     declared = sorted(set(re.findall(r"\b(wostgpu_[a-z_0-9]+)\s*\(", hdr)))
     lib = C.CDLL(_lib.LIB_PATH)
     missing = [s for s in declared if not hasattr(lib, s)]
@@ -101,6 +102,15 @@ def test_ctypes_struct_layouts_match_header(tmp_path):
                      abi.GUIDE_RECORD_DTYPE.itemsize, abi.POINT_STATS_DTYPE.itemsize,
                      C.sizeof(abi.ValueSpec), C.sizeof(abi.FieldConfig), abi.MIXTURE_DTYPE.itemsize]
     assert abi.field_param_count(abi.field_config()) == 94433  # guide_field.hpp defaults
+    src3 = tmp_path / "sz3.c"
+    src3.write_text('#include <stdio.h>\n#include "%s"\nint main(){printf("%%zu %%zu\\n", '
+                    'sizeof(wg_value3_spec), sizeof(wg_guide_record3));}\n'
+                    % os.path.join(ROOT, "include", "wostgpu_types.h"))
+    exe3 = tmp_path / "sz3"
+    subprocess.run(["/usr/bin/gcc", str(src3), "-o", str(exe3)], check=True)
+    sizes3 = [int(x) for x in subprocess.run([str(exe3)], capture_output=True, text=True).stdout.split()]
+    assert sizes3 == [C.sizeof(abi.Value3Spec), abi.GUIDE_RECORD3_DTYPE.itemsize]
+    assert C.sizeof(abi.GuideRecord3) == abi.GUIDE_RECORD3_DTYPE.itemsize
 
 
 def build_facade_demo(out_dir):
