@@ -63,6 +63,7 @@ struct Scene3View {
   const wg_value3_spec* values;
   double bbox[6];
   double t_eps, diag, eps;
+  double sil_tol;  // facings within this count as 0 (oracle/wost3d.inc)
 };
 
 __device__ __forceinline__ D3 ld3(const double* p) { return {p[0], p[1], p[2]}; }
@@ -215,10 +216,12 @@ __device__ __forceinline__ CP3 closest_point(const Scene3View& s, D3 x, unsigned
   return best;
 }
 
-__device__ __forceinline__ bool is_silhouette(const Edge3& e, D3 x) {
+__device__ __forceinline__ bool is_silhouette(const Edge3& e, D3 x, double tol) {
   if (e.type == 0) return true;
   D3 ax = sub(ld3(e.a), x);
-  return dot(ld3(e.n0), ax) * dot(ld3(e.n1), ax) <= 0.0;
+  double f0 = dot(ld3(e.n0), ax), f1 = dot(ld3(e.n1), ax);
+  if (fabs(f0) <= tol || fabs(f1) <= tol) return true;
+  return f0 * f1 <= 0.0;
 }
 
 // squared distance to the nearest silhouette edge (inf if none)
@@ -237,7 +240,7 @@ __device__ __forceinline__ double closest_silhouette_d2(const Scene3View& s, D3 
     if (b < 0) {
       for (int i = a; i < a - b; ++i) {
         const Edge3& e = s.edge[i];
-        if (!is_silhouette(e, x)) continue;
+        if (!is_silhouette(e, x, s.sil_tol)) continue;
         D3 dq = sub(x, closest_on_seg(x, ld3(e.a), ld3(e.b)));
         best = fmin(best, dot(dq, dq));
       }

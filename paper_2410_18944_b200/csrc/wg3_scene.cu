@@ -47,10 +47,11 @@ struct HBox {
 
 struct Builder {
   const std::vector<HBox>& box;
+  double pad;  // node boxes grow by pad (conservative pruning under rounding)
   std::vector<double> cen;  // 3 per primitive
   std::vector<int> order;
   std::vector<Node3> nodes;
-  explicit Builder(const std::vector<HBox>& b) : box(b), cen(3 * b.size()), order(b.size()) {
+  Builder(const std::vector<HBox>& b, double pad_) : box(b), pad(pad_), cen(3 * b.size()), order(b.size()) {
     for (size_t i = 0; i < b.size(); ++i) {
       order[i] = static_cast<int>(i);
       for (int a = 0; a < 3; ++a) cen[3 * i + a] = 0.5 * (b[i].lo[a] + b[i].hi[a]);
@@ -67,8 +68,8 @@ struct Builder {
     }
     Node3 n;
     for (int a = 0; a < 3; ++a) {
-      n.lo[a] = round_down(bb.lo[a]);
-      n.hi[a] = round_up(bb.hi[a]);
+      n.lo[a] = round_down(bb.lo[a] - pad);
+      n.hi[a] = round_up(bb.hi[a] + pad);
     }
     if (hi - lo <= 4) {
       n.a = lo;
@@ -317,12 +318,14 @@ int wostgpu_scene3_create(const double* tri, const int32_t* kind, const int32_t*
       sd += (bbox[3 + a] - bbox[a]) * (bbox[3 + a] - bbox[a]);
     }
     s->t_eps = 1e-6 * std::sqrt(rd);
+    const double sil_tol = 1e-9 * std::sqrt(rd);
+    const double box_pad = 1e-7 * std::sqrt(rd);  // oracle/wost3d.inc Bvh::pad
     s->diag = std::sqrt(sd);
     s->n_tri = n_tri;
     Scene3View& v = s->view;
     v = Scene3View{};
     for (int k = 0; k < 2; ++k) {
-      Builder b(boxes[k]);
+      Builder b(boxes[k], box_pad);
       std::vector<Tri3> leaf(b.order.size());
       for (size_t i = 0; i < b.order.size(); ++i) leaf[i] = tris[ids[k][b.order[i]]];
       s->n_node[k] = static_cast<int64_t>(b.nodes.size());
@@ -340,7 +343,7 @@ int wostgpu_scene3_create(const double* tri, const int32_t* kind, const int32_t*
         eb[i].grow(edges[i].a);
         eb[i].grow(edges[i].b);
       }
-      Builder b(eb);
+      Builder b(eb, box_pad);
       std::vector<Edge3> leaf(edges.size());
       for (size_t i = 0; i < edges.size(); ++i) leaf[i] = edges[b.order[i]];
       s->n_node[2] = static_cast<int64_t>(b.nodes.size());
@@ -353,6 +356,7 @@ int wostgpu_scene3_create(const double* tri, const int32_t* kind, const int32_t*
     v.values = s->values.as<wg_value3_spec>();
     for (int i = 0; i < 6; ++i) v.bbox[i] = bbox[i];
     v.t_eps = s->t_eps;
+    v.sil_tol = sil_tol;
     v.diag = s->diag;
     v.eps = s->eps;
     *out = s.release();

@@ -74,6 +74,14 @@ def test_field3_init_and_eval_bit_exact(gpu, o3):
     o3.field_destroy(fo)
 
 
+def _outside_obstacle(x):
+    """Evaluation points of the obstacle scene must lie in the domain: a walk
+    started inside the insulated obstacle never meets a Dirichlet boundary."""
+    inside = ((x[:, 0] > 0.35) & (x[:, 0] < 0.65) & (x[:, 1] > 0.35) & (x[:, 1] < 0.65) &
+              (x[:, 2] > 0.3) & (x[:, 2] < 0.7))
+    return x[~inside]
+
+
 def _walks(o3, sc, cfg, x, seed, field_o=None, field_g=None):
     ho = o3.scene(sc)
     est_o, esc_o, steps_o = o3.walks(ho, field_o, cfg, x, seed, 0)
@@ -88,7 +96,7 @@ def _walks(o3, sc, cfg, x, seed, field_o=None, field_g=None):
 @pytest.mark.parametrize("name", ["box", "obstacle", "jitter"])
 def test_uniform_walks_match_oracle_per_walk(gpu, o3, name):
     sc = _scenes()[name]
-    x = probes3(31, 3000, 0.05, 0.95)
+    x = _outside_obstacle(probes3(31, 3000, 0.05, 0.95))
     est_o, esc_o, st_o, est_g, esc_g, st_g = _walks(o3, sc, abi.solver_config("uniform"), x, 7)
     close = np.abs(est_o - est_g) <= 1e-9 * np.maximum(1.0, np.abs(est_o))
     assert close.mean() >= 0.999, close.mean()
@@ -106,7 +114,7 @@ def test_guided_walks_exact_mlp_match_oracle(gpu, o3, mode):
     p = p + np.float32(0.3) * np.random.default_rng(8).standard_normal(len(p)).astype(np.float32)
     fg.set_params(p)
     o3.field_set_params(fo, p)
-    x = probes3(41, 1500, 0.05, 0.95)
+    x = _outside_obstacle(probes3(41, 1500, 0.05, 0.95))
     est_o, esc_o, st_o, est_g, esc_g, st_g = _walks(o3, sc, abi.solver_config(mode), x, 99, fo, fg)
     close = np.abs(est_o - est_g) <= 1e-9 * np.maximum(1.0, np.abs(est_o))
     assert close.mean() >= 0.99, close.mean()
@@ -143,7 +151,7 @@ def test_field_grad_matches_oracle(gpu, o3):
     fo, fg = o3.field(cfg_f, BOX, 29), GuidingField3(cfg_f, BOX, 29)
     cfg = abi.solver_config("learnable_mis")
     ho = o3.scene(sc)
-    recs = o3.walk_records(ho, fo, cfg, probes3(3, 600, 0.05, 0.95), 3, 0)
+    recs = o3.walk_records(ho, fo, cfg, _outside_obstacle(probes3(3, 600, 0.05, 0.95)), 3, 0)
     tc = abi.train_config()
     g_o = o3.field_grad(fo, recs, tc)
     sol = Solver3(Accel3(sc), fg, cfg)
@@ -172,8 +180,12 @@ def test_uniform_run_matches_analytic(gpu):
     st = sol.stats()
     ref = strip_vlin_np(x[:, 0], x[:, 1])
     se = np.sqrt(st["m2"] / (st["count"] - 1) / st["count"])
-    z = (st["mean"] - ref) / se
+    # next to x = 0 most walks end on g = 0 and the estimator is strongly
+    # skewed (few non-zero samples): the per-point z test uses the interior
+    ok = (st["m2"] > 0) & (x[:, 0] > 0.1)
+    z = (st["mean"][ok] - ref[ok]) / se[ok]
     assert np.abs(z).max() < 5.0
+    assert (np.abs(z) > 3.0).mean() < 0.01
     assert abs(z.mean()) < 0.2
 
 
@@ -195,6 +207,7 @@ def test_guided_training_reduces_error(gpu):
     sg = g.stats()
     assert tst.steps >= 64 and tst.records_consumed > 0
     rel = lambda s: float(np.mean((s["mean"] - ref) ** 2 / (ref ** 2 + 1e-4)))
-    z = (sg["mean"] - ref) / np.sqrt(sg["m2"] / (sg["count"] - 1) / sg["count"])
+    ok = (sg["m2"] > 0) & (x[:, 0] > 0.1)
+    z = (sg["mean"][ok] - ref[ok]) / np.sqrt(sg["m2"][ok] / (sg["count"][ok] - 1) / sg["count"][ok])
     assert abs(z.mean()) < 0.25
     assert rel(sg) < 1.5 * rel(su), (rel(sg), rel(su))
