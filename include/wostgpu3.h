@@ -61,7 +61,9 @@ int wostgpu_star_radius3(wg_scene3 scene, int64_t n, const double* xyz, double r
  * set_state / destroy apply; the 2D-only calls reject it. */
 int wostgpu_field3_create(const wg_field_config* cfg, const double bbox[6], uint64_t seed,
                           wg_field* out);
-int wostgpu_field3_eval_batch(wg_field field, int64_t n, const double* xyz, double* out);
+/* mlp = WG_MLP_EXACT: fp32 CUDA cores in the oracle's operation order (bit
+ * for bit); WG_MLP_TENSOR: tcgen05 split-fp16 MMAs (~1e-6 relative) */
+int wostgpu_field3_eval_batch(wg_field field, int64_t n, const double* xyz, double* out, int mlp);
 
 /* ---- solver ------------------------------------------------------------------
  * solve_batch / Engine analogues over 3D points (include/wostgpu.h for the
@@ -69,6 +71,10 @@ int wostgpu_field3_eval_batch(wg_field field, int64_t n, const double* xyz, doub
 int wostgpu_solver3_create(wg_scene3 scene, wg_field field, const wg_solver_config* cfg,
                            wg_solver3* out);
 int wostgpu_solver3_destroy(wg_solver3 solver);
+/* MLP path inside guided walks: WG_MLP_TENSOR (default; lockstep 128-walk
+ * CTAs with the tcgen05 MLP) or WG_MLP_EXACT (per-thread fp32 MLP in the
+ * oracle's operation order: per-walk parity with oracle/wost3d.inc) */
+int wostgpu_solver3_set_mlp(wg_solver3 solver, int mlp);
 int wostgpu_solver3_set_points(wg_solver3 solver, int64_t n, const double* xyz,
                                int64_t global_offset);
 int wostgpu_solver3_get_stats(wg_solver3 solver, wg_point_stats* stats);

@@ -89,7 +89,8 @@ _SIGS = {
     "wostgpu_ray_first_hit3": (C.c_int, [VP, C.c_int64, D, D, D, C.c_uint32, I32, D, D, D, I32, I32]),
     "wostgpu_star_radius3": (C.c_int, [VP, C.c_int64, D, C.c_double, D]),
     "wostgpu_field3_create": (C.c_int, [C.POINTER(abi.FieldConfig), D, C.c_uint64, C.POINTER(VP)]),
-    "wostgpu_field3_eval_batch": (C.c_int, [VP, C.c_int64, D, D]),
+    "wostgpu_field3_eval_batch": (C.c_int, [VP, C.c_int64, D, D, C.c_int]),
+    "wostgpu_solver3_set_mlp": (C.c_int, [VP, C.c_int]),
     "wostgpu_solver3_create": (C.c_int, [VP, VP, C.POINTER(abi.SolverConfig), C.POINTER(VP)]),
     "wostgpu_solver3_destroy": (C.c_int, [VP]),
     "wostgpu_solver3_set_points": (C.c_int, [VP, C.c_int64, D, C.c_int64]),

@@ -11,6 +11,7 @@ import numpy as np
 from . import abi
 from ._lib import check, load
 
+MLP_EXACT, MLP_TENSOR = 0, 1
 D = C.POINTER(C.c_double)
 I32 = C.POINTER(C.c_int32)
 
@@ -124,22 +125,27 @@ class GuidingField3:
         _, m, v, st = self.state()
         check(load().wostgpu_field_set_state(self.h, p.ctypes.data_as(C.POINTER(C.c_float)), _d(m), _d(v), st))
 
-    def eval_batch(self, x):
+    def eval_batch(self, x, mlp=MLP_EXACT):
         x = _xyz(x)
         out = np.zeros((len(x), self.output_dim))
-        check(load().wostgpu_field3_eval_batch(self.h, len(x), _d(x), _d(out)))
+        check(load().wostgpu_field3_eval_batch(self.h, len(x), _d(x), _d(out), mlp))
         return out
 
 
 class Solver3:
     """solve_batch / Engine over 3D evaluation points (wostgpu_solver3_*)."""
 
-    def __init__(self, accel: Accel3, field: GuidingField3 | None, cfg: abi.SolverConfig):
+    def __init__(self, accel: Accel3, field: GuidingField3 | None, cfg: abi.SolverConfig, mlp=None):
         self.accel, self.field, self.cfg = accel, field, cfg
         h = C.c_void_p()
         check(load().wostgpu_solver3_create(accel.h, field.h if field else None, C.byref(cfg), C.byref(h)))
         self.h = h
         self.n_points = 0
+        if mlp is not None:
+            self.set_mlp(mlp)
+
+    def set_mlp(self, mlp):
+        check(load().wostgpu_solver3_set_mlp(self.h, mlp))
 
     def __del__(self):
         if getattr(self, "h", None):

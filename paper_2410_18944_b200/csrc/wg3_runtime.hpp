@@ -33,6 +33,10 @@ struct wg_solver3_s {
   wgrt::DBuf recs, rec_counter, rec_tail, rec_term;
   int64_t rec_cap = 0;
   bool have_records = false;
+  // wavefront walk pool (WG_MLP_TENSOR guided walks, wg3_walk_tc.cu)
+  wgrt::DBuf w_lanes, w_dirs, w_rec, w_state, w_queue, w_qlen, w_next;
+  int64_t w_slots = 0;
+  unsigned int* h_qlen = nullptr;  // pinned
   // training
   wgrt::DBuf grad, lists, ctl, totals;
   int64_t list_cap = 0;

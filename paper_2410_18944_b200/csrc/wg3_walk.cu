@@ -17,110 +17,14 @@
 // z, nu_z, n_z in the slots 3D never uses (dacc: 3D scenes have no local
 // source / flux terms, so targets are |S_K / Q_k| without a chain walk).
 #include <cstdio>
+#include <cstdlib>
+#include <string>
 #include <map>
 
-#include "wg3_mix.cuh"
 #include "wg3_runtime.hpp"
+#include "wg3_walk_common.cuh"
 
 namespace wg3 {
-
-using wg::DevRecord;
-using wg::Pcg;
-using wg::REC_ON_NEUMANN;
-using wg::REC_WRITTEN;
-
-struct __align__(16) DevRecord3 {
-  float x, y, nux, nuy, nx, ny;
-  float pdf_mis, pdf_g, pdf_u, c;
-  float target;
-  float z;  // DevRecord::dacc
-  float thr_q;
-  float nuz;  // DevRecord::pad_
-  int32_t walk;
-  uint32_t flags;
-  uint64_t key;
-  int32_t prev;
-  float nz;  // DevRecord::pad2_
-};
-static_assert(sizeof(DevRecord3) == sizeof(DevRecord), "DevRecord3 aliases DevRecord");
-static_assert(offsetof(DevRecord3, pdf_mis) == offsetof(DevRecord, pdf_mis) &&
-                  offsetof(DevRecord3, target) == offsetof(DevRecord, target) &&
-                  offsetof(DevRecord3, thr_q) == offsetof(DevRecord, thr_q) &&
-                  offsetof(DevRecord3, walk) == offsetof(DevRecord, walk) &&
-                  offsetof(DevRecord3, flags) == offsetof(DevRecord, flags) &&
-                  offsetof(DevRecord3, key) == offsetof(DevRecord, key) &&
-                  offsetof(DevRecord3, prev) == offsetof(DevRecord, prev),
-              "fields the shared record kernels read");
-
-// default 3D field shape: 4 levels x 4 features -> 64 -> 64 -> 41 (K = 8)
-constexpr int IN = 16, HID = 64, K8 = 8, OD = 5 * K8 + 1;
-constexpr int MLPN = IN * HID + HID + HID * HID + HID + HID * OD + OD;  // 7913
-
-bool default_shape3(const Field3View& v) {
-  return v.levels == 4 && v.F == 4 && v.in == IN && v.hid == HID && v.od == OD && v.k == K8;
-}
-
-struct Walk3Args {
-  Scene3View s;
-  Field3View f;
-  wg::SolverParams sp;
-  const double* points;  // [n_points][3]
-  int64_t n_points, point_offset;
-  uint64_t seed, wpp_first;
-  int32_t n_rounds;
-  double* est;
-  int32_t* esc;
-  int32_t* steps;
-  DevRecord3* recs;
-  unsigned long long* rec_counter;
-  int64_t rec_capacity;
-  uint64_t key_seed;
-  unsigned long long* counters;  // [0] steps [1] escaped [2] walks [3] rec overflow [4] scene error
-  int32_t* rec_tail;
-  double* rec_term;
-};
-
-struct Lane3 {
-  D3 x, n;
-  double T, acc, R;
-  int tri, depth, round, rec_left, last_rec;
-  bool on_n, alive, rec_ok;
-  Pcg rng;
-  int64_t point, rec_base;
-};
-
-__device__ __forceinline__ void lane3_init(Lane3& w, const Walk3Args& a, int64_t id) {
-  w.round = static_cast<int>(id / a.n_points);
-  w.point = id - static_cast<int64_t>(w.round) * a.n_points;
-  w.x = {a.points[3 * w.point], a.points[3 * w.point + 1], a.points[3 * w.point + 2]};
-  w.n = {0.0, 0.0, 0.0};
-  w.on_n = false;
-  w.tri = -1;
-  w.T = 1.0;
-  w.acc = 0.0;
-  w.R = 0.0;
-  w.depth = 0;
-  w.alive = true;
-  w.rng = Pcg::walk(a.seed, static_cast<uint64_t>(a.point_offset + w.point),
-                    a.wpp_first + static_cast<uint64_t>(w.round));
-  w.last_rec = -1;
-  w.rec_ok = true;
-}
-
-__device__ __forceinline__ void finish3(Lane3& w, const Walk3Args& a, bool escaped, double terminal,
-                                        bool collect) {
-  const int64_t slot = static_cast<int64_t>(w.round) * a.n_points + w.point;
-  a.est[slot] = escaped ? 0.0 : w.acc;
-  a.esc[slot] = escaped ? 1 : 0;
-  if (a.steps) a.steps[slot] = w.depth;
-  atomicAdd(&a.counters[0], static_cast<unsigned long long>(w.depth));
-  if (escaped) atomicAdd(&a.counters[1], 1ull);
-  if (collect) {
-    a.rec_tail[slot] = w.last_rec;
-    a.rec_term[slot] = escaped ? 0.0 : w.T * terminal;
-  }
-  w.alive = false;
-}
 
 template <bool GUIDED>
 __global__ void __launch_bounds__(128) walk3_kernel(Walk3Args a) {
@@ -129,12 +33,10 @@ __global__ void __launch_bounds__(128) walk3_kernel(Walk3Args a) {
     for (int i = threadIdx.x; i < a.f.mlp_count; i += blockDim.x) mlp_s[i] = a.f.p[a.f.w1 + i];
     __syncthreads();
   }
-  const Scene3View& s = a.s;
   const bool collect = a.recs != nullptr;
   const int64_t total = a.n_points * static_cast<int64_t>(a.n_rounds);
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   int64_t next = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const double eps = a.sp.eps, rmin = a.sp.rmin, pad = 1e-9 * s.diag;
   Lane3 w;
   w.alive = false;
   w.rec_base = 0;
@@ -147,122 +49,21 @@ __global__ void __launch_bounds__(128) walk3_kernel(Walk3Args a) {
       next += stride;
       ++walks_done;
     }
-    // ---------------- begin_step (wost.cpp:148-216, d = 3, f = h = 0)
-    CP3 cd = closest_point(s, w.x, WG_KIND_DIRICHLET);
-    const double dd = cd.tri >= 0 ? sqrt(cd.d2) : dinf();
-    if (cd.tri >= 0 && dd <= eps) {
-      const double g = value_at(s.values[s.tri[0][cd.local].value], cd.p);
-      w.acc += w.T * g;
-      finish3(w, a, false, g, collect);
-      continue;
-    }
-    if (w.depth >= a.sp.max_steps) {
-      finish3(w, a, true, 0.0, collect);
-      continue;
-    }
-    if (w.depth > a.sp.rr_depth) {
-      const double q = fmin(1.0, fabs(w.T));
-      if (q <= 0.0 || w.rng.uni() >= q) {
-        finish3(w, a, false, 0.0, collect);
-        continue;
-      }
-      w.T /= q;
-    }
-    const double dsil = closest_silhouette(s, w.x);
-    if (dd == dinf() && dsil == dinf()) {
-      atomicOr(&a.counters[4], 1ull);
-      finish3(w, a, true, 0.0, false);
-      continue;
-    }
-    w.R = fmin(dd, fmax(dsil, rmin));
-    int rec = -1;
-    if (collect && w.rec_ok) {  // trace push (wost.cpp:206-214), chunks of 8 slots
-      if (w.rec_left == 0) {
-        unsigned long long b = atomicAdd(a.rec_counter, 8ull);
-        if (static_cast<int64_t>(b) + 8 > a.rec_capacity) {
-          w.rec_ok = false;
-          atomicAdd(&a.counters[3], 1ull);
-        } else {
-          w.rec_base = static_cast<int64_t>(b);
-          w.rec_left = 8;
-        }
-      }
-      if (w.rec_ok) {
-        rec = static_cast<int>(w.rec_base + (8 - w.rec_left));
-        --w.rec_left;
-      }
-    }
-    // ---------------- direction + finish_step (wost.cpp:111-146, 218-264)
-    D3 nu;
-    double pmis, pg, pu, sel, mult;
+    int rec;
+    if (!step_begin(w, a, collect, rec)) continue;
     if (GUIDED) {
       Mix3<K8> m;
       {
         float raw[OD];
         field3_eval_exact<IN, HID, OD>(a.f, mlp_s, w.x.x, w.x.y, w.x.z, raw);
-        normalize3<K8>(raw, m);
+        decode3(raw, a.sp, m);
       }
-      if (a.sp.mode == WG_MODE_GUIDING_ONLY) m.c = 1.0;
-      else if (a.sp.mode == WG_MODE_FIXED_MIS) m.c = a.sp.fixed_c;
-      Mis3 o = mis_sample(w.rng, m, w.on_n, w.n, a.sp.reflect != 0);
-      nu = o.nu;
-      pmis = o.pmis;
-      pg = o.pg;
-      pu = o.pu;
-      sel = m.c;
-      mult = pu / pmis;
+      step_finish(w, a, collect, rec, &m);
     } else {
-      nu = uniform_sample(w.rng, w.on_n, w.n);
-      pu = uniform_pdf(nu, w.on_n, w.n);
-      pmis = pu;
-      pg = 0.0;
-      sel = 0.0;
-      mult = 1.0;
+      step_finish(w, a, collect, rec, nullptr);
     }
-    if (rec >= 0) {
-      DevRecord3 r;
-      r.x = static_cast<float>(w.x.x);
-      r.y = static_cast<float>(w.x.y);
-      r.z = static_cast<float>(w.x.z);
-      r.nux = static_cast<float>(nu.x);
-      r.nuy = static_cast<float>(nu.y);
-      r.nuz = static_cast<float>(nu.z);
-      r.nx = static_cast<float>(w.n.x);
-      r.ny = static_cast<float>(w.n.y);
-      r.nz = static_cast<float>(w.n.z);
-      r.pdf_mis = static_cast<float>(pmis);
-      r.pdf_g = static_cast<float>(pg);
-      r.pdf_u = static_cast<float>(pu);
-      r.c = static_cast<float>(sel);
-      r.target = 0.0f;
-      r.thr_q = static_cast<float>(GUIDED ? w.T * mult : w.T);
-      r.walk = static_cast<int32_t>(static_cast<int64_t>(w.round) * a.n_points + w.point);
-      r.flags = REC_WRITTEN | (w.on_n ? REC_ON_NEUMANN : 0u);
-      r.key = Pcg::mix(a.key_seed ^ Pcg::mix((static_cast<uint64_t>(a.point_offset + w.point) << 20) ^
-                                             static_cast<uint64_t>(w.depth)));
-      r.prev = w.last_rec;
-      a.recs[rec] = r;
-      w.last_rec = rec;
-    }
-    if (mult == 0.0) {
-      finish3(w, a, false, 0.0, collect);
-      continue;
-    }
-    Hit3 h = ray_first_hit(s, w.x, nu, w.R, WG_KIND_NEUMANN, w.tri);
-    if (h.tri >= 0) {
-      w.x = add(w.x, scl(nu, h.t));
-      w.n = hit_normal(s, h, nu);
-      w.on_n = true;
-      w.tri = h.tri;
-    } else {
-      w.x = add(w.x, scl(nu, w.R));
-      w.on_n = false;
-      w.tri = -1;
-    }
-    if (GUIDED) w.T *= mult;
-    ++w.depth;
-    if (!bbox_contains(s, w.x, pad)) finish3(w, a, true, 0.0, collect);
   }
+  // unused slots of this lane's record chunk are marked invalid
   if (collect)
     for (int i = 0; i < w.rec_left; ++i) a.recs[w.rec_base + (8 - w.rec_left) + i].flags = 0u;
   unsigned long long wd = static_cast<unsigned long long>(walks_done);
@@ -699,11 +500,13 @@ void enqueue3_rounds(wg_solver3_s* s, uint64_t seed, uint64_t wpp_first, int32_t
   a.key_seed = key_seed;
   a.rec_tail = collect ? s->rec_tail.as<int32_t>() : nullptr;
   a.rec_term = collect ? s->rec_term.as<double>() : nullptr;
+  const bool tc = guided && s->mlp == WG_MLP_TENSOR;
   const int smem = guided ? static_cast<int>(sizeof(float) * s->field->view3.mlp_count) : 0;
-  if (guided)
+  if (guided && !tc)
     CK(cudaFuncSetAttribute(walk3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   static int per_sm[2] = {0, 0};
-  if (!per_sm[guided]) per_sm[guided] = walk3_blocks_per_sm(guided, smem);
+  if (!tc && !per_sm[guided]) per_sm[guided] = walk3_blocks_per_sm(guided, smem);
+  const int sm_blocks = tc ? walk3_tc_blocks_per_sm() : per_sm[guided];
   const int sms = sm_count();
   Ev3& e = events()[s];
   for (int32_t r0 = 0; r0 < rounds; r0 += chunk) {
@@ -711,9 +514,38 @@ void enqueue3_rounds(wg_solver3_s* s, uint64_t seed, uint64_t wpp_first, int32_t
     a.wpp_first = wpp_first + r0;
     a.n_rounds = n;
     const int64_t want = (s->n_points * n + 127) / 128;
-    const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm[guided] * sms)));
+    const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_blocks * sms)));
     CK(cudaEventRecord(ev_next(e.walk, e.nw), s->st));
-    if (guided) walk3_kernel<true><<<blocks, 128, smem, s->st>>>(a);
+    // wavefront pair once enough walks are in flight to fill the GPU (measured
+    // on cfg 4, 512^2 points: 9.0M vs 3.0M walks/s multi-round, 4.4M vs 2.5M
+    // per training round); lockstep tiles below that (128^2 training rounds:
+    // the wavefront's per-iteration launches dominate). WOSTGPU_WALK3 =
+    // wave / lockstep forces one.
+    static const int force = [] {
+      const char* e = std::getenv("WOSTGPU_WALK3");
+      if (!e) return 0;
+      return std::string(e) == "wave" ? 1 : std::string(e) == "lockstep" ? 2 : 0;
+    }();
+    const bool wave = force == 1 || (force == 0 && s->n_points * n >= 65536);
+    if (tc && wave) {
+      const int64_t slots = std::min<int64_t>(s->n_points * n, (int64_t)sms * 16 * 128);
+      if (s->w_slots < slots) {
+        s->w_lanes.alloc(sizeof(Lane3) * slots);
+        s->w_dirs.alloc(sizeof(Dir3) * slots);
+        s->w_rec.alloc(sizeof(int32_t) * slots);
+        s->w_state.alloc(slots);
+        s->w_queue.alloc(sizeof(int32_t) * slots);
+        s->w_slots = slots;
+      }
+      s->w_qlen.alloc(2 * sizeof(unsigned int));
+      s->w_next.alloc(sizeof(unsigned long long));
+      if (!s->h_qlen) CK(cudaMallocHost(&s->h_qlen, 4 * sizeof(unsigned int)));
+      Wave3 v{s->w_lanes.as<Lane3>(), s->w_dirs.as<Dir3>(), s->w_rec.as<int32_t>(), s->w_state.as<uint8_t>(),
+              s->w_queue.as<int32_t>(), s->w_qlen.as<unsigned int>(), s->w_next.as<unsigned long long>(),
+              slots};
+      CKL(launch_walks3_wave(a, v, sms, s->h_qlen, s->st));
+    } else if (tc) CKL(launch_walks3_tc(a, blocks, s->st));
+    else if (guided) walk3_kernel<true><<<blocks, 128, smem, s->st>>>(a);
     else walk3_kernel<false><<<blocks, 128, 0, s->st>>>(a);
     CKL(cudaGetLastError());
     CK(cudaEventRecord(ev_next(e.walk, e.nw), s->st));
@@ -842,6 +674,7 @@ uint64_t key_seed3(uint64_t seed, uint64_t wpp) {
 
 wg_solver3_s::~wg_solver3_s() {
   if (comm) nccl().commDestroy(comm);
+  if (h_qlen) cudaFreeHost(h_qlen);
   if (st) cudaStreamDestroy(st);
   auto it = events().find(this);
   if (it != events().end()) {
@@ -907,7 +740,7 @@ int wostgpu_field3_create(const wg_field_config* cfg, const double bbox[6], uint
   });
 }
 
-int wostgpu_field3_eval_batch(wg_field f, int64_t n, const double* x, double* out) {
+int wostgpu_field3_eval_batch(wg_field f, int64_t n, const double* x, double* out, int mlp) {
   return guarded([&] {
     need(f->sdim == 3, WG_ERR_INVALID, "field3_eval_batch: 2D field");
     need(default_shape3(f->view3), WG_ERR_NOT_BUILT, "3D field evaluation is built for the default 3D shape");
@@ -915,6 +748,11 @@ int wostgpu_field3_eval_batch(wg_field f, int64_t n, const double* x, double* ou
     DBuf dx, dout;
     dx.upload(x, static_cast<size_t>(3 * n));
     dout.alloc(sizeof(double) * n * OD);
+    if (mlp == WG_MLP_TENSOR) {
+      CKL(launch_field3_eval_tc(f->view3, n, dx.as<double>(), dout.as<double>(), nullptr));
+      CK(cudaMemcpy(out, dout.p, sizeof(double) * n * OD, cudaMemcpyDeviceToHost));
+      return;
+    }
     const int smem = static_cast<int>(sizeof(float) * f->view3.mlp_count);
     CK(cudaFuncSetAttribute(field3_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int blocks = static_cast<int>(std::min<int64_t>((n + 127) / 128, 148 * 8));
@@ -936,10 +774,18 @@ int wostgpu_solver3_create(wg_scene3 scene, wg_field field, const wg_solver_conf
     s->scene = scene;
     s->field = field;
     s->cfg = *cfg;
+    s->mlp = WG_MLP_TENSOR;  // the tensor-core walk kernel for guided modes (exact: set_mlp)
     CK(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
     s->counters.alloc(sizeof(unsigned long long) * C_N);
     CK(cudaMemset(s->counters.p, 0, sizeof(unsigned long long) * C_N));
     *out = s.release();
+  });
+}
+
+int wostgpu_solver3_set_mlp(wg_solver3 s, int mlp) {
+  return guarded([&] {
+    need(mlp == WG_MLP_EXACT || mlp == WG_MLP_TENSOR, WG_ERR_INVALID, "mlp must be WG_MLP_EXACT or WG_MLP_TENSOR");
+    s->mlp = mlp;
   });
 }
 

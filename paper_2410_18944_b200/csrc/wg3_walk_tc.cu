@@ -1,0 +1,299 @@
+// 3D guided walks with the guiding-field MLP on the 5th-generation tensor
+// cores (the WG_MLP_TENSOR path of the 3D solver; default for the default 3D
+// field shape).
+//
+// Lockstep CTA of 128 threads = one M = 128 tcgen05 tile: every iteration
+//   A  each thread advances its walk through step_begin (fp64 BVH queries);
+//      a walk that ends there is replaced at once by the thread's next walk,
+//      so a row stays busy while walks remain;
+//   B  the rows that need a direction gather their trilinear features (fp32,
+//      one 16-B load per lattice corner) and the CTA runs the 3-layer MLP
+//      on the tensor cores (wg_mlp_tc.cuh: split-fp16 operands, fp32 TMEM
+//      accumulation, ~1e-6 relative to the fp32 MLP; the 41 outputs fit the
+//      N = 48 last layer);
+//   C  fp64 normalisation, d = 3 MIS sampling, ray and move (step_finish).
+// Weights are split into fp16 hi/lo once per CTA from the fp32 parameters.
+// This translation unit may contract FMAs (Makefile FAST_TUS): its results
+// are compared with the oracle statistically, the exact kernel bit for bit.
+#include "wg3_walk_common.cuh"
+#include "wg_mlp_tc.cuh"
+
+namespace wg3 {
+
+__device__ __forceinline__ void gather3_tc(const Field3View& f, D3 x, float* in) {
+  const float u = static_cast<float>(wg::sclamp((x.x - f.bbox[0]) / (f.bbox[3] - f.bbox[0]), 0.0, 1.0));
+  const float v = static_cast<float>(wg::sclamp((x.y - f.bbox[1]) / (f.bbox[4] - f.bbox[1]), 0.0, 1.0));
+  const float q = static_cast<float>(wg::sclamp((x.z - f.bbox[2]) / (f.bbox[5] - f.bbox[2]), 0.0, 1.0));
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    const int res = f.res[l];
+    const float rm = static_cast<float>(res - 1);
+    const float px = u * rm, py = v * rm, pz = q * rm;
+    const int ix = wg::imin(static_cast<int>(px), res - 2), iy = wg::imin(static_cast<int>(py), res - 2),
+              iz = wg::imin(static_cast<int>(pz), res - 2);
+    const float fx = px - ix, fy = py - iy, fz = pz - iz, gx = 1.0f - fx, gy = 1.0f - fy, gz = 1.0f - fz;
+    const float4* b = reinterpret_cast<const float4*>(f.p + f.lvl_off[l]) + (iz * res + iy) * res + ix;
+    const int sy = res, sz = res * res;
+    const float4 c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + sy), c110 = __ldg(b + sy + 1);
+    const float4 c001 = __ldg(b + sz), c101 = __ldg(b + sz + 1), c011 = __ldg(b + sz + sy),
+                 c111 = __ldg(b + sz + sy + 1);
+    const float w00 = gx * gy, w10 = fx * gy, w01 = gx * fy, w11 = fx * fy;
+    const float a0 = w00 * gz, a1 = w10 * gz, a2 = w01 * gz, a3 = w11 * gz;
+    const float a4 = w00 * fz, a5 = w10 * fz, a6 = w01 * fz, a7 = w11 * fz;
+#define WG3_MIX(C)                                                                                     \
+  ((a0 * c000.C + a1 * c100.C) + (a2 * c010.C + a3 * c110.C)) +                                        \
+      ((a4 * c001.C + a5 * c101.C) + (a6 * c011.C + a7 * c111.C))
+    in[4 * l + 0] = WG3_MIX(x);
+    in[4 * l + 1] = WG3_MIX(y);
+    in[4 * l + 2] = WG3_MIX(z);
+    in[4 * l + 3] = WG3_MIX(w);
+#undef WG3_MIX
+  }
+}
+
+__device__ __forceinline__ void tc3_prologue(unsigned char* smem, const Field3View& f) {
+  wg::tc_stage_weights_raw(smem, f.p, f.w1, f.b1, f.w2, f.b2, f.w3, f.b3, OD);
+  wg::tc_setup(smem);
+  wg::umma::fence_before();
+  __syncthreads();
+  wg::umma::fence_after();
+}
+
+__global__ void __launch_bounds__(128, 1) walk3_tc_kernel(Walk3Args a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  tc3_prologue(smem, a.f);
+  const bool collect = a.recs != nullptr;
+  const int64_t total = a.n_points * static_cast<int64_t>(a.n_rounds);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t next = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint32_t phase = 0;
+  Lane3 w;
+  w.alive = false;
+  w.rec_base = 0;
+  w.rec_left = 0;
+  int64_t walks_done = 0;
+  for (;;) {
+    // ---- A: advance to a step that needs a direction (or run out of walks)
+    bool need = false;
+    int rec = -1;
+    while (!need) {
+      if (!w.alive) {
+        if (next >= total) break;
+        lane3_init(w, a, next);
+        next += stride;
+        ++walks_done;
+      }
+      need = step_begin(w, a, collect, rec);
+    }
+    if (__syncthreads_count(need) == 0) break;
+    // ---- B: features + MLP on the tensor cores for the whole tile
+    float in[IN], raw[OD];
+    if (need) {
+      gather3_tc(a.f, w.x, in);
+    } else {
+#pragma unroll
+      for (int i = 0; i < IN; ++i) in[i] = 0.0f;
+    }
+    wg::tc_forward<OD>(smem, phase, in, raw);
+    // ---- C: mixture, MIS direction, move
+    if (need) {
+      Mix3<K8> m;
+      decode3(raw, a.sp, m);
+      step_finish(w, a, collect, rec, &m);
+    }
+  }
+  if (collect)
+    for (int i = 0; i < w.rec_left; ++i) a.recs[w.rec_base + (8 - w.rec_left) + i].flags = 0u;
+  unsigned long long wd = static_cast<unsigned long long>(walks_done);
+  for (int o = 16; o > 0; o >>= 1) wd += __shfl_down_sync(0xffffffffu, wd, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&a.counters[2], wd);
+  wg::tc_teardown(smem);
+}
+
+// field evaluation on the tensor cores: persistent CTAs over 128-point tiles
+__global__ void __launch_bounds__(128) field3_eval_tc_kernel(Field3View f, int64_t n, const double* x,
+                                                             double* out) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  tc3_prologue(smem, f);
+  uint32_t phase = 0;
+  const int64_t tiles = (n + 127) / 128;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int64_t i = t * 128 + threadIdx.x;
+    float in[IN], o[OD];
+    if (i < n) {
+      gather3_tc(f, D3{x[3 * i], x[3 * i + 1], x[3 * i + 2]}, in);
+    } else {
+#pragma unroll
+      for (int k = 0; k < IN; ++k) in[k] = 0.0f;
+    }
+    wg::tc_forward<OD>(smem, phase, in, o);
+    if (i < n)
+      for (int j = 0; j < OD; ++j) out[i * OD + j] = o[j];
+  }
+  wg::tc_teardown(smem);
+}
+
+// ---------------------------------------------------------------- wavefront
+// The guided 3D walk as two kernels per iteration over a pool of walk slots
+// (lane state in HBM, ~200 B per slot):
+//   wave_geom_kernel  one thread per slot (high occupancy for the latency-bound
+//                     fp64 BVH traversals): finishes the slot's pending move
+//                     (record, Neumann ray, move, escape), refills an empty
+//                     slot with the next walk id, runs step_begin, and queues
+//                     the slot when it needs a direction;
+//   wave_dir_kernel   persistent tcgen05 tiles over the queue: trilinear
+//                     gather, the MLP, then per row the fp64 decode and MIS
+//                     sampling (no BVH work, so no lockstep divergence).
+// The host re-launches the pair until a geometry pass queues nothing.
+enum : uint8_t { SLOT_EMPTY = 0, SLOT_NEED_DIR = 1, SLOT_NEED_MOVE = 2 };
+
+__global__ void __launch_bounds__(128) wave_geom_kernel(Walk3Args a, Wave3 v, int parity) {
+  const bool collect = a.recs != nullptr;
+  const unsigned long long total = static_cast<unsigned long long>(a.n_points) * a.n_rounds;
+  unsigned int* qlen = v.qlen + parity;
+  unsigned long long started = 0;
+  for (int64_t slot = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; slot < v.slots;
+       slot += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint8_t st = v.state[slot];
+    Lane3 w;
+    // a collecting slot carries its record chunk (rec_base / rec_left) from
+    // walk to walk, so the lane is loaded even when the slot is empty
+    if (st == SLOT_NEED_MOVE || collect) w = v.lanes[slot];
+    if (st != SLOT_NEED_MOVE) w.alive = false;
+    if (st == SLOT_NEED_MOVE) step_move(w, a, collect, v.rec[slot], v.dirs[slot], true);
+    bool need = false;
+    int rec = -1;
+    for (int tries = 0; tries < 4 && !need; ++tries) {
+      if (!w.alive) {
+        const unsigned long long id = atomicAdd(v.next_walk, 1ull);
+        if (id >= total) break;
+        lane3_init(w, a, static_cast<int64_t>(id));
+        if (!collect) {
+          w.rec_base = 0;
+          w.rec_left = 0;
+        }
+        ++started;
+      }
+      need = step_begin(w, a, collect, rec);
+    }
+    if (need) {
+      v.lanes[slot] = w;
+      v.rec[slot] = rec;
+      v.state[slot] = SLOT_NEED_DIR;
+      v.queue[atomicAdd(qlen, 1u)] = static_cast<int32_t>(slot);
+    } else {
+      if (collect) v.lanes[slot] = w;  // record-chunk bookkeeping
+      v.state[slot] = SLOT_EMPTY;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) started += __shfl_down_sync(0xffffffffu, started, o);
+  if ((threadIdx.x & 31) == 0 && started) atomicAdd(&a.counters[2], started);
+}
+
+__global__ void __launch_bounds__(128) wave_dir_kernel(Walk3Args a, Wave3 v, int parity) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  if (blockIdx.x == 0 && threadIdx.x == 0) v.qlen[parity ^ 1] = 0u;  // next geometry pass's queue
+  const unsigned int n = v.qlen[parity];
+  if (static_cast<unsigned int>(blockIdx.x) * 128u >= n) return;
+  tc3_prologue(smem, a.f);
+  uint32_t phase = 0;
+  for (unsigned int t = blockIdx.x; t * 128u < n; t += gridDim.x) {
+    const unsigned int row = t * 128u + threadIdx.x;
+    const bool live = row < n;
+    int32_t slot = live ? v.queue[row] : 0;
+    float in[IN], raw[OD];
+    Lane3 w;
+    if (live) {
+      w = v.lanes[slot];
+      gather3_tc(a.f, w.x, in);
+    } else {
+#pragma unroll
+      for (int i = 0; i < IN; ++i) in[i] = 0.0f;
+    }
+    wg::tc_forward<OD>(smem, phase, in, raw);
+    if (live) {
+      Mix3<K8> m;
+      decode3(raw, a.sp, m);
+      v.dirs[slot] = step_sample(w, a, &m);
+      v.lanes[slot].rng = w.rng;
+      v.state[slot] = SLOT_NEED_MOVE;
+    }
+  }
+  wg::tc_teardown(smem);
+}
+
+// trailing record slots of every lane's last chunk are marked unused
+__global__ void wave_close_kernel(Walk3Args a, Wave3 v) {
+  for (int64_t slot = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; slot < v.slots;
+       slot += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const Lane3& w = v.lanes[slot];
+    for (int i = 0; i < w.rec_left; ++i) a.recs[w.rec_base + (8 - w.rec_left) + i].flags = 0u;
+  }
+}
+
+cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsigned int* h_qlen,
+                               cudaStream_t st) {
+  const unsigned long long total = static_cast<unsigned long long>(a.n_points) * a.n_rounds;
+  unsigned long long handed = 0;
+  const int smem = walk3_tc_smem();
+  cudaError_t e = cudaFuncSetAttribute(wave_dir_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(v.state, 0, static_cast<size_t>(v.slots), st);
+  cudaMemsetAsync(v.qlen, 0, 2 * sizeof(unsigned int), st);
+  cudaMemsetAsync(v.next_walk, 0, sizeof(unsigned long long), st);
+  if (a.recs) cudaMemsetAsync(v.lanes, 0, sizeof(Lane3) * static_cast<size_t>(v.slots), st);
+  const int geom_blocks = static_cast<int>((v.slots + 127) / 128);
+  const int dir_blocks = sms * 3;
+  for (int it = 0;; ++it) {
+    const int par = it & 1;
+    wave_geom_kernel<<<geom_blocks, 128, 0, st>>>(a, v, par);
+    wave_dir_kernel<<<dir_blocks, 128, smem, st>>>(a, v, par);
+    if ((it & 7) == 7) {  // every 8 iterations: stop once a geometry pass queued
+                          // nothing and every walk id has been handed out
+      cudaMemcpyAsync(h_qlen, v.qlen + par, sizeof(unsigned int), cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(&handed, v.next_walk, sizeof(handed), cudaMemcpyDeviceToHost, st);
+      e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) return e;
+      if (*h_qlen == 0u && handed >= total) break;
+    }
+  }
+  if (a.recs) wave_close_kernel<<<geom_blocks, 128, 0, st>>>(a, v);
+  return cudaGetLastError();
+}
+
+int walk3_tc_smem() { return static_cast<int>((wg::TcLayout::BYTES + 127) / 128 * 128); }
+
+int walk3_tc_blocks_per_sm() {
+  static int n = [] {
+    int b = 0;
+    const int smem = walk3_tc_smem();
+    cudaFuncSetAttribute(walk3_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, walk3_tc_kernel, 128, smem);
+    return b < 1 ? 1 : b;
+  }();
+  return n;
+}
+
+cudaError_t launch_walks3_tc(const Walk3Args& a, int blocks, cudaStream_t st) {
+  const int smem = walk3_tc_smem();
+  cudaError_t e = cudaFuncSetAttribute(walk3_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  walk3_tc_kernel<<<blocks, 128, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_field3_eval_tc(const Field3View& f, int64_t n, const double* x, double* out,
+                                  cudaStream_t st) {
+  const int smem = walk3_tc_smem();
+  cudaError_t e =
+      cudaFuncSetAttribute(field3_eval_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int64_t tiles = (n + 127) / 128;
+  const int blocks = static_cast<int>(tiles < sms * 2 ? tiles : sms * 2);
+  field3_eval_tc_kernel<<<blocks > 0 ? blocks : 1, 128, smem, st>>>(f, n, x, out);
+  return cudaGetLastError();
+}
+
+}  // namespace wg3

@@ -56,11 +56,13 @@ __device__ __forceinline__ void tc_wait_weights(unsigned char* sm) {
 }
 
 
-// Stage B_l = W_l^T as split fp16 in the K-major layout, plus the biases.
-// Called by all threads of the CTA; caller syncs afterwards.
-__device__ __forceinline__ void tc_stage_weights(unsigned char* sm, const FieldView& f) {
+// Stage B_l = W_l^T as split fp16 in the K-major layout, plus the biases,
+// from fp32 parameters at absolute offsets (w1..b3) with `no` outputs
+// (<= NO_PAD: 33 for the 2D field, 41 for the 3D one). Called by all threads
+// of the CTA; caller syncs afterwards.
+__device__ __forceinline__ void tc_stage_weights_raw(unsigned char* sm, const float* p, int w1, int b1,
+                                                     int w2, int b2, int w3, int b3, int no) {
   using L = TcLayout;
-  const float* p = f.p;
   auto put = [&](uint32_t hi_off, uint32_t lo_off, int n, int k, int K, float v) {
     __half h, l;
     umma::split_f16(v, h, l);
@@ -70,24 +72,26 @@ __device__ __forceinline__ void tc_stage_weights(unsigned char* sm, const FieldV
   };
   for (int e = threadIdx.x; e < L::NH * L::NIN; e += blockDim.x) {  // W1[k][n], k < 16
     int n = e % L::NH, k = e / L::NH;
-    put(L::B1_HI, L::B1_LO, n, k, L::NIN, p[f.w1 + k * L::NH + n]);
+    put(L::B1_HI, L::B1_LO, n, k, L::NIN, p[w1 + k * L::NH + n]);
   }
   for (int e = threadIdx.x; e < L::NH * L::NH; e += blockDim.x) {
     int n = e % L::NH, k = e / L::NH;
-    put(L::B2_HI, L::B2_LO, n, k, L::NH, p[f.w2 + k * L::NH + n]);
+    put(L::B2_HI, L::B2_LO, n, k, L::NH, p[w2 + k * L::NH + n]);
   }
   for (int e = threadIdx.x; e < L::NO_PAD * L::NH; e += blockDim.x) {
     int n = e % L::NO_PAD, k = e / L::NO_PAD;
-    put(L::B3_HI, L::B3_LO, n, k, L::NH, n < L::NO ? p[f.w3 + k * L::NO + n] : 0.0f);
+    put(L::B3_HI, L::B3_LO, n, k, L::NH, n < no ? p[w3 + k * no + n] : 0.0f);
   }
   float* bias = reinterpret_cast<float*>(sm + L::BIAS);
   for (int i = threadIdx.x; i < L::NH; i += blockDim.x) {
-    bias[i] = p[f.b1 + i];
-    bias[L::NH + i] = p[f.b2 + i];
+    bias[i] = p[b1 + i];
+    bias[L::NH + i] = p[b2 + i];
   }
-  for (int i = threadIdx.x; i < L::NO_PAD; i += blockDim.x)
-    bias[2 * L::NH + i] = i < L::NO ? p[f.b3 + i] : 0.0f;
+  for (int i = threadIdx.x; i < L::NO_PAD; i += blockDim.x) bias[2 * L::NH + i] = i < no ? p[b3 + i] : 0.0f;
   umma::fence_async_smem();
+}
+__device__ __forceinline__ void tc_stage_weights(unsigned char* sm, const FieldView& f) {
+  tc_stage_weights_raw(sm, f.p, f.w1, f.b1, f.w2, f.b2, f.w3, f.b3, TcLayout::NO);
 }
 
 // One-time TMEM allocation (warp 0) and mbarrier init; caller syncs after.
@@ -375,9 +379,12 @@ __device__ __forceinline__ void tc_gather(const FieldView& f, double x, double y
 }
 
 // Forward pass of the whole 128-row tile. Every thread of the CTA calls it
-// with its row's 16 inputs (zeros for idle rows); out[0..32] = raw outputs.
+// with its row's 16 inputs (zeros for idle rows); out[0..NO) = raw outputs
+// (NO = 33 for the 2D field, 41 for the 3D one; both fit the N = 48 layer).
+template <int NO = TcLayout::NO>
 __device__ __forceinline__ void tc_forward(unsigned char* sm, uint32_t& phase, const float* x,
                                            float* out, long long* bp = nullptr) {
+  static_assert(NO <= TcLayout::NO_PAD, "output width exceeds the padded layer");
   long long* mma_cyc = bp;
   long long tq = bp ? clock64() : 0;
   using L = TcLayout;
@@ -469,7 +476,7 @@ __device__ __forceinline__ void tc_forward(unsigned char* sm, uint32_t& phase, c
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       int j = 16 * c + i;
-      if (j < L::NO) out[j] = a[i] * inv + bias[2 * L::NH + j];
+      if (j < NO) out[j] = a[i] * inv + bias[2 * L::NH + j];
     }
   }
   // TMEM columns are rewritten by the next tile's MMAs: order these loads first

@@ -11,7 +11,7 @@ import pytest
 from fixtures3 import directions3, jittered_box, probes3, soup_scene
 from oracle_lib import Oracle3
 from paper_2410_18944_b200 import abi
-from paper_2410_18944_b200.api3 import Accel3, GuidingField3, Solver3
+from paper_2410_18944_b200.api3 import MLP_EXACT, MLP_TENSOR, Accel3, GuidingField3, Solver3
 from paper_2410_18944_b200.scene3 import make_preset3, slice_points, strip_vlin_np
 
 pytestmark = pytest.mark.gpu
@@ -85,7 +85,7 @@ def _outside_obstacle(x):
 def _walks(o3, sc, cfg, x, seed, field_o=None, field_g=None):
     ho = o3.scene(sc)
     est_o, esc_o, steps_o = o3.walks(ho, field_o, cfg, x, seed, 0)
-    sol = Solver3(Accel3(sc), field_g, cfg)
+    sol = Solver3(Accel3(sc), field_g, cfg, MLP_EXACT)
     sol.set_points(x)
     sol.solve_rounds(seed, 0, 1)
     est_g, esc_g, steps_g = sol.walks()
@@ -131,7 +131,7 @@ def test_records_match_oracle(gpu, o3):
     x = slice_points(24, 24)
     ho = o3.scene(sc)
     rec_o = o3.walk_records(ho, fo, cfg, x, 5, 0)
-    sol = Solver3(Accel3(sc), fg, cfg)
+    sol = Solver3(Accel3(sc), fg, cfg, MLP_EXACT)
     sol.set_points(x)
     sol.solve_rounds(5, 0, 1, collect=True)
     rec_g = sol.records()
@@ -211,3 +211,43 @@ def test_guided_training_reduces_error(gpu):
     z = (sg["mean"][ok] - ref[ok]) / np.sqrt(sg["m2"][ok] / (sg["count"][ok] - 1) / sg["count"][ok])
     assert abs(z.mean()) < 0.25
     assert rel(sg) < 1.5 * rel(su), (rel(sg), rel(su))
+
+
+def test_field3_tensor_eval_matches_exact(gpu):
+    """tcgen05 MLP (split-fp16 operands, fp32 accumulation) against the exact
+    fp32 evaluation: 1e-4 of each row's scale (the 2D path's bound)."""
+    cfg = abi.field_config3()
+    f = GuidingField3(cfg, BOX, 41)
+    p = f.params()
+    p = p + np.float32(0.2) * np.random.default_rng(4).standard_normal(len(p)).astype(np.float32)
+    f.set_params(p)
+    x = probes3(7, 5000, -0.05, 1.05)
+    a, b = f.eval_batch(x, MLP_EXACT), f.eval_batch(x, MLP_TENSOR)
+    scale = np.maximum(np.abs(a).max(axis=1, keepdims=True), 1e-3)
+    assert (np.abs(a - b) / scale).max() < 1e-4
+
+
+@pytest.mark.parametrize("mode", ["learnable_mis", "guiding_only"])
+def test_tensor_walks_match_exact_statistically(gpu, mode):
+    """Guided walks with the tcgen05 MLP kernel against the exact kernel on
+    the obstacle scene (reflection, creases): per-point means over 128 walks
+    agree within 4.5 combined SE, and the mean z is centred."""
+    sc = make_preset3("box-strip-vlin-obstacle", n=12).scene
+    cfg_f = abi.field_config3()
+    f = GuidingField3(cfg_f, BOX, 5)
+    p = f.params()
+    p = p + np.float32(0.3) * np.random.default_rng(6).standard_normal(len(p)).astype(np.float32)
+    f.set_params(p)
+    x = _outside_obstacle(probes3(8, 400, 0.08, 0.92))
+    out = []
+    for mlp in (MLP_EXACT, MLP_TENSOR):
+        s = Solver3(Accel3(sc), f, abi.solver_config(mode), mlp)
+        s.set_points(x)
+        s.run(12, 128, 0, None)
+        out.append(s.stats())
+    a, b = out
+    se = np.sqrt(a["m2"] / (a["count"] - 1) / a["count"] + b["m2"] / (b["count"] - 1) / b["count"])
+    ok = se > 0
+    z = (a["mean"][ok] - b["mean"][ok]) / se[ok]
+    assert np.abs(z).max() < 4.5
+    assert abs(z.mean()) < 4.0 / np.sqrt(ok.sum())
