@@ -9,6 +9,7 @@ device walk round plus a training round) = 4,194,304 walks per GPU.
 
   python bench.py [--gpus N --steps K --warmup W]          our CUDA path
   python bench.py --impl reference [...]                   the reference C++ on host cores
+  python bench.py --workload cfg4|cfg5 [...]               the 3D path (configs[3], configs[4])
 
 N > 1 (torchrun, one rank per GPU): weak scaling; rank r owns rows
 [128 r, 128 r + 128) of a 128 x 128N grid over the same domain (global point
@@ -160,6 +161,193 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+# ---------------------------------------------------------------- 3D (cfg 4 / 5)
+# cfg 4 (BASELINE.json configs[3]): box-strip-vlin, the unit box as 99,372
+# triangles (Dirichlet x = 0 / x = 1, insulated lateral faces), a 512 x 512
+# slice at z = 0.5, 1024 walks per point, learnable MIS with online training
+# for the first 256 rounds. cfg 5 (configs[4]): the same domain, 2048 x 2048 =
+# 4,194,304 points x 1024 walks sharded over the GPUs (strong scaling).
+# Algorithmic HBM bytes per 3D walk step: 60 B SoA state read +
+# written = 120 B; training rounds add a 68 B record written + read = 136 B.
+BYTES_PER_STEP3 = 120
+BYTES_PER_TRAIN_STEP3 = 136
+
+
+def cpu_oracle3_rate(grid, rounds, train_until, threads):
+    """The 3D oracle (oracle/wost3d.inc, a port: the reference has no 3D code)
+    on the host cores: `rounds` wpp rounds of the same workload on a grid x
+    grid slice."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import Oracle3
+    from paper_2410_18944_b200 import abi
+    from paper_2410_18944_b200.scene3 import make_preset3, slice_points
+    os.environ["OMP_NUM_THREADS"] = str(threads)
+    o3 = Oracle3()
+    p = make_preset3("box-strip-vlin")
+    h = o3.scene(p.scene)
+    f = o3.field(abi.field_config3(), (0, 0, 0, 1, 1, 1), SEED)
+    x = slice_points(grid, grid)
+    t0 = time.perf_counter()
+    o3.run(h, f, abi.solver_config("learnable_mis"), x, SEED, rounds, train_until, abi.train_config(seed=SEED))
+    sec = time.perf_counter() - t0
+    o3.field_destroy(f)
+    o3.scene_destroy(h)
+    walks = grid * grid * rounds
+    return {"value": walks / sec, "seconds": sec, "walks": walks, "kind": "port"}
+
+
+def main3(args):
+    cfg5 = args.workload == "cfg5"
+    grid = args.grid or (2048 if cfg5 else 512)
+    wpp = args.wpp or 1024
+    train_until = min(args.train_until, wpp)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":  # the 3D oracle port on the host cores
+        if rank != 0:
+            return
+        threads = os.cpu_count() or 1
+        g, r = 48, 2
+        for _ in range(args.warmup):
+            cpu_oracle3_rate(g, r, r, threads)
+        rr = [cpu_oracle3_rate(g, r, r, threads) for _ in range(args.steps)]
+        value = float(np.mean([x["value"] for x in rr]))
+        sample = (f"{r} wpp rounds (both training rounds) of a {g}x{g} slice of {args.workload}'s domain "
+                  f"through the 3D oracle port (oracle/wost3d.inc; the reference has no 3D code)")
+        print(json.dumps({"metric": "guided WoSt walks/sec", "value": value, "unit": "walks/s",
+                          "impl": "reference", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": float(np.mean([x["seconds"] for x in rr])) * 1e3,
+                          "higher_is_better": True, "scaling": "strong" if cfg5 else "weak",
+                          "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                          "config": {"workload": f"{args.workload} oracle-port sample {g}x{g} x {r} wpp"},
+                          "cpu_baseline": {"value": value, "unit": "walks/s", "cores": threads, "kind": "port",
+                                           "sample": sample},
+                          "e2e": {"value": value, "unit": "walks/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}))
+        return
+
+    import torch
+    from paper_2410_18944_b200 import _lib, abi
+    from paper_2410_18944_b200.api3 import Accel3, GuidingField3, MLP_TENSOR, Solver3
+    from paper_2410_18944_b200.parallel import broadcast_comm_id, shard_points
+    from paper_2410_18944_b200.scene import relmse
+    from paper_2410_18944_b200.scene3 import make_preset3, slice_points, strip_vlin_np
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    _lib.init(local)
+    preset = make_preset3("box-strip-vlin")
+    # cfg 5: strong scaling, the fixed 2048^2 slice split over ranks; cfg 4: weak
+    # scaling, rank r owns rows [grid r, grid (r+1)) of a grid x grid*world slice
+    all_pts = slice_points(grid, grid if cfg5 else grid * world)
+    pts, offset = shard_points(all_pts, world, rank)
+    n_local = len(pts)
+    box = (0.0, 0.0, 0.0, 1.0, 1.0, 1.0)
+    field = GuidingField3(abi.field_config3(), box, SEED)
+    p0, m0, v0, s0 = field.state()
+    acc = Accel3(preset.scene)
+    solver = Solver3(acc, field, abi.solver_config("learnable_mis"), MLP_TENSOR)
+    if world > 1:
+        solver.attach_comm(broadcast_comm_id(dist, rank), world, rank)
+    tcfg = abi.train_config(seed=SEED)
+    solver.set_points(pts, offset)
+    l2 = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def one_step():
+        field.set_state(p0, m0, v0, s0)
+        flush_l2(l2)
+        torch.cuda.synchronize()
+        _, ms = solver.run(SEED, wpp, train_until, tcfg)
+        return ms
+
+    for _ in range(args.warmup):
+        one_step()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.kernel_launches()
+    times, prof = [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            times.append(one_step())
+            prof.append(solver.run_profile())
+    launches = (_lib.kernel_launches() - launches0) // max(1, args.steps)
+    total_ms = float(np.sum(times))
+    if dist:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    walks_per_step = len(all_pts) * wpp
+    value = walks_per_step * args.steps / (total_ms * 1e-3)
+    ref = strip_vlin_np(pts[:, 0], pts[:, 1])
+    rel_guided = relmse(solver.stats()["mean"], ref)
+    pr = prof[-1]
+    peaks, peak_kind = measured_peaks()
+    alg = pr["steps"] * BYTES_PER_STEP3 + pr["train_steps"] * BYTES_PER_TRAIN_STEP3
+    achieved = alg / (pr["walk_ms"] * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "wave_geom_kernel + wave_dir_kernel (3D wavefront)",
+                "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_source": peak_kind,
+                "algorithmic_bytes_per_step": alg, "walk_ms_per_step": pr["walk_ms"],
+                "train_ms_per_step": pr["train_ms"], "walk_steps_per_step": pr["steps"]}
+    ncu_json = os.path.join(ROOT, "profiles", "ncu_counters_wave_geom_kernel.json")
+    if os.path.exists(ncu_json):
+        with open(ncu_json) as f:
+            nc = json.load(f)
+        roofline["traffic"] = nc.get("dram_bytes")
+        roofline["traffic_source"] = os.path.relpath(ncu_json, ROOT)
+    # e2e through the public API with host buffers
+    field.set_state(p0, m0, v0, s0)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    solver.set_points(pts, offset)
+    solver.run(SEED, wpp, train_until, tcfg)
+    _ = solver.stats()
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    quality = {"relmse_guided": rel_guided}
+    if world == 1:  # uniform at equal samples
+        us = Solver3(acc, None, abi.solver_config("uniform"))
+        us.set_points(pts, offset)
+        _, ums = us.run(SEED, wpp, 0, None)
+        rel_u = relmse(us.stats()["mean"], ref)
+        quality.update({"relmse_uniform_equal_wpp": rel_u, "vr_factor": rel_u / rel_guided if rel_guided else None,
+                        "uniform_ms": ums, "uniform_walks_per_s": n_local * wpp / (ums * 1e-3)})
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        g, r = 48, 2
+        c = cpu_oracle3_rate(g, r, r, os.cpu_count() or 1)
+        cpu = {"value": c["value"], "unit": "walks/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"{r} training wpp rounds of a {g}x{g} slice ({c['walks']} walks, {c['seconds']:.1f} s) "
+                         f"through the 3D oracle port (no reference 3D code)"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": "guided WoSt walks/sec", "value": value, "unit": "walks/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(times)),
+            "higher_is_better": True, "scaling": "strong" if cfg5 else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: box-strip-vlin 3D (99,372 triangles), "
+                                   f"{grid}x{grid if cfg5 else grid * world} slice, {wpp} wpp, learnable_mis, "
+                                   f"training rounds < {train_until}",
+                       "grid": [grid, grid if cfg5 else grid * world], "wpp": wpp, "train_until": train_until,
+                       "mlp": "tensor (wavefront)", "l2": "flushed (256 MiB write) before every step",
+                       "parallelism": f"dp{world} (points sharded, NCCL grad allreduce)"},
+            "e2e": {"value": walks_per_step / e2e_s, "unit": "walks/s", "h2d_bytes_per_step": pts.nbytes,
+                    "d2h_bytes_per_step": n_local * abi.POINT_STATS_DTYPE.itemsize},
+            "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
+            "quality": quality}))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -169,7 +357,13 @@ def main():
     ap.add_argument("--mlp", default="tensor", choices=["exact", "tensor"])
     ap.add_argument("--ref-rounds", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg4", "cfg5"])
+    ap.add_argument("--grid", type=int, default=0, help="3D workloads: slice resolution (default 512 / 2048)")
+    ap.add_argument("--wpp", type=int, default=0, help="3D workloads: walks per point (default 1024)")
+    ap.add_argument("--train-until", type=int, default=TRAIN_UNTIL)
     args = ap.parse_args()
+    if args.workload != "cfg2":
+        return main3(args)
     if args.impl == "reference":
         return run_reference(args)
 

@@ -121,9 +121,14 @@ class GuidingField3:
         return p, m, v, st.value
 
     def set_params(self, p):
-        p = np.ascontiguousarray(p, dtype=np.float32)
         _, m, v, st = self.state()
-        check(load().wostgpu_field_set_state(self.h, p.ctypes.data_as(C.POINTER(C.c_float)), _d(m), _d(v), st))
+        self.set_state(p, m, v, st)
+
+    def set_state(self, p, m, v, steps):
+        p = np.ascontiguousarray(p, dtype=np.float32)
+        m = np.ascontiguousarray(m, dtype=np.float64)
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        check(load().wostgpu_field_set_state(self.h, p.ctypes.data_as(C.POINTER(C.c_float)), _d(m), _d(v), steps))
 
     def eval_batch(self, x, mlp=MLP_EXACT):
         x = _xyz(x)

@@ -543,7 +543,9 @@ void enqueue3_rounds(wg_solver3_s* s, uint64_t seed, uint64_t wpp_first, int32_t
       Wave3 v{s->w_lanes.as<Lane3>(), s->w_dirs.as<Dir3>(), s->w_rec.as<int32_t>(), s->w_state.as<uint8_t>(),
               s->w_queue.as<int32_t>(), s->w_qlen.as<unsigned int>(), s->w_next.as<unsigned long long>(),
               slots};
-      CKL(launch_walks3_wave(a, v, sms, s->h_qlen, s->st));
+      int64_t launched = 0;
+      CK(launch_walks3_wave(a, v, sms, s->h_qlen, &launched, s->st));
+      g_launches += launched;
     } else if (tc) CKL(launch_walks3_tc(a, blocks, s->st));
     else if (guided) walk3_kernel<true><<<blocks, 128, smem, s->st>>>(a);
     else walk3_kernel<false><<<blocks, 128, 0, s->st>>>(a);

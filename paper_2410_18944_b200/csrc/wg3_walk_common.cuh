@@ -271,8 +271,9 @@ struct Wave3 {
   unsigned long long* next_walk;  // walk-id hand-out counter
   int64_t slots;
 };
+// returns the number of kernels launched in *launches
 cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& w, int sms, unsigned int* h_qlen,
-                               cudaStream_t st);
+                               int64_t* launches, cudaStream_t st);
 int walk3_tc_smem();
 int walk3_tc_blocks_per_sm();
 cudaError_t launch_walks3_tc(const Walk3Args& a, int blocks, cudaStream_t st);

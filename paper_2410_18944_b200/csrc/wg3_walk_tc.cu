@@ -232,7 +232,8 @@ __global__ void wave_close_kernel(Walk3Args a, Wave3 v) {
 }
 
 cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsigned int* h_qlen,
-                               cudaStream_t st) {
+                               int64_t* launches, cudaStream_t st) {
+  *launches = 0;
   const unsigned long long total = static_cast<unsigned long long>(a.n_points) * a.n_rounds;
   unsigned long long handed = 0;
   const int smem = walk3_tc_smem();
@@ -248,6 +249,7 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsi
     const int par = it & 1;
     wave_geom_kernel<<<geom_blocks, 128, 0, st>>>(a, v, par);
     wave_dir_kernel<<<dir_blocks, 128, smem, st>>>(a, v, par);
+    *launches += 2;
     if ((it & 7) == 7) {  // every 8 iterations: stop once a geometry pass queued
                           // nothing and every walk id has been handed out
       cudaMemcpyAsync(h_qlen, v.qlen + par, sizeof(unsigned int), cudaMemcpyDeviceToHost, st);
@@ -257,7 +259,10 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsi
       if (*h_qlen == 0u && handed >= total) break;
     }
   }
-  if (a.recs) wave_close_kernel<<<geom_blocks, 128, 0, st>>>(a, v);
+  if (a.recs) {
+    wave_close_kernel<<<geom_blocks, 128, 0, st>>>(a, v);
+    *launches += 1;
+  }
   return cudaGetLastError();
 }
 
