@@ -108,7 +108,9 @@ void tri_normal(const double* a, const double* b, const double* c, double* n) {
 
 // silhouette candidates: edges of Neumann triangles keyed by the exact bits
 // of their endpoints; one (or > 2) incident triangles -> always, two
-// non-coplanar -> crease (facing test at query time), coplanar -> dropped
+// non-coplanar -> crease (facing test at query time), coplanar or convex as
+// seen from the domain (n0 . (v1 - a) < 0: never selected by the facing
+// rule from inside) -> dropped (oracle/wost3d.inc)
 std::vector<Edge3> silhouette_edges(const std::vector<Tri3>& tris, int64_t* n_always, int64_t* n_crease) {
   using VK = std::array<uint64_t, 3>;
   auto key = [](const double* p) {
@@ -118,7 +120,7 @@ std::vector<Edge3> silhouette_edges(const std::vector<Tri3>& tris, int64_t* n_al
   };
   struct E {
     double a[3], b[3];
-    std::vector<std::array<double, 3>> n;
+    std::vector<std::array<double, 3>> n, opp;
   };
   std::map<std::pair<VK, VK>, E> m;
   for (const Tri3& t : tris) {
@@ -138,6 +140,9 @@ std::vector<Edge3> silhouette_edges(const std::vector<Tri3>& tris, int64_t* n_al
       std::memcpy(e.a, p, 24);
       std::memcpy(e.b, q, 24);
       e.n.push_back(n);
+      std::array<double, 3> o;
+      std::memcpy(o.data(), v[(i + 2) % 3], 24);
+      e.opp.push_back(o);
     }
   }
   std::vector<Edge3> out;
@@ -150,6 +155,8 @@ std::vector<Edge3> silhouette_edges(const std::vector<Tri3>& tris, int64_t* n_al
     if (e.n.size() == 2) {
       const auto &n0 = e.n[0], &n1 = e.n[1];
       if (n0[0] * n1[0] + n0[1] * n1[1] + n0[2] * n1[2] > 1.0 - 1e-9) continue;  // coplanar
+      const auto& o1 = e.opp[1];
+      if (n0[0] * (o1[0] - e.a[0]) + n0[1] * (o1[1] - e.a[1]) + n0[2] * (o1[2] - e.a[2]) < 0.0) continue;
       g.type = 1;
       std::memcpy(g.n0, n0.data(), 24);
       std::memcpy(g.n1, n1.data(), 24);

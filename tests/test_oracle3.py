@@ -43,15 +43,18 @@ def test_box_closed_forms(o3):
     assert np.isinf(t2).all()
     r = o3.star_radius(h, x, 1e-3)
     assert (r <= d + 0.0).all()
-    assert o3.silhouette_info(h) == (8 * 8, 4 * 8)  # x-face perimeters always; lateral creases
+    # x-face perimeters are always silhouettes; the lateral creases are convex
+    # from the domain and dropped
+    assert o3.silhouette_info(h) == (8 * 8, 0)
     o3.scene_destroy(h)
 
 
 def test_obstacle_silhouette_counts(o3):
     p = make_preset3("box-strip-vlin-obstacle", n=8)
     h = o3.scene(p.scene)
-    # obstacle_n = 4: its 12 edges x 4 segments are creases, plus the box's
-    assert o3.silhouette_info(h) == (8 * 8, 4 * 8 + 12 * 4)
+    # obstacle_n = 4: its 12 edges x 4 segments are reflex creases (kept);
+    # the box's lateral creases are convex (dropped)
+    assert o3.silhouette_info(h) == (8 * 8, 12 * 4)
     # a point facing one obstacle face sees its rim edges: silhouette within
     # reach; a point far away in the corner of the box does too (box creases
     # never flip from inside, the obstacle's do)
@@ -87,7 +90,7 @@ def test_jittered_box_creases_and_scene_errors(o3):
     sc = jittered_box(3, n=6)
     h = o3.scene(sc)
     a, c = o3.silhouette_info(h)
-    assert c > 100  # jitter turns every shared lateral edge into a crease
+    assert c > 50  # jitter turns shared lateral edges into creases, about half of them reflex
     x = probes3(4, 500, 0.1, 0.9)
     ds = o3.closest_silhouette(h, x)
     assert np.isfinite(ds).all()
@@ -150,4 +153,39 @@ def test_guided_walk_records(o3):
     np.testing.assert_allclose(recs["pdf_mis"], pm, rtol=1e-12)
     assert (recs["target"] >= 0).all()
     o3.field_destroy(f)
+    o3.scene_destroy(h)
+
+
+def test_silhouette_index_equals_raw_facing_rule(o3):
+    """Dropping coplanar and domain-convex creases from the index leaves the
+    closest silhouette of every interior point unchanged: a numpy brute force
+    over ALL Neumann edges with the plain facing rule (open edges always,
+    shared edges when n0.(a-x) and n1.(a-x) differ in sign) agrees."""
+    sc = jittered_box(9, n=5)
+    h = o3.scene(sc)
+    x = probes3(10, 300, 0.08, 0.92)
+    got = o3.closest_silhouette(h, x)
+    edges = {}
+    for t, k in zip(sc.tris, sc.kind):
+        if k != abi.NEUMANN:
+            continue
+        n = np.cross(t[1] - t[0], t[2] - t[0])
+        n /= np.linalg.norm(n)
+        for i in range(3):
+            p, q = t[i], t[(i + 1) % 3]
+            key = tuple(sorted((tuple(p), tuple(q))))
+            edges.setdefault(key, []).append(n)
+    want = np.full(len(x), np.inf)
+    for (p, q), ns in edges.items():
+        p, q = np.array(p), np.array(q)
+        ab = q - p
+        s = np.clip(((x - p) @ ab) / (ab @ ab), 0.0, 1.0)
+        d = np.linalg.norm(x - (p + s[:, None] * ab), axis=1)
+        if len(ns) == 2:
+            f0, f1 = (p - x) @ ns[0], (p - x) @ ns[1]
+            sil = f0 * f1 <= 0.0
+        else:
+            sil = np.ones(len(x), bool)
+        want = np.where(sil, np.minimum(want, d), want)
+    np.testing.assert_allclose(got, want, rtol=1e-12)
     o3.scene_destroy(h)

@@ -29,7 +29,14 @@ def main():
     cmd = sys.argv[3] if len(sys.argv) > 3 else ""
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    h, units, vals = rows[0], rows[1], rows[2]
+    h, units = rows[0], rows[1]
+    # the last launch whose kernel name matches (reports may hold several
+    # kernels / launches; later launches are past the warm-up)
+    ki = h.index("Kernel Name") if "Kernel Name" in h else None
+    match = [r for r in rows[2:] if ki is None or r[ki].startswith(kernel)]
+    if not match:
+        sys.exit(f"no launch of {kernel} in {rep}")
+    vals = match[-1]
     res = {"kernel": kernel, "report": rep, "capture": cmd}
     for k, name in KEYS.items():
         if k in h:
