@@ -146,8 +146,18 @@ __global__ void __launch_bounds__(128) field3_eval_tc_kernel(Field3View f, int64
 //                     sampling (no BVH work, so no lockstep divergence).
 // The host re-launches the pair until a geometry pass queues nothing.
 enum : uint8_t { SLOT_EMPTY = 0, SLOT_NEED_DIR = 1, SLOT_NEED_MOVE = 2 };
+// occupancy of the latency-bound geometry kernel: 5 CTAs/SM (<= 102
+// registers, a few hundred bytes of spills) measured 144 vs 171 ms walk time
+// at 512^2 x 8 wpp against the unconstrained 132-register build; the
+// tensor-core direction kernel is best left at 2 CTAs/SM (3: 193 ms)
+#ifndef WG3_GEOM_MINB
+#define WG3_GEOM_MINB 5
+#endif
+#ifndef WG3_DIR_MINB
+#define WG3_DIR_MINB 1
+#endif
 
-__global__ void __launch_bounds__(128) wave_geom_kernel(Walk3Args a, Wave3 v, int parity) {
+__global__ void __launch_bounds__(128, WG3_GEOM_MINB) wave_geom_kernel(Walk3Args a, Wave3 v, int parity) {
   const bool collect = a.recs != nullptr;
   const unsigned long long total = static_cast<unsigned long long>(a.n_points) * a.n_rounds;
   unsigned int* qlen = v.qlen + parity;
@@ -190,7 +200,7 @@ __global__ void __launch_bounds__(128) wave_geom_kernel(Walk3Args a, Wave3 v, in
   if ((threadIdx.x & 31) == 0 && started) atomicAdd(&a.counters[2], started);
 }
 
-__global__ void __launch_bounds__(128) wave_dir_kernel(Walk3Args a, Wave3 v, int parity) {
+__global__ void __launch_bounds__(128, WG3_DIR_MINB) wave_dir_kernel(Walk3Args a, Wave3 v, int parity) {
   extern __shared__ __align__(128) unsigned char smem[];
   if (blockIdx.x == 0 && threadIdx.x == 0) v.qlen[parity ^ 1] = 0u;  // next geometry pass's queue
   const unsigned int n = v.qlen[parity];
