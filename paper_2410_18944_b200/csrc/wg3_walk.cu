@@ -988,7 +988,8 @@ int wostgpu_solver3_attach_comm(wg_solver3 s, const char id[128], int32_t nranks
       nccl().commDestroy(s->comm);
       s->comm = nullptr;
     }
-    if (nranks == 1) return;
+    // a single-rank communicator is created too: it runs the multi-GPU
+    // pipeline (allreduce on the solver stream before Adam) on one GPU
     ncclUniqueId uid;
     std::memcpy(&uid, id, sizeof(uid));
     NCK(nccl().commInitRank(&s->comm, nranks, uid, rank));
