@@ -208,6 +208,21 @@ __device__ __forceinline__ void cp_bvh(const Node3* nodes, const Tri3* tris, D3 
   }
 }
 
+// closest Dirichlet point seeded with a candidate triangle (leaf-order index
+// `seed`, -1 for none): the candidate's exact distance bounds the traversal
+// from the start; the result is the same minimum over (d^2, id)
+__device__ __forceinline__ CP3 closest_dirichlet_seeded(const Scene3View& s, D3 x, int seed) {
+  CP3 best{{0.0, 0.0, 0.0}, dinf(), -1, -1};
+  if (seed >= 0 && s.node[0]) {
+    const Tri3& t = s.tri[0][seed];
+    D3 q = closest_on_tri(x, ld3(t.a), ld3(t.b), ld3(t.c));
+    D3 dq = sub(x, q);
+    best = {q, dot(dq, dq), t.id, seed};
+  }
+  cp_bvh(s.node[0], s.tri[0], x, best);
+  return best;
+}
+
 // Accel::closest_point analogue: (point, distance, triangle id) or id -1, d = inf
 __device__ __forceinline__ CP3 closest_point(const Scene3View& s, D3 x, unsigned kinds) {
   CP3 best{{0.0, 0.0, 0.0}, dinf(), -1, -1};
@@ -224,11 +239,13 @@ __device__ __forceinline__ bool is_silhouette(const Edge3& e, D3 x, double tol) 
   return f0 * f1 <= 0.0;
 }
 
-// squared distance to the nearest silhouette edge (inf if none)
-__device__ __forceinline__ double closest_silhouette_d2(const Scene3View& s, D3 x) {
+// squared distance to the nearest silhouette edge (inf if none); with a
+// bound, only edges strictly closer than sqrt(bound2) are searched for and
+// bound2 comes back when there is none
+__device__ __forceinline__ double closest_silhouette_d2(const Scene3View& s, D3 x, double bound2 = dinf()) {
   const Node3* nodes = s.node[2];
   if (!nodes) return dinf();
-  double best = dinf();
+  double best = bound2;
   int stack[64];
   int sp = 0;
   stack[sp++] = 0;

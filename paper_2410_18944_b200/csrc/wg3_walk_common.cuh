@@ -76,6 +76,7 @@ struct Lane3 {
   D3 x, n;
   double T, acc, R;
   int tri, depth, round, rec_left, last_rec;
+  int cp_seed;  // leaf-order index of the previous step's closest Dirichlet triangle (-1: none)
   bool on_n, alive, rec_ok;
   Pcg rng;
   int64_t point, rec_base;
@@ -97,6 +98,7 @@ __device__ __forceinline__ void lane3_init(Lane3& w, const Walk3Args& a, int64_t
                     a.wpp_first + static_cast<uint64_t>(w.round));
   w.last_rec = -1;
   w.rec_ok = true;
+  w.cp_seed = -1;
 }
 
 __device__ __forceinline__ void finish3(Lane3& w, const Walk3Args& a, bool escaped, double terminal,
@@ -120,7 +122,8 @@ __device__ __forceinline__ void finish3(Lane3& w, const Walk3Args& a, bool escap
 __device__ __forceinline__ bool step_begin(Lane3& w, const Walk3Args& a, bool collect, int& rec) {
   const Scene3View& s = a.s;
   rec = -1;
-  CP3 cd = closest_point(s, w.x, WG_KIND_DIRICHLET);
+  CP3 cd = closest_dirichlet_seeded(s, w.x, w.cp_seed);
+  w.cp_seed = cd.local;
   const double dd = cd.tri >= 0 ? sqrt(cd.d2) : dinf();
   if (cd.tri >= 0 && dd <= a.sp.eps) {
     const double g = value_at(s.values[s.tri[0][cd.local].value], cd.p);
@@ -140,7 +143,12 @@ __device__ __forceinline__ bool step_begin(Lane3& w, const Walk3Args& a, bool co
     }
     w.T /= q;
   }
-  const double dsil = closest_silhouette(s, w.x);
+  // R = min(dD, max(d_sil, r_min)) needs d_sil only when it is below dD: the
+  // silhouette search starts bounded by dD^2 and reports inf when nothing
+  // is closer, which leaves R = dD exactly as the unbounded query would
+  const double bound2 = dd == dinf() ? dinf() : dd * dd;
+  const double ds2 = closest_silhouette_d2(s, w.x, bound2);
+  const double dsil = ds2 < bound2 ? sqrt(ds2) : dinf();
   if (dd == dinf() && dsil == dinf()) {  // SceneError, wost.cpp:184-186
     atomicOr(&a.counters[4], 1ull);
     finish3(w, a, true, 0.0, false);
