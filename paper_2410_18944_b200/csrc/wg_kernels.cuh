@@ -83,6 +83,10 @@ struct WalkArgs {
   double* rec_term;
   // tensor-core kernel: the field's packed split-fp16 weights (wg_wpack.cuh)
   const unsigned char* wblob;
+  // tensor-core lockstep kernel: CUDA-core MLP for tail iterations (<= 16
+  // live rows). Off when its shared memory would cost the launch its second
+  // CTA per SM (large staged scenes with many walks in flight)
+  int32_t small_mlp;
   // optional per-CTA phase timing [gridDim][8]: cycles in phase A (begin
   // step + barrier), B (MLP), C (sample + move), iterations, MMA windows,
   // gather, MLP prep (WOSTGPU_PHASE_PROF)

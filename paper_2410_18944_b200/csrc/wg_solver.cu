@@ -198,6 +198,14 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
              (guided ? ((int)sizeof(float) * s->field->view.mlp_count + 15) / 16 * 16 : 0);
   if (g8) smem = walk_g8_smem(a);
   if (tc) {
+    // CUDA-core tail MLP on; WOSTGPU_SMALL_MLP=0 drops it (and its 46 KB of
+    // shared memory). Measured on cfg 3 at 512^2, where that lets a second
+    // CTA onto each SM: 2.70 vs 2.73M walks/s, so the default keeps it.
+    static const int small_env = [] {
+      const char* e = std::getenv("WOSTGPU_SMALL_MLP");
+      return e ? std::atoi(e) : 1;
+    }();
+    a.small_mlp = small_env != 0;
     smem = walk_tc_smem(a);
     a.wblob = field_blob(s->field, s->stream);
   }

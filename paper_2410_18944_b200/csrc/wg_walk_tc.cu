@@ -256,7 +256,8 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
   unsigned char* tc = smem;  // TcLayout block first (128-B aligned)
   SceneView s = a.scene;
   if (a.scene_smem_bytes > 0) {
-    unsigned char* p = smem + al16(kWarp ? TcLayoutW::BYTES : TcLayout::BYTES + sizeof(SmallMlp));
+    unsigned char* p =
+        smem + al16(kWarp ? TcLayoutW::BYTES : TcLayout::BYTES + (a.small_mlp ? sizeof(SmallMlp) : 0));
     size_t off = 0;
     auto carve = [&](size_t bytes) {
       unsigned char* q = p + off;
@@ -296,7 +297,7 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
   } else {
     tc_fetch_weights(tc, a.wblob);
     tc_setup(tc);
-    small_stage(small, a.field);
+    if (a.small_mlp) small_stage(small, a.field);
   }
   umma::fence_before();
   __syncthreads();
@@ -327,7 +328,7 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
       if (threadIdx.x == 0) a.phase_prof[8 * blockIdx.x + 2] += static_cast<unsigned long long>(t_top - t_iter);
       t_iter = t_top;
     }
-    if (!kWarp && threadIdx.x == 0) small.slot_count = 0;  // consumed after the phase-A barrier
+    if (!kWarp && a.small_mlp && threadIdx.x == 0) small.slot_count = 0;  // consumed after the phase-A barrier
     // ---- phase A: every slot advances to a walk that needs a direction
     bool need = false;
     for (;;) {
@@ -385,7 +386,7 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
     SUB_ADD(3, tg);
     SUB_T(tb);
     float raw[TcLayout::NO];
-    if (!kWarp && active <= kSmallRows) {  // tail iteration: CUDA-core rows (SmallMlp)
+    if (!kWarp && a.small_mlp && active <= kSmallRows) {  // tail iteration: CUDA-core rows (SmallMlp)
       int slot = -1;
       if (need) {
         slot = atomicAdd(&small.slot_count, 1);
@@ -603,7 +604,7 @@ cudaError_t launch_mix32_sample(const float* raw, int64_t n, uint64_t seed, doub
 }
 
 int walk_tc_smem(const WalkArgs& a) {
-  size_t tile = walk_tc_warps() == 0 ? TcLayout::BYTES + sizeof(SmallMlp) : TcLayoutW::BYTES;
+  size_t tile = walk_tc_warps() == 0 ? TcLayout::BYTES + (a.small_mlp ? sizeof(SmallMlp) : 0) : TcLayoutW::BYTES;
   return static_cast<int>(al16(tile) + (a.scene_smem_bytes > 0 ? al16(a.scene_smem_bytes) : 0));
 }
 
