@@ -12,8 +12,8 @@
  *
  * Scenes are triangle meshes: tri = n x {a.xyz, b.xyz, c.xyz} (fp64), kind
  * WG_DIRICHLET / WG_NEUMANN, value_index into wg_value3_spec values
- * (Dirichlet g constant or linear; Neumann triangles must carry the
- * constant 0: 3D scenes have no flux and no source term).
+ * (Dirichlet g / Neumann flux h, constant or linear), an optional source f
+ * (constant or linear, 0 outside the scene bbox; NULL or WG_VALUE_ZERO: none).
  */
 #ifndef WOSTGPU3_H
 #define WOSTGPU3_H
@@ -34,7 +34,8 @@ typedef struct wg_solver3_s* wg_solver3;
  * degenerate triangles, undefined values. */
 int wostgpu_scene3_create(const double* tri, const int32_t* kind, const int32_t* value_index,
                           int32_t n_tri, const wg_value3_spec* values, int32_t n_values,
-                          const double bbox[6], double epsilon_shell, wg_scene3* out);
+                          const wg_value3_spec* source, const double bbox[6], double epsilon_shell,
+                          wg_scene3* out);
 int wostgpu_scene3_destroy(wg_scene3 scene);
 /* t_epsilon (1e-6 x root-box diagonal, geom2d.hpp:61 analogue), BVH node
  * counts (Dirichlet, Neumann, edges) and silhouette-edge counts (always /

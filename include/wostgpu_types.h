@@ -147,9 +147,9 @@ typedef struct wg_mixture {
 } wg_mixture;
 
 /* ---- 3D (no reference counterpart; SURVEY.md §8 a', configs 4-5) ------ */
-/* Dirichlet value of a 3D triangle: Constant c0 or Linear c0 + cx x + cy y +
- * cz z (the 3D analogue of ValueSpec, scene.hpp:31-67); Neumann triangles
- * carry the constant 0 (no flux in 3D scenes) */
+/* value of a 3D triangle (Dirichlet g or Neumann flux h) or of the 3D
+ * source f: Constant c0 or Linear c0 + cx x + cy y + cz z (the 3D analogue of
+ * ValueSpec, scene.hpp:31-67); type WG_VALUE_ZERO marks "no source" */
 typedef struct wg_value3_spec {
   int32_t type; /* WG_VALUE_CONSTANT or WG_VALUE_LINEAR */
   int32_t pad_;

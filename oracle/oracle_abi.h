@@ -85,7 +85,7 @@ WG_ORACLE_DECLS(orc)
 /* 3D contract (oracle/wost3d.inc): restatement only, no reference code */
 void* orc3_scene_create(const double* tri, const int32_t* kind, const int32_t* value_index,
                         int32_t n_tri, const wg_value3_spec* values, int32_t n_values,
-                        const double* bbox, double epsilon_shell);
+                        const wg_value3_spec* source, const double* bbox, double epsilon_shell);
 void orc3_scene_destroy(void* scene);
 double orc3_t_epsilon(void* scene);
 void orc3_silhouette_info(void* scene, int64_t* n_always, int64_t* n_crease);

@@ -80,8 +80,8 @@ _SIGS = {
     "wostgpu_solver_attach_comm": (C.c_int, [VP, C.c_char_p, C.c_int32, C.c_int32]),
     "wostgpu_solver_timing": (C.c_int, [VP, D, D]),
     # ---- 3D path (include/wostgpu3.h)
-    "wostgpu_scene3_create": (C.c_int, [D, I32, I32, C.c_int32, C.POINTER(abi.Value3Spec), C.c_int32, D,
-                                        C.c_double, C.POINTER(VP)]),
+    "wostgpu_scene3_create": (C.c_int, [D, I32, I32, C.c_int32, C.POINTER(abi.Value3Spec), C.c_int32,
+                                        C.POINTER(abi.Value3Spec), D, C.c_double, C.POINTER(VP)]),
     "wostgpu_scene3_destroy": (C.c_int, [VP]),
     "wostgpu_scene3_info": (C.c_int, [VP, D, I64, I64, I64]),
     "wostgpu_closest_point3": (C.c_int, [VP, C.c_int64, D, C.c_uint32, D, D, I32]),

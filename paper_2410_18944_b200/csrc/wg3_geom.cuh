@@ -64,6 +64,9 @@ struct Scene3View {
   double bbox[6];
   double t_eps, diag, eps;
   double sil_tol;  // facings within this count as 0 (oracle/wost3d.inc)
+  wg_value3_spec source;  // type WG_VALUE_ZERO: no source term
+  int32_t has_flux;       // some Neumann triangle has h != 0
+  int32_t pad_;
 };
 
 __device__ __forceinline__ D3 ld3(const double* p) { return {p[0], p[1], p[2]}; }

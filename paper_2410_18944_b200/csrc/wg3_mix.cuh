@@ -181,6 +181,31 @@ __device__ __forceinline__ Mis3 mis_sample(wg::Pcg& rng, const Mix3<K>& m, bool 
   return o;
 }
 
+// ---------------------------------------------------------------- Green's
+// greens_ball / sample_greens_radius for d = 3 (proj/src/wost.cpp:27-65)
+__device__ __forceinline__ double greens_ball3(double r, double R) {
+  if (r <= 0.0) return dinf();
+  return (1.0 / r - 1.0 / R) / kFourPi;
+}
+__device__ __forceinline__ double greens_radius3(double u, double R) {
+  if (u <= 0.0) return 0.0;
+  if (u >= 1.0) return R;
+  double lo = 0.0, hi = 1.0, s = sqrt(u);
+  for (int it = 0; it < 100; ++it) {
+    double f = s * s * (3.0 - 2.0 * s) - u;
+    double df = 6.0 * s * (1.0 - s);
+    if (f > 0.0) hi = s;
+    else lo = s;
+    if (fabs(f) < 1e-10) break;
+    double step = df > 0.0 ? f / df : 0.0;
+    double nx = s - step;
+    if (!(nx > lo && nx < hi)) nx = 0.5 * (lo + hi);
+    if (nx == s) break;
+    s = nx;
+  }
+  return s * R;
+}
+
 // ---------------------------------------------------------------- gradient
 __device__ __forceinline__ double dlogv_dkappa3(double t, double kappa) {  // sphdist.cpp:315-321
   double e = expm1(-2.0 * kappa);

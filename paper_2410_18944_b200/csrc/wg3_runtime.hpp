@@ -30,7 +30,7 @@ struct wg_solver3_s {
   wgrt::DBuf points, stats, est, esc, steps, counters;
   int32_t last_rounds = 0;
   // records of the last collecting round (wg3::DevRecord3 in a wg::DevRecord arena)
-  wgrt::DBuf recs, rec_counter, rec_tail, rec_term;
+  wgrt::DBuf recs, rec_counter, rec_tail, rec_term, rec_dacc;
   int64_t rec_cap = 0;
   bool have_records = false;
   // wavefront walk pool (WG_MLP_TENSOR guided walks, wg3_walk_tc.cu)

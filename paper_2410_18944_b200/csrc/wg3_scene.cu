@@ -269,7 +269,7 @@ extern "C" {
 
 int wostgpu_scene3_create(const double* tri, const int32_t* kind, const int32_t* value_index,
                           int32_t n_tri, const wg_value3_spec* values, int32_t n_values,
-                          const double bbox[6], double eps, wg_scene3* out) {
+                          const wg_value3_spec* source, const double bbox[6], double eps, wg_scene3* out) {
   return guarded([&] {
     check_device();
     need(n_tri > 0, WG_ERR_SCENE, "Accel: empty scene");
@@ -281,6 +281,7 @@ int wostgpu_scene3_create(const double* tri, const int32_t* kind, const int32_t*
       need(values[i].type == WG_VALUE_CONSTANT || values[i].type == WG_VALUE_LINEAR, WG_ERR_INVALID,
            "3D scene: values must be constant or linear");
     std::vector<Tri3> tris(static_cast<size_t>(n_tri));
+    int32_t has_flux = 0;
     HBox root;
     std::vector<HBox> boxes[2];
     std::vector<int> ids[2];
@@ -308,9 +309,8 @@ int wostgpu_scene3_create(const double* tri, const int32_t* kind, const int32_t*
           for (int a = 0; a < 3; ++a)
             need(p[a] >= bbox[a] && p[a] <= bbox[3 + a], WG_ERR_SCENE, "3D scene: vertex outside scene bbox");
       }
-      if (t.kind == WG_NEUMANN)
-        need(values[t.value].type == WG_VALUE_CONSTANT && values[t.value].c0 == 0.0, WG_ERR_INVALID,
-             "3D scene: Neumann flux must be zero");
+      if (t.kind == WG_NEUMANN && !(values[t.value].type == WG_VALUE_CONSTANT && values[t.value].c0 == 0.0))
+        has_flux = 1;  // Scene::has_neumann_flux analogue (scene.cpp:83-91)
       HBox b;
       b.grow(t.a);
       b.grow(t.b);
@@ -364,6 +364,14 @@ int wostgpu_scene3_create(const double* tri, const int32_t* kind, const int32_t*
     for (int i = 0; i < 6; ++i) v.bbox[i] = bbox[i];
     v.t_eps = s->t_eps;
     v.sil_tol = sil_tol;
+    v.has_flux = has_flux;
+    v.source = wg_value3_spec{};
+    v.source.type = WG_VALUE_ZERO;
+    if (source && source->type != WG_VALUE_ZERO) {
+      need(source->type == WG_VALUE_CONSTANT || source->type == WG_VALUE_LINEAR, WG_ERR_INVALID,
+           "3D scene: the source must be constant or linear");
+      v.source = *source;
+    }
     v.diag = s->diag;
     v.eps = s->eps;
     *out = s.release();

@@ -404,6 +404,8 @@ wg::SolverParams params3(const wg_solver3_s* s) {
   p.eps = s->cfg.epsilon_shell > 0.0 ? s->cfg.epsilon_shell : s->scene->eps;
   p.rmin = s->cfg.r_min > 0.0 ? s->cfg.r_min : p.eps;
   p.fixed_c = s->cfg.fixed_c;
+  p.clamp_grazing = s->cfg.clamp_grazing;
+  p.grazing_floor = s->cfg.grazing_floor;
   p.rr_depth = s->cfg.rr_depth;
   p.max_steps = s->cfg.max_steps;
   p.mode = s->cfg.mode;
@@ -473,6 +475,7 @@ void enqueue3_rounds(wg_solver3_s* s, uint64_t seed, uint64_t wpp_first, int32_t
     int64_t cap = std::max<int64_t>(s->n_points * 128, int64_t(1) << 16);
     if (s->rec_cap < cap) {
       s->recs.alloc(sizeof(DevRecord3) * cap);
+      s->rec_dacc.alloc(sizeof(float) * cap);
       s->rec_cap = cap;
     }
     s->rec_counter.alloc(sizeof(unsigned long long));
@@ -500,6 +503,7 @@ void enqueue3_rounds(wg_solver3_s* s, uint64_t seed, uint64_t wpp_first, int32_t
   a.key_seed = key_seed;
   a.rec_tail = collect ? s->rec_tail.as<int32_t>() : nullptr;
   a.rec_term = collect ? s->rec_term.as<double>() : nullptr;
+  a.rec_dacc = collect ? s->rec_dacc.as<float>() : nullptr;
   const bool tc = guided && s->mlp == WG_MLP_TENSOR;
   const int smem = guided ? static_cast<int>(sizeof(float) * s->field->view3.mlp_count) : 0;
   if (guided && !tc)
@@ -555,14 +559,44 @@ void enqueue3_rounds(wg_solver3_s* s, uint64_t seed, uint64_t wpp_first, int32_t
   }
 }
 
+// backfill_targets_append (guide_train.cpp:58-79) for 3D scenes with source /
+// flux terms: per walk, backward over its record chain with the fp64 suffix
+// sum S (target_k = |S / Q_k|, then S += dacc_k), dacc from the side array
+__global__ void backfill3_chains_kernel(DevRecord3* recs, const float* dacc, int64_t n_walks,
+                                        const int32_t* tail, const double* term, const int32_t* esc) {
+  for (int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < n_walks;
+       w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (esc[w]) continue;
+    double s = term[w];
+    for (int32_t i = tail[w]; i >= 0;) {
+      DevRecord3& r = recs[i];
+      const double q = r.thr_q;
+      r.target = q == 0.0 ? 0.0f : static_cast<float>(fabs(s / q));
+      s += static_cast<double>(dacc[i]);
+      i = r.prev;
+    }
+  }
+}
+
 void enqueue3_finalize(wg_solver3_s* s, double pdf_floor, bool from_walks) {
   s->ctl.alloc(sizeof(wg::TrainCtl));
   CK(cudaMemsetAsync(s->ctl.p, 0, sizeof(wg::TrainCtl), s->st));
+  // scenes with local terms: chain targets here; the shared finalize then
+  // keeps them (chain = true, no walks for its 2D chain pass)
+  const Scene3View& v = s->scene->view;
+  const bool chain = from_walks && (v.source.type != WG_VALUE_ZERO || v.has_flux);
+  if (chain) {
+    const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((s->n_points + 127) / 128, 148 * 8)));
+    backfill3_chains_kernel<<<blocks, 128, 0, s->st>>>(s->recs.as<DevRecord3>(), s->rec_dacc.as<float>(),
+                                                       s->n_points, s->rec_tail.as<int32_t>(),
+                                                       s->rec_term.as<double>(), s->esc.as<int32_t>());
+    CKL(cudaGetLastError());
+  }
   CKL(wg::launch_finalize_records(reinterpret_cast<DevRecord*>(s->recs.p),
                                   s->rec_counter.as<unsigned long long>(), s->rec_cap,
-                                  from_walks ? s->n_points : 0, s->rec_tail.as<int32_t>(),
+                                  from_walks && !chain ? s->n_points : 0, s->rec_tail.as<int32_t>(),
                                   s->rec_term.as<double>(), s->esc.as<int32_t>(), pdf_floor,
-                                  s->ctl.as<wg::TrainCtl>(), false, s->st));
+                                  s->ctl.as<wg::TrainCtl>(), chain, s->st));
 }
 
 void ensure3_train(wg_solver3_s* s, const wg_train_config& tc) {
@@ -900,6 +934,7 @@ int wostgpu_solver3_field_grad(wg_solver3 s, const wg_guide_record3* recs, int64
     ensure3_train(s, tc);
     if (s->rec_cap < n) {
       s->recs.alloc(sizeof(DevRecord3) * n);
+      s->rec_dacc.alloc(sizeof(float) * n);
       s->rec_cap = n;
     }
     DBuf h;

@@ -70,11 +70,14 @@ struct Walk3Args {
   unsigned long long* counters;  // [0] steps [1] escaped [2] walks [3] rec overflow [4] scene error
   int32_t* rec_tail;
   double* rec_term;
+  float* rec_dacc;  // per record slot: accumulator increments since the walk's
+                    // previous record (DevRecord::dacc, held aside in 3D)
 };
 
 struct Lane3 {
   D3 x, n;
   double T, acc, R;
+  double dacc;  // source / flux increments since the walk's last record
   int tri, depth, round, rec_left, last_rec;
   int cp_seed;  // leaf-order index of the previous step's closest Dirichlet triangle (-1: none)
   bool on_n, alive, rec_ok;
@@ -91,6 +94,7 @@ __device__ __forceinline__ void lane3_init(Lane3& w, const Walk3Args& a, int64_t
   w.tri = -1;
   w.T = 1.0;
   w.acc = 0.0;
+  w.dacc = 0.0;
   w.R = 0.0;
   w.depth = 0;
   w.alive = true;
@@ -111,7 +115,7 @@ __device__ __forceinline__ void finish3(Lane3& w, const Walk3Args& a, bool escap
   if (escaped) atomicAdd(&a.counters[1], 1ull);
   if (collect) {
     a.rec_tail[slot] = w.last_rec;
-    a.rec_term[slot] = escaped ? 0.0 : w.T * terminal;
+    a.rec_term[slot] = escaped ? 0.0 : w.T * terminal + w.dacc;
   }
   w.alive = false;
 }
@@ -154,7 +158,36 @@ __device__ __forceinline__ bool step_begin(Lane3& w, const Walk3Args& a, bool co
     finish3(w, a, true, 0.0, false);
     return false;
   }
-  w.R = fmin(dd, fmax(dsil, a.sp.rmin));
+  const double R = fmin(dd, fmax(dsil, a.sp.rmin));
+  w.R = R;
+  if (s.source.type != WG_VALUE_ZERO || s.has_flux) {
+    double contrib = 0.0;
+    if (s.source.type != WG_VALUE_ZERO) {  // sample_source_point (wost.cpp:67-87), d = 3
+      const D3 dir = uniform_sample(w.rng, w.on_n, w.n);
+      const double r = greens_radius3(w.rng.uni(), R);
+      const D3 y = add(w.x, scl(dir, r));
+      const Hit3 h = ray_first_hit(s, w.x, dir, r, WG_KIND_ALL, -1);
+      const double wt = h.tri >= 0 ? 0.0 : R * R / 6.0;
+      if (wt != 0.0) contrib -= wt * (bbox_contains(s, y, 0.0) ? value_at(s.source, y) : 0.0);
+    }
+    if (s.has_flux) {  // sample_neumann_contrib (wost.cpp:89-109), d = 3
+      const D3 dir = uniform_sample(w.rng, w.on_n, w.n);
+      const Hit3 h = ray_first_hit(s, w.x, dir, R, WG_KIND_NEUMANN, w.tri);
+      double add_ = 0.0;
+      if (h.tri >= 0) {
+        const D3 hp = add(w.x, scl(dir, h.t));
+        const double hv = value_at(s.values[s.tri[1][h.local].value], hp);
+        if (hv != 0.0) {
+          double cz = fabs(dot(dir, hit_normal(s, h, dir)));
+          if (a.sp.clamp_grazing) cz = fmax(cz, a.sp.grazing_floor);
+          if (cz != 0.0) add_ = greens_ball3(h.t, R) * hv * h.t * h.t * kFourPi / cz;
+        }
+      }
+      contrib += add_;
+    }
+    w.acc += w.T * contrib;
+    w.dacc += w.T * contrib;
+  }
   if (collect && w.rec_ok) {  // trace push (wost.cpp:206-214), chunks of 8 slots
     if (w.rec_left == 0) {
       unsigned long long b = atomicAdd(a.rec_counter, 8ull);
@@ -231,6 +264,8 @@ __device__ __forceinline__ void step_move(Lane3& w, const Walk3Args& a, bool col
                                            static_cast<uint64_t>(w.depth)));
     r.prev = w.last_rec;
     a.recs[rec] = r;
+    a.rec_dacc[rec] = static_cast<float>(w.dacc);
+    w.dacc = 0.0;
     w.last_rec = rec;
   }
   if (d.mult == 0.0) {  // sampled into the invalid half space

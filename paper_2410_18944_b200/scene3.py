@@ -39,6 +39,7 @@ class Scene3:
     values: list = field(default_factory=list)  # (type, c0, cx, cy, cz)
     bbox: tuple = (0.0, 0.0, 0.0, 1.0, 1.0, 1.0)
     eps: float = 1e-3
+    source: Optional[tuple] = None  # (type, c0, cx, cy, cz) of f; None: no source
 
     @property
     def n_tris(self):
@@ -51,16 +52,20 @@ class Scene3:
         return arr
 
     def c_args(self):
-        """(tri, kind, value_index, n, values, n_values, bbox, eps) as ctypes
-        arguments (arrays kept alive on the returned tuple's owner)."""
+        """(tri, kind, value_index, n, values, n_values, source, bbox, eps) as
+        ctypes arguments (arrays kept alive on the scene object)."""
         tri = np.ascontiguousarray(self.tris.reshape(-1), dtype=np.float64)
         kind = np.ascontiguousarray(self.kind, dtype=np.int32)
         vi = np.ascontiguousarray(self.value_index, dtype=np.int32)
         bbox = np.ascontiguousarray(self.bbox, dtype=np.float64)
         vals = self.c_values()
-        self._keep = (tri, kind, vi, bbox, vals)
+        src = None
+        if self.source is not None:
+            t, c0, cx, cy, cz = self.source
+            src = abi.Value3Spec(t, 0, c0, cx, cy, cz)
+        self._keep = (tri, kind, vi, bbox, vals, src)
         return (abi.ptr(tri), abi.ptr(kind, C.c_int32), abi.ptr(vi, C.c_int32), self.n_tris, vals,
-                len(self.values), abi.ptr(bbox), self.eps)
+                len(self.values), C.byref(src) if src is not None else None, abi.ptr(bbox), self.eps)
 
 
 def box_mesh(n, lo=(0.0, 0.0, 0.0), hi=(1.0, 1.0, 1.0), outward=True):
@@ -112,6 +117,35 @@ def _box_strip_scene(n, obstacle=False, obstacle_n=4):
                   1e-3 * math.sqrt(3.0))
 
 
+def _box_poisson_scene(n):
+    """u = x^2: Delta u = 2 = f (the reference's sign, const-source-disk), g = 0
+    at x = 0 and 1 at x = 1, insulated lateral faces (du/dn = 0 there)."""
+    sc = _box_strip_scene(n)
+    sc.values = [(VALUE_CONSTANT, 0.0, 0.0, 0.0, 0.0), (VALUE_CONSTANT, 1.0, 0.0, 0.0, 0.0)]
+    sc.source = (VALUE_CONSTANT, 2.0, 0.0, 0.0, 0.0)
+    return sc
+
+
+def _box_flux_scene(n):
+    """u = y: Dirichlet g = y on the x faces, Neumann flux h = du/dn (outward
+    normal) = -1 on y = 0, +1 on y = 1, 0 on the z faces."""
+    values = [(VALUE_CONSTANT, 0.0, 0.0, 0.0, 0.0), (VALUE_LINEAR, 0.0, 0.0, 1.0, 0.0),
+              (VALUE_CONSTANT, -1.0, 0.0, 0.0, 0.0), (VALUE_CONSTANT, 1.0, 0.0, 0.0, 0.0)]
+    tris, kind, vidx = [], [], []
+    for axis, side, tr in box_mesh(n):
+        if axis == 0:
+            k, v = abi.DIRICHLET, 1
+        elif axis == 1:
+            k, v = abi.NEUMANN, (2 if side == 0.0 else 3)
+        else:
+            k, v = abi.NEUMANN, 0
+        tris += tr
+        kind += [k] * len(tr)
+        vidx += [v] * len(tr)
+    return Scene3(np.asarray(tris, dtype=np.float64), np.asarray(kind, dtype=np.int32),
+                  np.asarray(vidx, dtype=np.int32), values, (0.0, 0.0, 0.0, 1.0, 1.0, 1.0), 1e-3 * math.sqrt(3.0))
+
+
 @dataclass
 class Preset3:
     name: str
@@ -129,10 +163,14 @@ def make_preset3(name: str, n: int = 91) -> Preset3:
     if name == "box-strip-vlin-obstacle":
         sc = _box_strip_scene(n, obstacle=True)
         return Preset3(name, sc, None, (0.0, 0.0, 1.0, 1.0), 0.5)
+    if name == "box-poisson":
+        return Preset3(name, _box_poisson_scene(n), lambda x, y, z: x * x, (0.0, 0.0, 1.0, 1.0), 0.5)
+    if name == "box-flux":
+        return Preset3(name, _box_flux_scene(n), lambda x, y, z: y, (0.0, 0.0, 1.0, 1.0), 0.5)
     raise ValueError(f"unknown 3D preset '{name}'")
 
 
-PRESET3_NAMES = ["box-strip-vlin", "box-strip-vlin-obstacle"]
+PRESET3_NAMES = ["box-strip-vlin", "box-strip-vlin-obstacle", "box-poisson", "box-flux"]
 
 
 def slice_points(width, height, bbox=(0.0, 0.0, 1.0, 1.0), z=0.5):

@@ -231,7 +231,8 @@ def _sig3(lib):
         f = getattr(lib, f"orc3_{name}")
         f.restype = res
         f.argtypes = list(args)
-    s("scene_create", VP, D, I32, I32, C.c_int32, C.POINTER(abi.Value3Spec), C.c_int32, D, C.c_double)
+    s("scene_create", VP, D, I32, I32, C.c_int32, C.POINTER(abi.Value3Spec), C.c_int32,
+      C.POINTER(abi.Value3Spec), D, C.c_double)
     s("scene_destroy", None, VP)
     s("t_epsilon", C.c_double, VP)
     s("silhouette_info", None, VP, I64, I64)

@@ -251,3 +251,53 @@ def test_tensor_walks_match_exact_statistically(gpu, mode):
     z = (a["mean"][ok] - b["mean"][ok]) / se[ok]
     assert np.abs(z).max() < 4.5
     assert abs(z.mean()) < 4.0 / np.sqrt(ok.sum())
+
+
+@pytest.mark.parametrize("name", ["box-poisson", "box-flux"])
+def test_source_and_flux_walks_match_oracle(gpu, o3, name):
+    """d = 3 source (Green's mass, radius CDF, occlusion ray) and Neumann-flux
+    terms: per-walk estimates equal the oracle's (same draws, same order)."""
+    sc = make_preset3(name, n=10).scene
+    x = probes3(51, 2000, 0.05, 0.95)
+    for mode in ("uniform",):
+        est_o, esc_o, st_o, est_g, esc_g, st_g = _walks(o3, sc, abi.solver_config(mode), x, 3)
+        close = np.abs(est_o - est_g) <= 1e-9 * np.maximum(1.0, np.abs(est_o))
+        assert close.mean() >= 0.999, close.mean()
+
+
+def test_source_term_record_targets_match_oracle(gpu, o3):
+    """Records of a scene with a source term carry the walk's backward suffix
+    sums (target_k = |S_{k+1} / Q_k|, S += local_k), like the oracle's
+    backfill with local terms."""
+    sc = make_preset3("box-poisson", n=8).scene
+    cfg_f = abi.field_config3()
+    fo, fg = o3.field(cfg_f, BOX, 31), GuidingField3(cfg_f, BOX, 31)
+    cfg = abi.solver_config("learnable_mis")
+    x = slice_points(20, 20)
+    ho = o3.scene(sc)
+    rec_o = o3.walk_records(ho, fo, cfg, x, 7, 0)
+    sol = Solver3(Accel3(sc), fg, cfg, MLP_EXACT)
+    sol.set_points(x)
+    sol.solve_rounds(7, 0, 1, collect=True)
+    rec_g = sol.records()
+    assert abs(len(rec_g) - len(rec_o)) <= max(2, len(rec_o) // 500)
+    np.testing.assert_allclose(np.sort(rec_g["target"]), np.sort(rec_o["target"]), rtol=1e-4, atol=1e-6)
+    o3.scene_destroy(ho)
+    o3.field_destroy(fo)
+
+
+def test_poisson_tensor_path_matches_analytic(gpu):
+    """box-poisson (u = x^2, f = 2) through the product path (guided,
+    tensor-core wavefront, online training): per-point means within SE of x^2."""
+    p = make_preset3("box-poisson", n=32)
+    x = slice_points(24, 24)
+    f = GuidingField3(abi.field_config3(), BOX, 9)
+    s = Solver3(Accel3(p.scene), f, abi.solver_config("learnable_mis"))
+    s.set_points(x)
+    s.run(9, 96, 32, abi.train_config(seed=9))
+    st = s.stats()
+    ref = x[:, 0] ** 2
+    ok = (st["m2"] > 0) & (x[:, 0] > 0.1)
+    z = (st["mean"][ok] - ref[ok]) / np.sqrt(st["m2"][ok] / (st["count"][ok] - 1) / st["count"][ok])
+    assert np.abs(z).max() < 5.0
+    assert abs(z.mean()) < 0.3
