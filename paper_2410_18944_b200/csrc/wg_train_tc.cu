@@ -114,6 +114,9 @@ __device__ __forceinline__ void gemm(uint32_t tmem_d, uint32_t a_hi, uint32_t a_
                                      uint32_t a_sbo, uint32_t a_step, uint32_t b_hi, uint32_t b_lo,
                                      uint32_t b_lbo, uint32_t b_sbo, uint32_t b_step, int ksteps,
                                      uint32_t id, bool accumulate) {
+  // issued by one thread: kept rolled (unrolled, the nine call sites were
+  // ~1.6k instructions of a kernel whose time is mostly instruction fetch)
+#pragma unroll 1
   for (int k = 0; k < ksteps; ++k) {
     uint64_t ah = desc(a_hi + k * a_step, a_lbo, a_sbo), al = desc(a_lo + k * a_step, a_lbo, a_sbo);
     uint64_t bh = desc(b_hi + k * b_step, b_lbo, b_sbo), bl = desc(b_lo + k * b_step, b_lbo, b_sbo);
