@@ -18,7 +18,7 @@ all: $(PKG)/libwostgpu.so oracle
 
 # translation units whose results are only statistically compared with the
 # reference (tensor-core walk path, training) may contract FMAs
-FAST_TUS := wg_walk_tc wg_walk_coop wg_train wg_train_tc wg3_walk_tc
+FAST_TUS := wg_walk_tc wg_walk_coop wg_train wg_train_tc wg3_walk_tc wg_wave2
 
 build/%.o: $(PKG)/csrc/%.cu $(HDR)
 	@mkdir -p build

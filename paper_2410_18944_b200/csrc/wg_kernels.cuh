@@ -130,6 +130,12 @@ int walk_coop_smem(const WalkArgs& a);
 int walk_coop_block();
 int walk_coop_blocks_per_sm(int smem);
 cudaError_t launch_walks_coop(const WalkArgs& a, int blocks, cudaStream_t st);
+// wavefront pair for guided 2D walks on the tensor cores (wg_wave2.cu)
+void wave2_sizes(size_t* lane_bytes, size_t* dir_bytes);
+cudaError_t launch_walks2_wave(const WalkArgs& a, void* lanes, void* dirs, int32_t* rec, uint8_t* state,
+                               int32_t* queue, unsigned int* qlen, unsigned long long* next_walk,
+                               int64_t slots, int sms, unsigned int* h_qlen, int64_t* launches,
+                               cudaStream_t st);
 cudaError_t launch_mix32_pdf(const float* raw, int64_t n, const double* nu, double* out, cudaStream_t st);
 cudaError_t launch_mix32_sample(const float* raw, int64_t n, uint64_t seed, double* out, cudaStream_t st);
 cudaError_t launch_field_eval_tc(const FieldView& f, int64_t n, const double* xy, double* out,

@@ -69,6 +69,10 @@ struct wg_solver_s {
   // NCCL
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
+  // wavefront walk pool (wg_wave2.cu)
+  DBuf w_lanes, w_dirs, w_rec, w_state, w_queue, w_qlen, w_next;
+  int64_t w_slots = 0;
+  unsigned int* h_qlen = nullptr;  // pinned
 };
 
 namespace {
@@ -229,7 +233,37 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
       a.phase_prof = s->phase_prof.as<unsigned long long>();
     }
     CK(cudaEventRecord(pool_event(s->ev_walk, s->n_walk_ev), s->stream));
-    if (tc) CKL(launch_walks_tc(a, std::max(1, blocks), s->stream));
+    // tensor-core walks as a wavefront pair when geometry dominates and
+    // enough walks are in flight to fill the GPU (cfg 3, 256 segments at
+    // 512^2: 3.28 vs 2.72M walks/s); lockstep tiles otherwise: small scenes
+    // (<= 16 segments, shared-memory segment lists; cfg 2 multi-round: 99 vs
+    // 41M walks/s) and 16,384-walk training rounds. WOSTGPU_WALK2 = wave /
+    // lockstep forces one.
+    const char* w2 = std::getenv("WOSTGPU_WALK2");
+    const int force2 = !w2 ? 0 : std::string(w2) == "wave" ? 1 : std::string(w2) == "lockstep" ? 2 : 0;
+    const bool wave = tc && (force2 == 1 || (force2 == 0 && s->scene->view.n_segs > 16 &&
+                                              s->n_points * n >= 65536));
+    if (wave) {
+      const int64_t slots = std::min<int64_t>(s->n_points * n, (int64_t)s->sms * 16 * 128);
+      if (s->w_slots < slots) {
+        size_t lb = 0, db = 0;
+        wave2_sizes(&lb, &db);
+        s->w_lanes.alloc(lb * slots);
+        s->w_dirs.alloc(db * slots);
+        s->w_rec.alloc(sizeof(int32_t) * slots);
+        s->w_state.alloc(slots);
+        s->w_queue.alloc(sizeof(int32_t) * slots);
+        s->w_slots = slots;
+      }
+      s->w_qlen.alloc(2 * sizeof(unsigned int));
+      s->w_next.alloc(sizeof(unsigned long long));
+      if (!s->h_qlen) CK(cudaMallocHost(&s->h_qlen, 4 * sizeof(unsigned int)));
+      int64_t launched = 0;
+      CK(launch_walks2_wave(a, s->w_lanes.p, s->w_dirs.p, s->w_rec.as<int32_t>(), s->w_state.as<uint8_t>(),
+                            s->w_queue.as<int32_t>(), s->w_qlen.as<unsigned int>(),
+                            s->w_next.as<unsigned long long>(), slots, s->sms, s->h_qlen, &launched, s->stream));
+      g_launches += launched;
+    } else if (tc) CKL(launch_walks_tc(a, std::max(1, blocks), s->stream));
     if (phase_prof && tc) {  // diagnostics: cycles per CTA iteration of the slowest CTA
       std::vector<unsigned long long> h(8 * blocks);
       CK(cudaMemcpyAsync(h.data(), s->phase_prof.p, sizeof(unsigned long long) * 8 * blocks,
@@ -249,7 +283,7 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
                    worst, it, q[0] / it, q[1] / it, q[5] / it, prep / it, q[4] / it, q[2] / it, small_it,
                    small_it > 0 ? q[7] / small_it : 0.0);
     }
-    if (tc) {
+    if (tc || wave) {
     } else if (coop) CKL(launch_walks_coop(a, std::max(1, blocks), s->stream));
     else if (g8) CKL(launch_walks_g8(a, std::max(1, blocks), s->stream));
     else CKL(launch_walks(a, dflt, guided && !dflt, std::max(1, blocks), s->stream));
@@ -454,6 +488,7 @@ int wostgpu_solver_destroy(wg_solver s) {
     cudaEventDestroy(s->ev_run0);
     cudaEventDestroy(s->ev_run1);
     cudaStreamDestroy(s->stream);
+    if (s->h_qlen) cudaFreeHost(s->h_qlen);
     delete s;
   });
 }

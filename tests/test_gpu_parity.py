@@ -398,3 +398,30 @@ def test_cpp_facade_drop_in_run(gpu, tmp_path):
     out = subprocess.run([exe, "32", "64"], capture_output=True, text=True, check=True).stdout.split()
     rel_u, rel_g, steps = float(out[0]), float(out[1]), int(out[2])
     assert steps > 0 and rel_g < rel_u, out
+
+
+def test_wavefront_2d_matches_lockstep_statistically(gpu, monkeypatch):
+    """The 2D wavefront pair (wg_wave2.cu, chosen for large scenes with many
+    walks in flight) against the lockstep tensor-core kernel on the
+    source-term disk (cfg 3's scene): per-point means over 64 guided walks
+    agree within 4.5 combined SE, mean z centred."""
+    p = make_preset("const-source-disk")
+    pts = cell_centers(40, 40, p.eval_bbox)
+    cfg = abi.field_config()
+    f = api.GuidingField(cfg, p.scene.bbox, 4)
+    prm = f.params()
+    prm = prm + np.float32(0.2) * np.random.default_rng(3).standard_normal(len(prm)).astype(np.float32)
+    f.set_params(prm)
+    out = []
+    for mode in ("lockstep", "wave"):
+        monkeypatch.setenv("WOSTGPU_WALK2", mode)
+        s = api.Solver(api.Accel(p.scene), f, abi.solver_config("learnable_mis"), api.MLP_TENSOR)
+        s.set_points(pts)
+        s.run(5, 64, 0, None)
+        out.append(s.stats())
+    a, b = out
+    se = np.sqrt(a["m2"] / (a["count"] - 1) / a["count"] + b["m2"] / (b["count"] - 1) / b["count"])
+    ok = se > 0
+    z = (a["mean"][ok] - b["mean"][ok]) / se[ok]
+    assert np.abs(z).max() < 4.5
+    assert abs(z.mean()) < 4.0 / np.sqrt(ok.sum())
