@@ -89,6 +89,44 @@ def test_two_rank_protocol_matches_single_rank(orc):
     np.testing.assert_allclose(out["grad"], g, rtol=1e-9, atol=1e-15)
 
 
+def _worker3(rank, world, port, out):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from oracle_lib import Oracle3
+    from paper_2410_18944_b200.scene3 import make_preset3, slice_points
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    o3 = Oracle3()
+    h = o3.scene(make_preset3("box-strip-vlin", n=6).scene)
+    pts = slice_points(12, 12)
+    mine, off = shard_points(pts, world, rank)
+    # 3D walks keyed by the GLOBAL point index (cfg 5 sharding)
+    st = o3.run(h, None, abi.solver_config("uniform"), mine, 5, 3, point_offset=off)
+    full = gather_stats(dist, st, world)
+    if rank == 0:
+        out["stats"] = full
+    dist.destroy_process_group()
+
+
+def test_two_rank_3d_sharding_matches_single_rank():
+    """cfg 5's protocol on the 3D oracle: points sharded over ranks with walk
+    streams keyed by the global index give the single-rank statistics."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from oracle_lib import Oracle3
+    from paper_2410_18944_b200.scene3 import make_preset3, slice_points
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker3, args=(2, _port(), out), nprocs=2, join=True)
+    o3 = Oracle3()
+    h = o3.scene(make_preset3("box-strip-vlin", n=6).scene)
+    st = o3.run(h, None, abi.solver_config("uniform"), slice_points(12, 12), 5, 3)
+    full = out["stats"]
+    assert np.array_equal(full["count"], st["count"])
+    assert np.array_equal(full["mean"], st["mean"])
+
+
 def test_shard_bounds_cover_all_points():
     for n in (1, 7, 16384, 16385):
         for world in (1, 2, 3, 8):
