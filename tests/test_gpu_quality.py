@@ -74,3 +74,34 @@ def test_guided_relmse_and_variance_reduction_within_10_percent(gpu):
     assert abs(np.mean(ours_g) - ref_g) / ref_g < 0.10, (ours_g, ref_g)
     vr_ours, vr_ref = np.mean(ours_u) / np.mean(ours_g), ref_u / ref_g
     assert abs(vr_ours - vr_ref) / vr_ref < 0.10, (vr_ours, vr_ref)
+
+
+def test_cfg3_six_seed_relmse_and_vr_within_10pct(gpu):
+    """cfg 3 (const-source-disk: source term f = 4, eps = 1e-6, learnable MIS
+    with online training) at 128^2 x 256 wpp, seeds 1-6, against the
+    reference's own run_solve over the same seeds
+    (tests/golden/ref_cfg3_seeds.json, tests/golden/make_cfg3_seeds.py):
+    mean relMSE and the variance-reduction factor within 10%; uniform relMSE
+    equal to the reference's (same walks)."""
+    with open(os.path.join(G, "ref_cfg3_seeds.json")) as f:
+        ref = json.load(f)
+    pr = make_preset("const-source-disk")
+    pts = cell_centers(128, 128, pr.eval_bbox)
+    truth = np.array([pr.analytic(x, y) for x, y in pts])
+    acc = api.Accel(pr.scene)
+    g, u = [], []
+    for seed in range(1, 7):
+        f = api.GuidingField(abi.field_config(), pr.scene.bbox, seed)
+        s = api.Solver(acc, f, abi.solver_config("learnable_mis"), api.MLP_TENSOR)
+        s.set_points(pts)
+        s.run(seed, 256, 256, abi.train_config(seed=seed))
+        g.append(relmse(s.stats()["mean"], truth))
+        us = api.Solver(acc, None, abi.solver_config("uniform"))
+        us.set_points(pts)
+        us.run(seed, 256, 0, None)
+        u.append(relmse(us.stats()["mean"], truth))
+    rg = np.mean([ref["learnable_mis"][str(i)] for i in range(1, 7)])
+    ru = np.mean([ref["uniform"][str(i)] for i in range(1, 7)])
+    assert np.mean(u) == pytest.approx(ru, rel=1e-6)
+    assert abs(np.mean(g) / rg - 1.0) < 0.10, (np.mean(g), rg)
+    assert abs((np.mean(u) / np.mean(g)) / (ru / rg) - 1.0) < 0.10
