@@ -32,6 +32,7 @@ struct wg_solver3_s {
   // records of the last collecting round (wg3::DevRecord3 in a wg::DevRecord arena)
   wgrt::DBuf recs, rec_counter, rec_tail, rec_term, rec_dacc;
   int64_t rec_cap = 0;
+  int64_t rec_cap_min = 0;  // grown after an arena overflow
   bool have_records = false;
   // wavefront walk pool (WG_MLP_TENSOR guided walks, wg3_walk_tc.cu)
   wgrt::DBuf w_lanes, w_dirs, w_rec, w_state, w_queue, w_qlen, w_next;

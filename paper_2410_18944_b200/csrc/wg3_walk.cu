@@ -472,7 +472,9 @@ void enqueue3_rounds(wg_solver3_s* s, uint64_t seed, uint64_t wpp_first, int32_t
     s->last_rounds = chunk;
   }
   if (collect) {
-    int64_t cap = std::max<int64_t>(s->n_points * 128, int64_t(1) << 16);
+    // 3D walks average ~20 steps (cfg 4): 48 records per point, doubled for
+    // the next call after any overflow (as in 2D); 80 + 4 B per record
+    int64_t cap = std::max<int64_t>({s->n_points * 48, int64_t(1) << 16, s->rec_cap_min});
     if (s->rec_cap < cap) {
       s->recs.alloc(sizeof(DevRecord3) * cap);
       s->rec_dacc.alloc(sizeof(float) * cap);
@@ -665,8 +667,11 @@ wg_train_stats sync3(wg_solver3_s* s, long long steps_before) {
   CK(cudaStreamSynchronize(s->st));
   unsigned long long c[C_N];
   CK(cudaMemcpy(c, s->counters.p, sizeof(c), cudaMemcpyDeviceToHost));
-  if (c[C_REC_OVERFLOW] > 0)
-    std::fprintf(stderr, "wostgpu: 3D record arena overflow (%llu chunks dropped)\n", c[C_REC_OVERFLOW]);
+  if (c[C_REC_OVERFLOW] > 0) {
+    s->rec_cap_min = std::max<int64_t>(s->rec_cap_min, 2 * s->rec_cap);
+    std::fprintf(stderr, "wostgpu: 3D record arena overflow (%llu chunks dropped, capacity %lld); the next call uses %lld\n",
+                 c[C_REC_OVERFLOW], static_cast<long long>(s->rec_cap), static_cast<long long>(s->rec_cap_min));
+  }
   Ev3& e = events()[s];
   s->last_walk_ms = static_cast<float>(ev_ms(e.walk, e.nw));
   s->last_train_ms = static_cast<float>(ev_ms(e.train, e.nt));
