@@ -225,6 +225,9 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
     a.wpp_first = wpp_first + r0;
     a.n_rounds = n;
     int64_t want = (s->n_points * n * lanes_per_walk + block - 1) / block;
+    // tensor-core lockstep kernel: at least one CTA per SM (walk ids are
+    // interleaved over CTAs, so a small round spreads over every SM)
+    if (tc) want = std::max<int64_t>(want, s->sms);
     int blocks = static_cast<int>(std::min<int64_t>(want, (int64_t)per_sm * s->sms));
     static const bool phase_prof = std::getenv("WOSTGPU_PHASE_PROF") != nullptr;
     if (phase_prof && tc) {

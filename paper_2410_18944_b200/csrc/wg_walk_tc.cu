@@ -309,7 +309,10 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
   const bool collect = a.recs != nullptr;
   const int64_t total = a.n_points * static_cast<int64_t>(a.n_rounds);
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  int64_t next = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  // walk ids interleaved over the CTAs (id = thread * grid + block): a round
+  // with fewer walks than slots spreads evenly over every SM instead of
+  // filling the first CTAs (a CTA lasts as long as its longest walk)
+  int64_t next = static_cast<int64_t>(threadIdx.x) * gridDim.x + blockIdx.x;
   const double pad = 1e-9 * s.diag;
   const FieldView& fv = a.field;
   uint32_t phase = 0;
