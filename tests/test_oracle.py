@@ -172,3 +172,58 @@ def test_harmonic_disk_unbiased(orc):
                           point_index=np.arange(n))
     se = est.std(ddof=1) / math.sqrt(n)
     assert abs(est.mean() - 0.05) < 3 * se
+
+
+def test_d3_mixture_and_gradient_match_reference(orc, ref):
+    """The d = 3 vMF pieces the 3D path builds on, oracle vs the reference
+    library: Table-1 normalisation (sphdist.cpp:287-310), mixture and MIS
+    densities with and without a Neumann normal (:176-270), and the
+    raw-parameter gradient through a mixture_dim = 3 field (mixture_grad with
+    dlogv_dkappa's d = 3 branch, sphdist.cpp:315-381; kl_grad /
+    selection_grad, guide_train.cpp:25-56). Plus the reference test's d = 3
+    vMF peak (kappa = 2: 0.324236, proj/tests/test_sphdist.cpp)."""
+    rng = np.random.default_rng(17)
+    raw = rng.normal(scale=1.5, size=(40, 41))
+    mo, mr = orc.normalize(raw, 8, 3), ref.normalize(raw, 8, 3)
+    for k in ("mu", "kappa", "lambda", "log_a", "c"):
+        np.testing.assert_allclose(mo[k], mr[k], rtol=1e-14, atol=1e-300)
+    for i in range(len(raw)):
+        nu = rng.normal(size=3)
+        nu /= np.linalg.norm(nu)
+        n = rng.normal(size=3)
+        n /= np.linalg.norm(n)
+        a = orc.fn("mixture_pdf")(abi.vptr(mo[i:i + 1]), abi.ptr(nu))
+        b = ref.fn("mixture_pdf")(abi.vptr(mr[i:i + 1]), abi.ptr(nu))
+        assert a == pytest.approx(b, rel=1e-13)
+        for normal in (None, n):
+            a = orc.fn("mis_pdf")(abi.vptr(mo[i:i + 1]), abi.ptr(nu), None if normal is None else abi.ptr(normal), 1)
+            b = ref.fn("mis_pdf")(abi.vptr(mr[i:i + 1]), abi.ptr(nu), None if normal is None else abi.ptr(normal), 1)
+            assert a == pytest.approx(b, rel=1e-13)
+    # single component, kappa = 2, at its mode
+    one = np.zeros(1, dtype=abi.MIXTURE_DTYPE)
+    one["k"], one["dim"], one["c"] = 1, 3, 1.0
+    one["mu"][0, 0] = [0.0, 0.0, 1.0]
+    one["kappa"][0, 0], one["lambda"][0, 0] = 2.0, 1.0
+    peak = ref.fn("mixture_pdf")(abi.vptr(one), abi.ptr(np.array([0.0, 0.0, 1.0])))
+    # proj/tests/test_sphdist.cpp:91-95: 2 e^2 / (4 pi sinh 2) to 1e-12 (the
+    # literal 0.324236 there is checked with doctest's loose epsilon)
+    assert peak == pytest.approx(2.0 * math.exp(2.0) / (4.0 * math.pi * math.sinh(2.0)), rel=1e-12)
+    assert orc.fn("mixture_pdf")(abi.vptr(one), abi.ptr(np.array([0.0, 0.0, 1.0]))) == pytest.approx(peak, rel=1e-14)
+    # gradient through a 2D-position field with a d = 3 mixture
+    pr = make_preset("neumann-strip-vlin")
+    cfg = abi.field_config(mixture_dim=3)
+    fo, fr = orc.field(cfg, pr.scene.bbox, 5), ref.field(cfg, pr.scene.bbox, 5)
+    recs = np.zeros(300, dtype=abi.GUIDE_RECORD_DTYPE)
+    recs["x"] = rng.uniform(0.02, 0.98, (300, 2))
+    nu = rng.normal(size=(300, 3))
+    recs["nu"] = nu / np.linalg.norm(nu, axis=1)[:, None]
+    recs["target"] = rng.uniform(0.0, 2.0, 300)
+    recs["pdf_mis"] = rng.uniform(0.05, 0.5, 300)
+    recs["pdf_g"] = rng.uniform(0.05, 0.5, 300)
+    recs["pdf_u"] = 1.0 / (4.0 * np.pi)
+    recs["c"] = 0.5
+    recs["on_neumann"] = rng.integers(0, 2, 300)
+    recs["normal"] = np.where(rng.random((300, 1)) < 0.5, [[0.0, 1.0]], [[0.0, -1.0]])
+    tc = abi.train_config()
+    go, gr = orc.field_grad(fo, recs, tc), ref.field_grad(fr, recs, tc)
+    np.testing.assert_allclose(go, gr, rtol=1e-9, atol=1e-14 * np.abs(gr).max())
