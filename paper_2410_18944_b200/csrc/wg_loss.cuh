@@ -97,7 +97,8 @@ WG_D bool record_dy(const float* raw, const DevRecord& r, const TrainArgs& a, fl
 // I1/I0 by rational approximation; sampling-time quantities (target, pdf_mis,
 // pdf_u) come from the record.
 __device__ __forceinline__ float mix_grad_one32(const Mix32& m, const float* raw, const float* inv_mn,
-                                                const bool* kap_free, float nx, float ny, float* g) {
+                                                const bool* kap_free, const float* i10, float nx, float ny,
+                                                float* g) {
   float v[8], t[8];
   float val = 0.0f;
 #pragma unroll
@@ -110,7 +111,7 @@ __device__ __forceinline__ float mix_grad_one32(const Mix32& m, const float* raw
   for (int i = 0; i < 8; ++i) {
     const float lv = m.lambda[i] * v[i];
     g[24 + i] += lv - m.lambda[i] * val;
-    if (kap_free[i]) g[16 + i] += lv * (t[i] - i1_over_i0_f(m.kappa[i])) * m.kappa[i];
+    if (kap_free[i]) g[16 + i] += lv * (t[i] - i10[i]) * m.kappa[i];
     const float s = lv * m.kappa[i] * inv_mn[i];
     g[2 * i] += (nx - m.mux[i] * t[i]) * s;
     g[2 * i + 1] += (ny - m.muy[i] * t[i]) * s;
@@ -125,10 +126,11 @@ __device__ __forceinline__ bool record_dy32(const float* raw, const DevRecord& r
   for (int j = 0; j < 33; ++j) g[j] = 0.0f;
   Mix32 m;
   normalize32(raw, m);
-  float inv_mn[8];
+  float inv_mn[8], i10[8];  // I1/I0(kappa) once per record (both directions share it)
   bool kap_free[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
+    i10[i] = i1_over_i0_f(m.kappa[i]);
     const float mx = raw[2 * i], my = raw[2 * i + 1];
     const float mn = sqrtf(mx * mx + my * my);
     inv_mn[i] = mn >= 1e-12f ? 1.0f / mn : 0.0f;  // zero-norm means get no mu gradient
@@ -142,10 +144,10 @@ __device__ __forceinline__ bool record_dy32(const float* raw, const DevRecord& r
     float dv[33];
 #pragma unroll
     for (int j = 0; j < 33; ++j) dv[j] = 0.0f;
-    float v = mix_grad_one32(m, raw, inv_mn, kap_free, nx, ny, dv);
+    float v = mix_grad_one32(m, raw, inv_mn, kap_free, i10, nx, ny, dv);
     if (on_n && a.reflect) {
       const float d = 2.0f * (nx * px + ny * py);
-      v += mix_grad_one32(m, raw, inv_mn, kap_free, nx - px * d, ny - py * d, dv);
+      v += mix_grad_one32(m, raw, inv_mn, kap_free, i10, nx - px * d, ny - py * d, dv);
     }
     if (!(static_cast<double>(v) > a.v_floor)) return false;
     const float s = -target / (r.pdf_mis * v);
