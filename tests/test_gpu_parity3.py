@@ -301,3 +301,44 @@ def test_poisson_tensor_path_matches_analytic(gpu):
     z = (st["mean"][ok] - ref[ok]) / np.sqrt(st["m2"][ok] / (st["count"][ok] - 1) / st["count"][ok])
     assert np.abs(z).max() < 5.0
     assert abs(z.mean()) < 0.3
+
+
+def test_error_paths(gpu):
+    """The 3D boundary's failure modes map to the reference's exception
+    classes (SceneError / invalid_argument), like the 2D C-ABI."""
+    from paper_2410_18944_b200._lib import InvalidArgument, SceneError, WostGpuError
+    from paper_2410_18944_b200.scene3 import Scene3
+    from paper_2410_18944_b200 import api
+    empty = Scene3(np.zeros((0, 3, 3)), np.zeros(0, np.int32), np.zeros(0, np.int32),
+                   [(0, 0.0, 0.0, 0.0, 0.0)])
+    with pytest.raises(SceneError):
+        Accel3(empty)
+    bad = make_preset3("box-strip-vlin", n=2).scene
+    bad.value_index = bad.value_index.copy()
+    bad.value_index[0] = 7  # undefined value
+    with pytest.raises(SceneError):
+        Accel3(bad)
+    with pytest.raises(InvalidArgument):
+        GuidingField3(abi.field_config(mixture_dim=2), BOX, 1)  # 3D fields need a d = 3 mixture
+    with pytest.raises(InvalidArgument):
+        GuidingField3(abi.field_config3(), (0, 0, 0, 1, 0, 1), 1)  # empty bbox
+    acc = Accel3(make_preset3("box-strip-vlin", n=4).scene)
+    with pytest.raises(InvalidArgument):
+        Solver3(acc, None, abi.solver_config("learnable_mis"))  # guided without a field
+    f2 = api.GuidingField(abi.field_config(), (0, 0, 1, 1), 1)
+    with pytest.raises(WostGpuError):
+        Solver3(acc, f2, abi.solver_config("learnable_mis"))  # a 2D field
+    s = Solver3(acc, None, abi.solver_config("uniform"))
+    with pytest.raises(WostGpuError):
+        s.set_points(np.zeros((0, 3)))
+    # a Neumann-only closed box: no Dirichlet boundary, no silhouette -> unbounded star
+    only_n = make_preset3("box-strip-vlin", n=2).scene
+    only_n.kind = np.full(only_n.n_tris, abi.NEUMANN, dtype=np.int32)
+    only_n.value_index = np.zeros(only_n.n_tris, dtype=np.int32)
+    acc_n = Accel3(only_n)
+    with pytest.raises(SceneError):
+        acc_n.star_radius(np.array([[0.5, 0.5, 0.5]]), 1e-3)
+    sn = Solver3(acc_n, None, abi.solver_config("uniform"))
+    sn.set_points(np.array([[0.5, 0.5, 0.5]]))
+    with pytest.raises(SceneError):
+        sn.run(1, 1, 0, None)
