@@ -15,10 +15,23 @@
 // Weights are split into fp16 hi/lo once per CTA from the fp32 parameters.
 // This translation unit may contract FMAs (Makefile FAST_TUS): its results
 // are compared with the oracle statistically, the exact kernel bit for bit.
+#include "wg3_mix32.cuh"
 #include "wg3_walk_common.cuh"
 #include "wg_mlp_tc.cuh"
 
 namespace wg3 {
+
+// decode_guiding (wost.cpp:111-122) + sample_next_direction with the fp32
+// mixture (wg3_mix32.cuh)
+__device__ __forceinline__ Dir3 sample_guided_f(Lane3& w, const Walk3Args& a, const float* raw) {
+  Mix3f m;
+  normalize3f(raw, m);
+  double c = m.c;
+  if (a.sp.mode == WG_MODE_GUIDING_ONLY) c = 1.0;
+  else if (a.sp.mode == WG_MODE_FIXED_MIS) c = a.sp.fixed_c;
+  const Mis3 o = mis_sample3f(w.rng, m, c, w.on_n, w.n, a.sp.reflect != 0);
+  return Dir3{o.nu, o.pmis, o.pg, o.pu, c, o.pu / o.pmis};
+}
 
 __device__ __forceinline__ void gather3_tc(const Field3View& f, D3 x, float* in) {
   const float u = static_cast<float>(wg::sclamp((x.x - f.bbox[0]) / (f.bbox[3] - f.bbox[0]), 0.0, 1.0));
@@ -96,11 +109,7 @@ __global__ void __launch_bounds__(128, 1) walk3_tc_kernel(Walk3Args a) {
     }
     wg::tc_forward<OD>(smem, phase, in, raw);
     // ---- C: mixture, MIS direction, move
-    if (need) {
-      Mix3<K8> m;
-      decode3(raw, a.sp, m);
-      step_finish(w, a, collect, rec, &m);
-    }
+    if (need) step_move(w, a, collect, rec, sample_guided_f(w, a, raw), true);
   }
   if (collect)
     for (int i = 0; i < w.rec_left; ++i) a.recs[w.rec_base + (8 - w.rec_left) + i].flags = 0u;
@@ -222,9 +231,7 @@ __global__ void __launch_bounds__(128, WG3_DIR_MINB) wave_dir_kernel(Walk3Args a
     }
     wg::tc_forward<OD>(smem, phase, in, raw);
     if (live) {
-      Mix3<K8> m;
-      decode3(raw, a.sp, m);
-      v.dirs[slot] = step_sample(w, a, &m);
+      v.dirs[slot] = sample_guided_f(w, a, raw);
       v.lanes[slot].rng = w.rng;
       v.state[slot] = SLOT_NEED_MOVE;
     }
