@@ -8,8 +8,9 @@
 //                      star radius, source / Neumann terms; wost.cpp:148-216)
 //                      and queues the slot when it needs a direction;
 //   wave2_dir_kernel   persistent tcgen05 tiles over the queue: bilinear
-//                      gather, the MLP (wg_mlp_tc.cuh), then per row the fp64
-//                      decode and MIS sampling (sphdist.cpp:254-270).
+//                      gather, the MLP (wg_mlp_tc.cuh), then per row the
+//                      decode and MIS sampling (sphdist.cpp:254-270) with the
+//                      tensor path's fp32 mixture math (wg_mix32.cuh).
 // Used for the tensor-core path when enough walks are in flight to fill the
 // GPU (cfg 3: a 256-segment disk, 512^2 points): the lockstep kernel's
 // iteration waits for the slowest of 128 BVH traversals (phase A ~60k
@@ -18,6 +19,7 @@
 // translation unit may contract FMAs (statistical parity, like the tensor
 // path).
 #include "wg_kernels.cuh"
+#include "wg_mix32.cuh"
 #include "wg_mlp_tc.cuh"
 #include "wg_sphdist.cuh"
 
@@ -179,12 +181,6 @@ __device__ __forceinline__ bool step2_begin(Lane2& w, const WalkArgs& a, bool co
   return true;
 }
 
-// guided direction from the decoded mixture (mis_sample, sphdist.cpp:254-270)
-__device__ __forceinline__ Dir2 step2_sample(Lane2& w, const WalkArgs& a, const Mix& m) {
-  MisOut o = mis_sample(w.rng, m, w.on_n, w.nx, w.ny, a.sp.reflect != 0);
-  return Dir2{o.nx, o.ny, o.pmis, o.pg, o.pu, m.c, o.pu / o.pmis};
-}
-
 // record + finish_step (wost.cpp:218-264) along a guided direction
 __device__ __forceinline__ void step2_move(Lane2& w, const WalkArgs& a, bool collect, int rec, const Dir2& d) {
   const SceneView& s = a.scene;
@@ -315,11 +311,16 @@ __global__ void __launch_bounds__(128) wave2_dir_kernel(WalkArgs a, Wave2 v, int
     }
     tc_forward(smem, phase, in, raw);
     if (live) {
-      Mix m;
-      normalize2<8>(raw, 8, m);  // decode_guiding, wost.cpp:111-122
-      if (a.sp.mode == WG_MODE_GUIDING_ONLY) m.c = 1.0;
-      else if (a.sp.mode == WG_MODE_FIXED_MIS) m.c = a.sp.fixed_c;
-      v.dirs[slot] = step2_sample(w, a, m);
+      // decode + MIS with the tensor path's fp32 mixture math (wg_mix32.cuh)
+      Mix32 m;
+      normalize32(raw, m);
+      double sel = m.c;  // decode_guiding, wost.cpp:111-122
+      if (a.sp.mode == WG_MODE_GUIDING_ONLY) sel = 1.0;
+      else if (a.sp.mode == WG_MODE_FIXED_MIS) sel = a.sp.fixed_c;
+      double dnx, dny;
+      mis_draw32(w.rng, m, sel, w.on_n, w.nx, w.ny, a.sp.reflect != 0, &dnx, &dny);
+      const MisOut o = mis_eval32(m, sel, w.on_n, w.nx, w.ny, a.sp.reflect != 0, dnx, dny);
+      v.dirs[slot] = Dir2{o.nx, o.ny, o.pmis, o.pg, o.pu, sel, o.pu / o.pmis};
       v.lanes[slot].rng = w.rng;
       v.state[slot] = SLOT_NEED_MOVE;
     }
