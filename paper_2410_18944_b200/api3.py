@@ -130,6 +130,54 @@ class GuidingField3:
         v = np.ascontiguousarray(v, dtype=np.float64)
         check(load().wostgpu_field_set_state(self.h, p.ctypes.data_as(C.POINTER(C.c_float)), _d(m), _d(v), steps))
 
+    def save(self, path):
+        """Checkpoint in the WGF1 layout (GuidingField::save,
+        proj/src/guide_field.cpp:351-372) with magic "WGF3" and a 3D bbox
+        (6 doubles): WGF1 itself is 2D-only."""
+        p, m, v, steps = self.state()
+        c = self.cfg
+        with open(path, "wb") as f:
+            f.write(b"WGF3")
+            hdr = [1, c.n_levels] + [c.level_res[i] for i in range(c.n_levels)]
+            hdr += [c.features, c.hidden, c.mixture_k, c.mixture_dim]
+            f.write(np.array(hdr, dtype="<u4").tobytes())
+            f.write(np.array(self.bbox, dtype="<f8").tobytes())
+            f.write(np.array([steps], dtype="<i8").tobytes())
+            f.write(np.array([len(p)], dtype="<u8").tobytes())
+            f.write(p.astype("<f4").tobytes())
+            f.write(m.astype("<f8").tobytes())
+            f.write(v.astype("<f8").tobytes())
+
+    @classmethod
+    def load(cls, path):
+        with open(path, "rb") as f:
+            data = f.read()
+        if data[:4] != b"WGF3":
+            raise ValueError("3D guiding field checkpoint: bad magic")
+        off = 4
+        ver, nl = (int(x) for x in np.frombuffer(data, "<u4", 2, off))
+        if ver != 1:
+            raise ValueError("3D guiding field checkpoint: unknown version")
+        off += 8
+        res = [int(r) for r in np.frombuffer(data, "<u4", nl, off)]
+        off += 4 * nl
+        feat, hid, k, dim = (int(x) for x in np.frombuffer(data, "<u4", 4, off))
+        off += 16
+        bbox = tuple(float(x) for x in np.frombuffer(data, "<f8", 6, off))
+        off += 48
+        steps = int(np.frombuffer(data, "<i8", 1, off)[0])
+        off += 8
+        n = int(np.frombuffer(data, "<u8", 1, off)[0])
+        off += 8
+        field = cls(abi.field_config(tuple(res), features=feat, hidden=hid, mixture_k=k, mixture_dim=dim), bbox, 0)
+        if n != field.n_params or len(data) < off + 20 * n:
+            raise ValueError("3D guiding field checkpoint: size mismatch or truncated")
+        p = np.frombuffer(data, "<f4", n, off)
+        m = np.frombuffer(data, "<f8", n, off + 4 * n)
+        v = np.frombuffer(data, "<f8", n, off + 12 * n)
+        field.set_state(p, m, v, steps)
+        return field
+
     def eval_batch(self, x, mlp=MLP_EXACT):
         x = _xyz(x)
         out = np.zeros((len(x), self.output_dim))

@@ -342,3 +342,22 @@ def test_error_paths(gpu):
     sn.set_points(np.array([[0.5, 0.5, 0.5]]))
     with pytest.raises(SceneError):
         sn.run(1, 1, 0, None)
+
+
+def test_field3_checkpoint_round_trip(gpu, tmp_path):
+    """A trained 3D field saved (WGF1 layout, magic WGF3) and loaded gives the
+    same parameters, Adam state and evaluation."""
+    p = make_preset3("box-strip-vlin", n=8)
+    f = GuidingField3(abi.field_config3(), BOX, 4)
+    s = Solver3(Accel3(p.scene), f, abi.solver_config("learnable_mis"))
+    s.set_points(slice_points(16, 16))
+    s.run(4, 3, 3, abi.train_config(seed=4))
+    path = str(tmp_path / "field.wgf3")
+    f.save(path)
+    g = GuidingField3.load(path)
+    a, b = f.state(), g.state()
+    for u, v in zip(a[:3], b[:3]):
+        assert np.array_equal(u, v)
+    assert a[3] == b[3] and a[3] >= 3
+    x = probes3(9, 500)
+    assert np.array_equal(f.eval_batch(x), g.eval_batch(x))
