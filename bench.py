@@ -342,6 +342,7 @@ def main3(args):
             "e2e": {"value": walks_per_step / e2e_s, "unit": "walks/s", "h2d_bytes_per_step": pts.nbytes,
                     "d2h_bytes_per_step": n_local * abi.POINT_STATS_DTYPE.itemsize},
             "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
+            "walk_steps_per_s": pr["steps"] * world / (float(np.mean(times)) * 1e-3),
             "quality": quality}))
     if dist:
         dist.barrier()
@@ -546,6 +547,9 @@ def main():
                 "e2e": {"value": walks_per_step / e2e_s, "unit": "walks/s",
                         "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                 "gpu_launches": int(launches),
+                # walk steps per second: the walk kernel's steps of one
+                # step (solve) over its device time, all ranks (weak scaling)
+                "walk_steps_per_s": pr["steps"] * world / (step_ms * 1e-3),
                 "roofline": roofline,
                 "cpu_baseline": cpu,
                 "clocks": clk.summary(),
