@@ -26,7 +26,7 @@ namespace wg3 {
 __device__ __forceinline__ Dir3 sample_guided_f(Lane3& w, const Walk3Args& a, const float* raw) {
   Mix3f m;
   normalize3f(raw, m);
-  double c = m.c;
+  double c = sigmoid(static_cast<double>(raw[40]));  // fp64: 1 - c must not round to 0 (see wg_walk_tc.cu)
   if (a.sp.mode == WG_MODE_GUIDING_ONLY) c = 1.0;
   else if (a.sp.mode == WG_MODE_FIXED_MIS) c = a.sp.fixed_c;
   const Mis3 o = mis_sample3f(w.rng, m, c, w.on_n, w.n, a.sp.reflect != 0);

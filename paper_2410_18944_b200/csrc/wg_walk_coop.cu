@@ -366,7 +366,7 @@ __device__ __forceinline__ float sum8(float v) {
   return v;
 }
 
-__device__ __forceinline__ Lobe c_decode(float y, float y32, int lane, float* c_out) {
+__device__ __forceinline__ Lobe c_decode(float y, float y32, int lane, double* c_out) {
   const int i = lane & 7;
   const float mx = __shfl_sync(0xffffffffu, y, 2 * i), my = __shfl_sync(0xffffffffu, y, 2 * i + 1);
   const float kr = __shfl_sync(0xffffffffu, y, 16 + i), lr = __shfl_sync(0xffffffffu, y, 24 + i);
@@ -393,7 +393,11 @@ __device__ __forceinline__ Lobe c_decode(float y, float y32, int lane, float* c_
   L.lambda = e * __frcp_rn(sum8(e));
   const float ec = __expf(-fabsf(cr));
   const float sg = 1.0f / (1.0f + ec);
-  *c_out = cr >= 0.0f ? sg : ec * sg;
+  // c in fp64 from the logit: an fp32 sigmoid rounds to 1 above ~16.6 and
+  // would drop the defensive (1 - c) p_u term from p_mis
+  (void)sg;
+  (void)ec;
+  *c_out = sigmoid(static_cast<double>(cr));
   return L;
 }
 
@@ -524,7 +528,7 @@ __global__ void __launch_bounds__(kCoopThreads, 2) walk_kernel_coop(WalkArgs a) 
       c_gather(f, w.x, w.y, xin);
       float y32;
       const float y = c_mlp(W, hbuf, xin, lane, &y32);
-      float cdec;
+      double cdec;
       const Lobe L = c_decode(y, y32, lane, &cdec);
       double sel = cdec;
       if (a.sp.mode == WG_MODE_GUIDING_ONLY) sel = 1.0;

@@ -432,7 +432,10 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
     normalize32(raw, m);
     SUB_ADD(5, tn);
     SUB_T(ts);
-    double sel = m.c;
+    // the selection probability in fp64 from the logit (sphdist.cpp:280-283):
+    // an fp32 sigmoid rounds to exactly 1 above ~16.6, which would drop the
+    // defensive (1 - c) p_u term from p_mis and leave p_u / p_mis unbounded
+    double sel = sigmoid(static_cast<double>(raw[32]));
     if (a.sp.mode == WG_MODE_GUIDING_ONLY) sel = 1.0;
     else if (a.sp.mode == WG_MODE_FIXED_MIS) sel = a.sp.fixed_c;
     double dnx, dny;

@@ -314,7 +314,9 @@ __global__ void __launch_bounds__(128) wave2_dir_kernel(WalkArgs a, Wave2 v, int
       // decode + MIS with the tensor path's fp32 mixture math (wg_mix32.cuh)
       Mix32 m;
       normalize32(raw, m);
-      double sel = m.c;  // decode_guiding, wost.cpp:111-122
+      // decode_guiding (wost.cpp:111-122); c in fp64 from the logit so that
+      // 1 - c (the defensive uniform weight in p_mis) never rounds to 0
+      double sel = sigmoid(static_cast<double>(raw[32]));
       if (a.sp.mode == WG_MODE_GUIDING_ONLY) sel = 1.0;
       else if (a.sp.mode == WG_MODE_FIXED_MIS) sel = a.sp.fixed_c;
       double dnx, dny;
