@@ -444,8 +444,12 @@ def main():
     alg_bytes = pr["steps"] * BYTES_PER_STEP + pr["train_steps"] * BYTES_PER_TRAIN_STEP
     achieved = alg_bytes / (pr["walk_ms"] * 1e-3) / 1e9
     kname = "walk_kernel_tc" if args.mlp == "tensor" else "walk_kernel_g8"
+    # the walk phase of a round: the lockstep tile kernel plus, on small
+    # scenes, the warp-per-walk kernel that finishes each CTA's last <= 24
+    # walks (walk_kernel_coop_resume); walk_ms spans both
+    klabel = kname + (" + walk_kernel_coop_resume (walk phase)" if args.mlp == "tensor" else "")
     rounds = max(1, WPP)
-    roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved,
+    roofline = {"bound": "hbm", "kernel": klabel, "achieved": achieved,
                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                 "traffic": None, "peak_source": peak_kind,
                 "algorithmic_bytes_per_launch": alg_bytes / rounds,

@@ -91,6 +91,21 @@ struct WalkArgs {
   // step + barrier), B (MLP), C (sample + move), iterations, MMA windows,
   // gather, MLP prep (WOSTGPU_PHASE_PROF)
   unsigned long long* phase_prof;
+  // lockstep-kernel tail handoff: once at most spill_rows walks of a CTA are
+  // live and it has no fresh walks left, the CTA writes them here (count in
+  // counters[7]) and exits; the warp-per-walk kernel finishes them
+  // (walk_kernel_coop_resume). 0 = off
+  struct SpillLane* spill;
+  int32_t spill_rows;
+};
+
+// a walk handed from the lockstep kernel's tail to the warp-per-walk kernel:
+// its state after begin_step, direction still to draw (TLane / CLane fields)
+struct SpillLane {
+  double x, y, nx, ny, T, acc, dacc, R;
+  int64_t point, rec_base;
+  Pcg rng;
+  int32_t seg, depth, rec, round, rec_left, last_rec, on_n, rec_ok;
 };
 
 struct QueryArgs {
@@ -124,12 +139,14 @@ cudaError_t launch_walks_g8(const WalkArgs& a, int blocks, cudaStream_t st);
 int walk_tc_smem(const WalkArgs& a);
 int walk_tc_blocks_per_sm(int smem);
 int walk_tc_block();
+int walk_tc_warps();
 cudaError_t launch_walks_tc(const WalkArgs& a, int blocks, cudaStream_t st);
 // warp-per-walk guided kernel for the default field shape (wg_walk_coop.cu)
 int walk_coop_smem(const WalkArgs& a);
 int walk_coop_block();
 int walk_coop_blocks_per_sm(int smem);
 cudaError_t launch_walks_coop(const WalkArgs& a, int blocks, cudaStream_t st);
+cudaError_t launch_walks_coop_resume(const WalkArgs& a, int max_walks, int sms, cudaStream_t st);
 // wavefront pair for guided 2D walks on the tensor cores (wg_wave2.cu)
 void wave2_sizes(size_t* lane_bytes, size_t* dir_bytes);
 cudaError_t launch_walks2_wave(const WalkArgs& a, void* lanes, void* dirs, int32_t* rec, uint8_t* state,

@@ -59,6 +59,7 @@ struct wg_solver_s {
   DBuf lists, grad;
   int64_t list_cap = 0;
   DBuf phase_prof;  // WOSTGPU_PHASE_PROF diagnostics
+  DBuf spill;       // lockstep-kernel tail handoff (SpillLane per slot)
   // timing: event pairs around walk launches and training rounds
   std::vector<cudaEvent_t> ev_walk, ev_train;
   int n_walk_ev = 0, n_train_ev = 0;
@@ -266,7 +267,28 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
                             s->w_queue.as<int32_t>(), s->w_qlen.as<unsigned int>(),
                             s->w_next.as<unsigned long long>(), slots, s->sms, s->h_qlen, &launched, s->stream));
       g_launches += launched;
-    } else if (tc) CKL(launch_walks_tc(a, std::max(1, blocks), s->stream));
+    } else if (tc) {
+      // tail handoff to the warp-per-walk kernel (WalkArgs::spill) once a
+      // CTA has <= 24 live walks: small scenes only, where both kernels scan
+      // shared-memory segment lists. cfg 2 walk time per round 0.566 -> 0.478
+      // ms (T = 16 / 32 / 48 / 64: 0.485 / 0.481 / 0.493 / 0.519); cfg 3's
+      // 256-gon: 1.55 vs 1.59 ms, off. WOSTGPU_SPILL_ROWS overrides (0 = off)
+      static const int spill_env = [] {
+        const char* e = std::getenv("WOSTGPU_SPILL_ROWS");
+        return e ? std::atoi(e) : -1;
+      }();
+      const int nb = std::max(1, blocks);
+      const int spill_want = spill_env >= 0 ? spill_env : s->scene->view.n_segs <= 16 ? 24 : 0;
+      const int spill_rows = walk_tc_warps() == 0 && a.small_mlp ? std::max(0, std::min(spill_want, 128)) : 0;
+      a.spill_rows = spill_rows;
+      if (spill_rows > 0) {
+        s->spill.alloc(sizeof(SpillLane) * nb * spill_rows);
+        a.spill = s->spill.as<SpillLane>();
+        CK(cudaMemsetAsync(a.counters + 7, 0, sizeof(unsigned long long), s->stream));
+      }
+      CKL(launch_walks_tc(a, nb, s->stream));
+      if (spill_rows > 0) CKL(launch_walks_coop_resume(a, nb * spill_rows, s->sms, s->stream));
+    }
     if (phase_prof && tc) {  // diagnostics: cycles per CTA iteration of the slowest CTA
       std::vector<unsigned long long> h(8 * blocks);
       CK(cudaMemcpyAsync(h.data(), s->phase_prof.p, sizeof(unsigned long long) * 8 * blocks,

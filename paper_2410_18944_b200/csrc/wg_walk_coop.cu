@@ -432,8 +432,10 @@ __device__ __forceinline__ void c_mixture_sample(Pcg& rng, const Lobe& L, int la
 
 }  // namespace
 
-__global__ void __launch_bounds__(kCoopThreads, 2) walk_kernel_coop(WalkArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
+// kResume: finish the walks the lockstep kernel handed off (WalkArgs::spill)
+// instead of starting fresh ones
+template <bool kResume>
+__device__ __forceinline__ void walk_coop_body(const WalkArgs& a, unsigned char* smem) {
   CoopW& W = *reinterpret_cast<CoopW*>(smem);
   float* hbuf = reinterpret_cast<float*>(smem + al16c(sizeof(CoopW))) + 64 * (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -503,6 +505,31 @@ __global__ void __launch_bounds__(kCoopThreads, 2) walk_kernel_coop(WalkArgs a) 
     unsigned long long idx = 0;
     if (lane == 0) idx = atomicAdd(&a.counters[6], 1ull);  // work queue head
     idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (kResume) {
+      if (idx >= a.counters[7]) break;  // handed-off walks (written by the previous launch)
+      if (collect && lane == 0)  // the previous walk's record block ends with it
+        for (int i = 0; i < w.rec_left; ++i) a.recs[w.rec_base + (8 - w.rec_left) + i].flags = 0u;
+      const SpillLane& o = a.spill[idx];
+      w.x = o.x;
+      w.y = o.y;
+      w.nx = o.nx;
+      w.ny = o.ny;
+      w.T = o.T;
+      w.acc = o.acc;
+      w.dacc = o.dacc;
+      w.R = o.R;
+      w.point = o.point;
+      w.rec_base = o.rec_base;
+      w.rng = o.rng;
+      w.seg = o.seg;
+      w.depth = o.depth;
+      w.rec = o.rec;
+      w.round = o.round;
+      w.rec_left = o.rec_left;
+      w.last_rec = o.last_rec;
+      w.on_n = o.on_n != 0;
+      w.rec_ok = o.rec_ok != 0;
+    } else {
     if (static_cast<int64_t>(idx) >= total) break;
     w.round = static_cast<int>(static_cast<int64_t>(idx) / a.n_points);
     w.point = static_cast<int64_t>(idx) - static_cast<int64_t>(w.round) * a.n_points;
@@ -521,8 +548,10 @@ __global__ void __launch_bounds__(kCoopThreads, 2) walk_kernel_coop(WalkArgs a) 
     w.last_rec = -1;
     w.dacc = 0.0;
     ++walks_done;
+    }
 
-    while (c_begin(w, a, s, ss, collect, lane)) {
+    // a handed-off walk enters at its direction step (begin_step done)
+    for (bool go = kResume || c_begin(w, a, s, ss, collect, lane); go; go = c_begin(w, a, s, ss, collect, lane)) {
       // field evaluation and Table-1 decode
       float xin[16];
       c_gather(f, w.x, w.y, xin);
@@ -626,7 +655,17 @@ __global__ void __launch_bounds__(kCoopThreads, 2) walk_kernel_coop(WalkArgs a) 
   }
   if (collect && lane == 0)
     for (int i = 0; i < w.rec_left; ++i) a.recs[w.rec_base + (8 - w.rec_left) + i].flags = 0u;
-  if (lane == 0) atomicAdd(&a.counters[2], walks_done);
+  if (lane == 0 && walks_done) atomicAdd(&a.counters[2], walks_done);
+}
+
+__global__ void __launch_bounds__(kCoopThreads, 2) walk_kernel_coop(WalkArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  walk_coop_body<false>(a, smem);
+}
+
+__global__ void __launch_bounds__(kCoopThreads, 2) walk_kernel_coop_resume(WalkArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  walk_coop_body<true>(a, smem);
 }
 
 int walk_coop_smem(const WalkArgs& a) {
@@ -651,6 +690,20 @@ cudaError_t launch_walks_coop(const WalkArgs& a, int blocks, cudaStream_t st) {
   e = cudaMemsetAsync(a.counters + 6, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   walk_kernel_coop<<<blocks, kCoopThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+// the lockstep kernel's handed-off tail walks (counters[7] of them, at most
+// max_walks): one warp each
+cudaError_t launch_walks_coop_resume(const WalkArgs& a, int max_walks, int sms, cudaStream_t st) {
+  const int smem = walk_coop_smem(a);
+  cudaError_t e = cudaFuncSetAttribute(walk_kernel_coop_resume, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(a.counters + 6, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  const int blocks = std::max(1, std::min((max_walks + kCoopWarps - 1) / kCoopWarps,
+                                          sms * std::max(1, walk_coop_blocks_per_sm(smem))));
+  walk_kernel_coop_resume<<<blocks, kCoopThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -368,6 +368,34 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
     } else {
       active = __syncthreads_count(need);
       if (active == 0) break;
+      // tail handoff (WalkArgs::spill): a few live walks left and no fresh
+      // ones; a warp per walk finishes them with lower step latency
+      if (a.spill_rows > 0 && active <= a.spill_rows && !__syncthreads_or(next < total)) {
+        if (need) {
+          SpillLane& o = a.spill[atomicAdd(&a.counters[7], 1ull)];
+          o.x = w.x;
+          o.y = w.y;
+          o.nx = w.nx;
+          o.ny = w.ny;
+          o.T = w.T;
+          o.acc = w.acc;
+          o.dacc = w.dacc;
+          o.R = w.R;
+          o.point = w.point;
+          o.rec_base = w.rec_base;
+          o.rng = w.rng;
+          o.seg = w.seg;
+          o.depth = w.depth;
+          o.rec = w.rec;
+          o.round = w.round;
+          o.rec_left = w.rec_left;
+          o.last_rec = w.last_rec;
+          o.on_n = w.on_n;
+          o.rec_ok = w.rec_ok;
+          w.rec_left = 0;  // the record block travels with the walk
+        }
+        break;
+      }
     }
     long long t_b = a.phase_prof ? clock64() : 0;
     if (a.phase_prof && threadIdx.x == 0) {
