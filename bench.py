@@ -459,15 +459,20 @@ def main():
     # --set full capture (profiles/, tools/ncu_counters.py): the walk state
     # lives in registers and the records stay in L2, so DRAM traffic is far
     # below the SoA algorithmic bytes; the kernel is latency-bound
-    ncu_json = os.path.join(ROOT, "profiles", f"ncu_counters_{kname}.json")
-    if os.path.exists(ncu_json):
-        with open(ncu_json) as f:
-            nc = json.load(f)
-        roofline["traffic"] = nc.get("dram_bytes")
-        roofline["traffic_source"] = os.path.relpath(ncu_json, ROOT)
-        roofline["l2_bytes_per_launch"] = nc.get("l2_bytes")
-        roofline["l2_gbs_achieved"] = nc.get("l2_gbs")
-        roofline["tensor_pipe_active_pct"] = nc.get("tensor_pipe_active_pct")
+    # (walk phase = lockstep kernel + tail resume kernel: bytes summed)
+    names = [kname] + (["walk_kernel_coop_resume"] if args.mlp == "tensor" else [])
+    files = [os.path.join(ROOT, "profiles", f"ncu_counters_{k}.json") for k in names]
+    files = [f for f in files if os.path.exists(f)]
+    if files:
+        ncs = []
+        for fn in files:
+            with open(fn) as f:
+                ncs.append(json.load(f))
+        roofline["traffic"] = sum(nc.get("dram_bytes") or 0 for nc in ncs)
+        roofline["traffic_source"] = " + ".join(os.path.relpath(fn, ROOT) for fn in files)
+        roofline["l2_bytes_per_launch"] = sum(nc.get("l2_bytes") or 0 for nc in ncs)
+        roofline["l2_gbs_achieved"] = ncs[0].get("l2_gbs")
+        roofline["tensor_pipe_active_pct"] = ncs[0].get("tensor_pipe_active_pct")
 
     # e2e through the public API with host buffers (points in, statistics out)
     e2e_times = []

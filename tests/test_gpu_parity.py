@@ -2,6 +2,7 @@
 same inputs. Geometry, field evaluation, normalisation and per-walk estimates
 are compared bit for bit or with the tolerance stated in each test."""
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -425,3 +426,44 @@ def test_wavefront_2d_matches_lockstep_statistically(gpu, monkeypatch):
     z = (a["mean"][ok] - b["mean"][ok]) / se[ok]
     assert np.abs(z).max() < 4.5
     assert abs(z.mean()) < 4.0 / np.sqrt(ok.sum())
+
+
+_SPILL_SCRIPT = r"""
+import json, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np
+from paper_2410_18944_b200 import abi, api
+from paper_2410_18944_b200.scene import cell_centers, make_preset, relmse
+p = make_preset("neumann-strip-vlin")
+pts = cell_centers(64, 64, p.eval_bbox)
+truth = np.array([p.analytic(x, y) for x, y in pts])
+f = api.GuidingField(abi.field_config(), p.scene.bbox, 3)
+s = api.Solver(api.Accel(p.scene), f, abi.solver_config("learnable_mis"), api.MLP_TENSOR)
+s.set_points(pts)
+s.run(3, 64, 64, abi.train_config(seed=3))
+pr = s.run_profile()
+print(json.dumps({"relmse": relmse(s.stats()["mean"], truth), "steps": pr["steps"],
+                  "train_steps": pr["train_steps"], "walks": pr["walks"]}))
+"""
+
+
+@pytest.mark.parametrize("rows", ["0", "128"])
+def test_tail_handoff_records_and_estimate(gpu, rows):
+    """Lockstep-kernel tail handoff (WalkArgs::spill, walk_kernel_coop_resume):
+    with WOSTGPU_SPILL_ROWS=128 every walk moves to the warp-per-walk kernel
+    after its first begin_step, mid-step, record block included. Every walk
+    step still leaves exactly one training record (train_steps == steps), and
+    the 64-round guided estimate is as accurate as with the handoff off."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WOSTGPU_SPILL_ROWS=rows)
+    out = subprocess.run([sys.executable, "-c", _SPILL_SCRIPT, root], env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["walks"] == 64 * 64 * 64
+    assert d["train_steps"] == d["steps"] > 0
+    # 64 wpp guided on the strip: relMSE ~0.01 (uniform ~0.066)
+    assert d["relmse"] < 0.025, d
