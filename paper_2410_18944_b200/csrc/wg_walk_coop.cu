@@ -701,8 +701,9 @@ cudaError_t launch_walks_coop_resume(const WalkArgs& a, int max_walks, int sms, 
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(a.counters + 6, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
-  const int blocks = std::max(1, std::min((max_walks + kCoopWarps - 1) / kCoopWarps,
-                                          sms * std::max(1, walk_coop_blocks_per_sm(smem))));
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk_kernel_coop_resume, kCoopThreads, smem);
+  const int blocks = std::max(1, std::min((max_walks + kCoopWarps - 1) / kCoopWarps, sms * std::max(1, per_sm)));
   walk_kernel_coop_resume<<<blocks, kCoopThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
