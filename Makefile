@@ -11,7 +11,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 \
            --expt-relaxed-constexpr -Xptxas -warn-spills
 PKG := paper_2410_18944_b200
 SRC := $(wildcard $(PKG)/csrc/*.cu)
-HDR := $(wildcard $(PKG)/csrc/*.cuh) include/wostgpu.h include/wostgpu_types.h
+HDR := $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.hpp) include/wostgpu.h include/wostgpu3.h include/wostgpu_types.h
 OBJ := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))
 
 all: $(PKG)/libwostgpu.so oracle
@@ -25,7 +25,7 @@ build/%.o: $(PKG)/csrc/%.cu $(HDR)
 	$(NVCC) $(NVFLAGS) $(if $(filter $*,$(FAST_TUS)),-fmad=true,-fmad=false) -c $< -o $@
 
 $(PKG)/libwostgpu.so: $(OBJ)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart -ldl
+	$(NVCC) $(ARCH) -shared -Xlinker --no-undefined -o $@ $(OBJ) -lcudart -ldl
 
 oracle:
 	$(MAKE) -C oracle all

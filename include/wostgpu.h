@@ -147,8 +147,10 @@ int wostgpu_solver_counters(wg_solver solver, int64_t* walks, int64_t* steps, in
 /* train_batch on the records of the last collecting round
  * (proj/src/guide_train.cpp:94-198): filter pdf_mis < floor, random subset
  * of at most max_records_per_round, minibatch Adam. With a communicator
- * attached, gradient sums are allreduced over NVLink before every Adam step
- * and max_records_per_round is per rank. */
+ * attached the round is the single-GPU round over the union of the ranks'
+ * records: the usable count is allreduced before the selection (so the cap
+ * and the minibatch size are GLOBAL, guide_train.cpp:111-116,128) and the
+ * gradient sums before every Adam step; every rank takes the same step. */
 int wostgpu_train_round(wg_solver solver, const wg_train_config* cfg, uint64_t round,
                         wg_train_stats* stats);
 /* drop-in train_batch(field, records, cfg, round) with host records */
@@ -158,6 +160,27 @@ int wostgpu_train_batch(wg_solver solver, const wg_guide_record* records, int64_
  * (the inner loop of train_batch, guide_train.cpp:146-171) */
 int wostgpu_field_grad(wg_solver solver, const wg_guide_record* records, int64_t n,
                        const wg_train_config* cfg, double* grad);
+
+/* Split-phase training round for callers that reduce across ranks with
+ * their own collectives (MPI, gloo, ...). Steps and semantics are those of
+ * wostgpu_train_round's device pipeline with the two NCCL allreduces
+ * replaced by the caller's sums:
+ *   train_prepare        targets, validity; this rank's usable record count
+ *                        (records with pdf_mis >= cfg->pdf_floor)
+ *   train_select         the training set from the GLOBAL usable count (sum
+ *                        over ranks); *n_minibatches = ceil(cap / minibatch)
+ *   train_minibatch_grad this rank's gradient sum of minibatch b:
+ *                        grad_sum[n_params + 1], each record pre-scaled by
+ *                        1 / cfg->minibatch, grad_sum[n_params] = record count
+ *   train_apply          one Adam step (guide_field.cpp:317-331) on the
+ *                        summed buffer: mean = sum * minibatch / count; no step
+ *                        when the count is 0 */
+int wostgpu_train_prepare(wg_solver solver, const wg_train_config* cfg, int64_t* usable_local);
+int wostgpu_train_select(wg_solver solver, const wg_train_config* cfg, int64_t usable_global,
+                         int32_t* n_minibatches);
+int wostgpu_train_minibatch_grad(wg_solver solver, const wg_train_config* cfg, int32_t b,
+                                 float* grad_sum);
+int wostgpu_train_apply(wg_solver solver, const wg_train_config* cfg, const float* grad_sum);
 
 /* The Engine loop (proj/src/solver.cpp:92-104, 136-146) natively: for b in
  * [0, wpp): solve round b over the solver's points (collecting records while

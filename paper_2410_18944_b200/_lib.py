@@ -73,6 +73,10 @@ _SIGS = {
     "wostgpu_train_batch": (C.c_int, [VP, VP, C.c_int64, C.POINTER(abi.TrainConfig), C.c_uint64,
                                       C.POINTER(abi.TrainStats)]),
     "wostgpu_field_grad": (C.c_int, [VP, VP, C.c_int64, C.POINTER(abi.TrainConfig), D]),
+    "wostgpu_train_prepare": (C.c_int, [VP, C.POINTER(abi.TrainConfig), I64]),
+    "wostgpu_train_select": (C.c_int, [VP, C.POINTER(abi.TrainConfig), C.c_int64, I32]),
+    "wostgpu_train_minibatch_grad": (C.c_int, [VP, C.POINTER(abi.TrainConfig), C.c_int32, F32]),
+    "wostgpu_train_apply": (C.c_int, [VP, C.POINTER(abi.TrainConfig), F32]),
     "wostgpu_run": (C.c_int, [VP, C.c_uint64, C.c_int32, C.c_int64, C.POINTER(abi.TrainConfig),
                               C.POINTER(abi.TrainStats), D]),
     "wostgpu_run_profile": (C.c_int, [VP, D, D, I64, I64, I64, I64]),

@@ -336,6 +336,36 @@ class Solver:
                                          C.byref(cfg), _d(g)))
         return g
 
+    # split-phase training round (wostgpu.h): the library's NCCL round with
+    # the two allreduces (usable count, gradient sums) done by the caller
+    def train_prepare(self, cfg: abi.TrainConfig):
+        """Targets and validity of the last collecting round's records; returns
+        this rank's usable record count."""
+        u = C.c_int64()
+        check(load().wostgpu_train_prepare(self.h, C.byref(cfg), C.byref(u)))
+        return u.value
+
+    def train_select(self, cfg: abi.TrainConfig, usable_global):
+        """The round's training set from the global usable count; returns the
+        number of minibatches."""
+        nmb = C.c_int32()
+        check(load().wostgpu_train_select(self.h, C.byref(cfg), int(usable_global), C.byref(nmb)))
+        return nmb.value
+
+    def train_minibatch_grad(self, cfg: abi.TrainConfig, b):
+        """This rank's gradient sum of minibatch b (records pre-scaled by
+        1 / minibatch); the last entry is the record count."""
+        g = np.zeros(self.field.n_params + 1, dtype=np.float32)
+        check(load().wostgpu_train_minibatch_grad(self.h, C.byref(cfg), b,
+                                                   g.ctypes.data_as(C.POINTER(C.c_float))))
+        return g
+
+    def train_apply(self, cfg: abi.TrainConfig, grad_sum):
+        """One Adam step on a (globally summed) train_minibatch_grad buffer."""
+        g = np.ascontiguousarray(grad_sum, dtype=np.float32)
+        assert g.shape == (self.field.n_params + 1,)
+        check(load().wostgpu_train_apply(self.h, C.byref(cfg), g.ctypes.data_as(C.POINTER(C.c_float))))
+
     def run(self, seed, wpp, train_until=256, train_cfg: abi.TrainConfig | None = None):
         """Engine loop natively (wostgpu_run): returns (TrainStats, device ms)."""
         st = abi.TrainStats()

@@ -646,6 +646,14 @@ void enqueue3_train(wg_solver3_s* s, const wg_train_config& tc, bool from_walks)
   Ev3& e = events()[s];
   CK(cudaEventRecord(ev_next(e.train, e.nt), s->st));
   enqueue3_finalize(s, tc.pdf_floor, from_walks);
+  // selection rate from the usable count summed over the ranks (wg_train.cu
+  // compact_kernel): the cap and minibatch size are global
+  wg::TrainCtl* c = s->ctl.as<wg::TrainCtl>();
+  if (s->comm)
+    NCK(nccl().allReduce(&c->usable, &c->usable_global, 1, ncclUint64, ncclSum, s->comm, s->st));
+  else
+    CK(cudaMemcpyAsync(&c->usable_global, &c->usable, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+                       s->st));
   CKL(wg::launch_compact(reinterpret_cast<const DevRecord*>(s->recs.p),
                          s->rec_counter.as<unsigned long long>(), s->rec_cap,
                          s->ctl.as<wg::TrainCtl>(), s->totals.as<wg::TrainTotals>(),

@@ -374,21 +374,61 @@ void enqueue_minibatch(wg_solver_s* s, const wg_train_config& tc, int b, double 
   else CKL(launch_grad_cuda_core(ta, s->stream));
 }
 
-// train_batch on the arena's records (guide_train.cpp:94-198), enqueued only
-void enqueue_train(wg_solver_s* s, const wg_train_config& tc) {
-  wg_field_s* f = s->field;
-  need(f != nullptr, WG_ERR_INVALID, "training needs a guiding field");
-  need(default_shape(f->view), WG_ERR_NOT_BUILT,
+void check_trainable(wg_solver_s* s) {
+  need(s->field != nullptr, WG_ERR_INVALID, "training needs a guiding field");
+  need(default_shape(s->field->view), WG_ERR_NOT_BUILT,
        "device training is built for the default field shape (L=4, F=4, hidden 64, K=8, 2D)");
-  ensure_train_buffers(s, tc);
-  CK(cudaEventRecord(pool_event(s->ev_train, s->n_train_ev), s->stream));
-  enqueue_finalize(s, tc.pdf_floor);
+}
+
+// The selection rate of a round comes from the usable-record count summed
+// over the ranks: one 8-byte NCCL allreduce on the solver
+// stream, or the host-supplied global count of the split-phase API.
+void enqueue_usable_global(wg_solver_s* s, const int64_t* host_global) {
+  TrainCtl* c = s->ctl.as<TrainCtl>();
+  if (host_global) {
+    static_assert(sizeof(unsigned long long) == sizeof(int64_t), "count width");
+    CK(cudaMemcpyAsync(&c->usable_global, host_global, sizeof(int64_t), cudaMemcpyHostToDevice,
+                       s->stream));
+    CK(cudaStreamSynchronize(s->stream));  // the host value is borrowed for the call only
+  } else if (s->comm) {
+    NCK(nccl().allReduce(&c->usable, &c->usable_global, 1, ncclUint64, ncclSum, s->comm, s->stream));
+  } else {
+    CK(cudaMemcpyAsync(&c->usable_global, &c->usable, sizeof(unsigned long long),
+                       cudaMemcpyDeviceToDevice, s->stream));
+  }
+}
+
+void enqueue_select(wg_solver_s* s, const wg_train_config& tc) {
   CKL(launch_compact(s->recs.as<DevRecord>(), s->rec_counter.as<unsigned long long>(),
                      s->rec_capacity, s->ctl.as<TrainCtl>(), s->totals.as<TrainTotals>(),
                      s->lists.as<uint32_t>(), s->list_cap, tc.max_records_per_round, tc.minibatch,
                      s->stream));
-  const int n_mb = static_cast<int>((tc.max_records_per_round + tc.minibatch - 1) / tc.minibatch);
-  AdamCtl* actl = f->adam.as<AdamCtl>();
+}
+
+int n_minibatches(const wg_train_config& tc) {
+  return static_cast<int>((tc.max_records_per_round + tc.minibatch - 1) / tc.minibatch);
+}
+
+// Adam on the (globally reduced) gradient buffer; no step when its record
+// count slot is 0
+void enqueue_adam(wg_solver_s* s, const wg_train_config& tc) {
+  wg_field_s* f = s->field;
+  CKL(launch_adam(f->p.as<float>(), f->m.as<double>(), f->v.as<double>(), s->grad.as<float>(),
+                  f->n_params, tc.lr, tc.beta1, tc.beta2, tc.eps,
+                  static_cast<double>(tc.minibatch), f->adam.as<AdamCtl>(), f->view,
+                  f->wpack.p && !f->pack_dirty ? f->wpack.as<unsigned char>() : nullptr, s->stream));
+}
+
+// train_batch on the arena's records (guide_train.cpp:94-198), enqueued only
+void enqueue_train(wg_solver_s* s, const wg_train_config& tc) {
+  check_trainable(s);
+  wg_field_s* f = s->field;
+  ensure_train_buffers(s, tc);
+  CK(cudaEventRecord(pool_event(s->ev_train, s->n_train_ev), s->stream));
+  enqueue_finalize(s, tc.pdf_floor);
+  enqueue_usable_global(s, nullptr);
+  enqueue_select(s, tc);
+  const int n_mb = n_minibatches(tc);
   for (int b = 0; b < n_mb; ++b) {
     // records enter the fp32 gradient sum pre-scaled by 1 / minibatch (the
     // same constant on every rank); Adam divides by count / minibatch
@@ -396,10 +436,7 @@ void enqueue_train(wg_solver_s* s, const wg_train_config& tc) {
     if (s->comm)
       NCK(nccl().allReduce(s->grad.p, s->grad.p, f->n_params + 1, ncclFloat, ncclSum, s->comm,
                         s->stream));
-    CKL(launch_adam(f->p.as<float>(), f->m.as<double>(), f->v.as<double>(), s->grad.as<float>(),
-                    f->n_params, tc.lr, tc.beta1, tc.beta2, tc.eps,
-                    static_cast<double>(tc.minibatch), actl, f->view,
-                    f->wpack.p && !f->pack_dirty ? f->wpack.as<unsigned char>() : nullptr, s->stream));
+    enqueue_adam(s, tc);
   }
   CK(cudaEventRecord(pool_event(s->ev_train, s->n_train_ev), s->stream));
 }
@@ -761,11 +798,69 @@ int wostgpu_comm_unique_id(char id[128]) {
 
 int wostgpu_solver_attach_comm(wg_solver s, const char id[128], int32_t nranks, int32_t rank) {
   return guarded([&] {
+    need(nranks >= 1 && rank >= 0 && rank < nranks, WG_ERR_INVALID, "bad rank / nranks");
+    if (s->comm) {  // re-attach: release the previous communicator
+      CK(cudaStreamSynchronize(s->stream));
+      nccl().commDestroy(s->comm);
+      s->comm = nullptr;
+    }
     ncclUniqueId u;
     std::memcpy(&u, id, 128);
     NCK(nccl().commInitRank(&s->comm, nranks, u, rank));
     s->nranks = nranks;
     s->rank = rank;
+  });
+}
+
+int wostgpu_train_prepare(wg_solver s, const wg_train_config* cfg, int64_t* usable_local) {
+  return guarded([&] {
+    need(s->have_records && s->recs_from_walks, WG_ERR_INVALID, "train_prepare needs a collecting round");
+    check_trainable(s);
+    reset_run(s);
+    ensure_train_buffers(s, *cfg);
+    enqueue_finalize(s, cfg->pdf_floor);
+    unsigned long long u = 0;
+    CK(cudaMemcpyAsync(&u, &s->ctl.as<TrainCtl>()->usable, sizeof(u), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    if (usable_local) *usable_local = static_cast<int64_t>(u);
+  });
+}
+
+int wostgpu_train_select(wg_solver s, const wg_train_config* cfg, int64_t usable_global,
+                         int32_t* n_mb) {
+  return guarded([&] {
+    need(s->have_records, WG_ERR_INVALID, "train_select needs prepared records");
+    need(usable_global >= 0, WG_ERR_INVALID, "usable_global must be >= 0");
+    check_trainable(s);
+    ensure_train_buffers(s, *cfg);
+    enqueue_usable_global(s, &usable_global);
+    enqueue_select(s, *cfg);
+    CK(cudaStreamSynchronize(s->stream));
+    if (n_mb) *n_mb = n_minibatches(*cfg);
+  });
+}
+
+int wostgpu_train_minibatch_grad(wg_solver s, const wg_train_config* cfg, int32_t b, float* grad_sum) {
+  return guarded([&] {
+    need(s->have_records, WG_ERR_INVALID, "train_minibatch_grad needs selected records");
+    need(b >= 0 && b < n_minibatches(*cfg), WG_ERR_INVALID, "minibatch index out of range");
+    check_trainable(s);
+    ensure_train_buffers(s, *cfg);
+    enqueue_minibatch(s, *cfg, b, 1.0 / static_cast<double>(cfg->minibatch));
+    CK(cudaMemcpyAsync(grad_sum, s->grad.p, sizeof(float) * (s->field->n_params + 1),
+                       cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int wostgpu_train_apply(wg_solver s, const wg_train_config* cfg, const float* grad_sum) {
+  return guarded([&] {
+    check_trainable(s);
+    ensure_train_buffers(s, *cfg);
+    CK(cudaMemcpyAsync(s->grad.p, grad_sum, sizeof(float) * (s->field->n_params + 1),
+                       cudaMemcpyHostToDevice, s->stream));
+    enqueue_adam(s, *cfg);
+    CK(cudaStreamSynchronize(s->stream));
   });
 }
 

@@ -26,12 +26,16 @@ namespace wg {
 // u = key / 2^64) and assigned to minibatch floor(u / p * n_mb); i.e. a
 // uniformly random subset of expected size min(usable, cap) in random
 // minibatches, without a sort. Device-only: the host never waits.
+// `usable` is the GLOBAL count (summed over the ranks before this launch)
+// and keys depend only on (seed, round, global point, depth), so the union
+// of the ranks' selections is exactly the single-GPU selection: the cap and
+// the minibatch size are global, as in the reference's one-process loop.
 __global__ void compact_kernel(const DevRecord* recs, const unsigned long long* rec_count,
                                int64_t capacity, TrainCtl* ctl, TrainTotals* totals,
                                uint32_t* lists, int64_t list_cap, int64_t max_records,
                                int32_t minibatch) {
   const int64_t n = static_cast<int64_t>(min(*rec_count, static_cast<unsigned long long>(capacity)));
-  const double usable = static_cast<double>(ctl->usable);
+  const double usable = static_cast<double>(ctl->usable_global);
   const double take = fmin(usable, static_cast<double>(max_records));
   const int n_mb = take > 0.0 ? min(kMaxMinibatches, static_cast<int>(ceil(take / minibatch))) : 0;
   const double p = usable > 0.0 ? fmin(1.0, static_cast<double>(max_records) / usable) : 0.0;

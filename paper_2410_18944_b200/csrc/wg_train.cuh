@@ -18,7 +18,8 @@ constexpr int kNormRing = 4096;
 
 // per-solver, reset at the start of every collecting round
 struct TrainCtl {
-  unsigned long long seen, usable, low_pdf;  // filled at backfill
+  unsigned long long seen, usable, low_pdf;  // this rank's records, filled at backfill
+  unsigned long long usable_global;          // usable summed over the ranks (selection rate)
   unsigned long long mb_count[kMaxMinibatches];
   unsigned long long overflow;
 };

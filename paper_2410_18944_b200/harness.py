@@ -143,9 +143,9 @@ class Problem:
 
 def load_problem(cfg: RunConfig) -> Problem:
     """load_problem (solver.cpp): a preset, or a scene JSON file (scene_io.py)."""
-    if bool(cfg.scene_path) == bool(cfg.preset):
-        raise ValueError("run config: set exactly one of 'scene' and 'preset'")
-    if cfg.preset:
+    if not cfg.scene_path and not cfg.preset:
+        raise ValueError("run config needs a 'preset' or a 'scene'")
+    if cfg.preset:  # the preset wins when both are set (solver.cpp:30-41)
         p = make_preset(cfg.preset)
         return Problem(p.scene, p.analytic, p.eval_bbox)
     from .scene_io import load_scene_file
@@ -317,6 +317,12 @@ class Engine:
         self.solver = api.Solver(self.accel, self.field, cfg.solver_config(), cfg.mlp)
         self.solver.set_points(points)
         self.train_totals = abi.TrainStats()
+        # tcfg (solver.cpp:84-87): reflection follows the solver, the
+        # selection loss trains only under learnable MIS, seed = run seed
+        self.tcfg = abi.TrainConfig.from_buffer_copy(cfg.train)
+        self.tcfg.reflect = int(cfg.reflect)
+        self.tcfg.learn_selection = int(cfg.mode == "learnable_mis")
+        self.tcfg.seed = cfg.seed
 
     def run_batch(self, rnd: int):
         """Engine::run_batch (solver.cpp:92-104): one walk per point, then
@@ -324,7 +330,7 @@ class Engine:
         training = self.guided and rnd < self.cfg.train_until
         self.solver.solve_rounds(self.cfg.seed, rnd, 1, collect=training)
         if training:
-            st = self.solver.train_round(self.cfg.train, rnd)
+            st = self.solver.train_round(self.tcfg, rnd)
             for k in ("records_seen", "records_consumed", "skipped_low_pdf", "skipped_low_v", "steps"):
                 setattr(self.train_totals, k, getattr(self.train_totals, k) + getattr(st, k))
             self.train_totals.seconds += st.seconds
