@@ -153,7 +153,11 @@ int wostgpu_solver_counters(wg_solver solver, int64_t* walks, int64_t* steps, in
  * gradient sums before every Adam step; every rank takes the same step. */
 int wostgpu_train_round(wg_solver solver, const wg_train_config* cfg, uint64_t round,
                         wg_train_stats* stats);
-/* drop-in train_batch(field, records, cfg, round) with host records */
+/* drop-in train_batch(field, records, cfg, round) with host records
+ * (proj/src/guide_train.cpp:94-198, declared proj/include/wost/guide_train.hpp:104-105):
+ * the reference's own selection (Fisher-Yates order from the round's PCG32
+ * stream, cap, consecutive minibatches), so seen / consumed / skipped / steps
+ * equal the reference's on the same records; gradients on the device */
 int wostgpu_train_batch(wg_solver solver, const wg_guide_record* records, int64_t n,
                         const wg_train_config* cfg, uint64_t round, wg_train_stats* stats);
 /* mean gradient of one minibatch made of `records` in order, fp64 out

@@ -340,6 +340,13 @@ void* ref_field_load(const char* path) {
   return rc == WG_OK ? f : nullptr;
 }
 int64_t ref_field_adam_steps(void* fp) { return static_cast<GuidingField*>(fp)->adam_steps(); }
+// GuidingField::adam_step (proj/src/guide_field.cpp:317-331) on a given
+// gradient (which the reference zeroes on return)
+void ref_field_adam_step(void* fp, const double* grad, double lr, double beta1, double beta2, double eps) {
+  auto* f = static_cast<GuidingField*>(fp);
+  std::vector<double> g(grad, grad + f->param_count());
+  f->adam_step(g, lr, beta1, beta2, eps);
+}
 
 // result formats through the reference's own writers (proj/src/image.cpp,
 // solver.cpp:317-327) for byte-level comparison with the Python harness

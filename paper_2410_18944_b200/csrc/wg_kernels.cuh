@@ -139,13 +139,9 @@ cudaError_t launch_walks_g8(const WalkArgs& a, int blocks, cudaStream_t st);
 int walk_tc_smem(const WalkArgs& a);
 int walk_tc_blocks_per_sm(int smem);
 int walk_tc_block();
-int walk_tc_warps();
 cudaError_t launch_walks_tc(const WalkArgs& a, int blocks, cudaStream_t st);
 // warp-per-walk guided kernel for the default field shape (wg_walk_coop.cu)
 int walk_coop_smem(const WalkArgs& a);
-int walk_coop_block();
-int walk_coop_blocks_per_sm(int smem);
-cudaError_t launch_walks_coop(const WalkArgs& a, int blocks, cudaStream_t st);
 cudaError_t launch_walks_coop_resume(const WalkArgs& a, int max_walks, int sms, cudaStream_t st);
 // wavefront pair for guided 2D walks on the tensor cores (wg_wave2.cu)
 void wave2_sizes(size_t* lane_bytes, size_t* dir_bytes);

@@ -175,186 +175,6 @@ __device__ __forceinline__ void tc_issue(unsigned char* sm, uint32_t tmem_d, uin
   umma::commit(reinterpret_cast<uint64_t*>(sm + L::BAR));
 }
 
-// ---------------------------------------------------------------------------
-// Warp-independent variant: the 4 warps of a CTA each run their own MLP chain.
-// All warps share one 128-row A tile (warp w writes rows 32w..32w+31) and the
-// weights; warp w issues M = 128 MMAs into ITS OWN 64 TMEM columns, so rows
-// 32w..32w+31 of its result land exactly in the TMEM lanes warp w may read
-// (the other 96 rows are recomputed neighbours' data and ignored). No CTA
-// barrier inside the step loop: __syncwarp + proxy fence + a per-warp mbarrier.
-struct TcLayoutW {
-  static constexpr int M = 128, NIN = 16, NH = 64, NO = 33, NO_PAD = 48;
-  static constexpr uint32_t X_HI = 0;                      // 128 x 16
-  static constexpr uint32_t X_LO = X_HI + M * NIN * 2;
-  static constexpr uint32_t H_HI = X_LO + M * NIN * 2;     // 128 x 64
-  static constexpr uint32_t H_LO = H_HI + M * NH * 2;
-  static constexpr uint32_t B1_HI = H_LO + M * NH * 2;
-  static constexpr uint32_t B1_LO = B1_HI + NH * NIN * 2;
-  static constexpr uint32_t B2_HI = B1_LO + NH * NIN * 2;
-  static constexpr uint32_t B2_LO = B2_HI + NH * NH * 2;
-  static constexpr uint32_t B3_HI = B2_LO + NH * NH * 2;
-  static constexpr uint32_t B3_LO = B3_HI + NO_PAD * NH * 2;
-  static constexpr uint32_t BIAS = B3_LO + NO_PAD * NH * 2;
-  static constexpr uint32_t BAR = BIAS + (NH + NH + NO_PAD) * 4;  // 4 mbarriers
-  static constexpr uint32_t TMEM_SLOT = BAR + 32;
-  static constexpr uint32_t BYTES = TMEM_SLOT + 16;
-  // TMEM: 64 columns per warp (tcw_cols)
-};
-
-// 1, 2 or 4 warps per CTA -> 64, 128, 256 columns (a power of two >= 32)
-__device__ __forceinline__ uint32_t tcw_cols() { return 64u * (blockDim.x >> 5); }
-
-__device__ __forceinline__ void tcw_stage_weights(unsigned char* sm, const FieldView& f) {
-  using L = TcLayoutW;
-  const float* p = f.p;
-  auto put = [&](uint32_t hi_off, uint32_t lo_off, int n, int k, int K, float v) {
-    __half h, l;
-    umma::split_f16(v, h, l);
-    uint32_t o = umma::kmajor_off(n, k, K);
-    *reinterpret_cast<__half*>(sm + hi_off + o) = h;
-    *reinterpret_cast<__half*>(sm + lo_off + o) = l;
-  };
-  for (int e = threadIdx.x; e < L::NH * L::NIN; e += blockDim.x) {
-    int n = e % L::NH, k = e / L::NH;
-    put(L::B1_HI, L::B1_LO, n, k, L::NIN, p[f.w1 + k * L::NH + n]);
-  }
-  for (int e = threadIdx.x; e < L::NH * L::NH; e += blockDim.x) {
-    int n = e % L::NH, k = e / L::NH;
-    put(L::B2_HI, L::B2_LO, n, k, L::NH, p[f.w2 + k * L::NH + n]);
-  }
-  for (int e = threadIdx.x; e < L::NO_PAD * L::NH; e += blockDim.x) {
-    int n = e % L::NO_PAD, k = e / L::NO_PAD;
-    put(L::B3_HI, L::B3_LO, n, k, L::NH, n < L::NO ? p[f.w3 + k * L::NO + n] : 0.0f);
-  }
-  float* bias = reinterpret_cast<float*>(sm + L::BIAS);
-  for (int i = threadIdx.x; i < L::NH; i += blockDim.x) {
-    bias[i] = p[f.b1 + i];
-    bias[L::NH + i] = p[f.b2 + i];
-  }
-  for (int i = threadIdx.x; i < L::NO_PAD; i += blockDim.x)
-    bias[2 * L::NH + i] = i < L::NO ? p[f.b3 + i] : 0.0f;
-  if (threadIdx.x < 32)
-    umma::tmem_alloc(reinterpret_cast<uint32_t*>(sm + L::TMEM_SLOT), tcw_cols());
-  if (threadIdx.x < 4) umma::mbar_init(reinterpret_cast<uint64_t*>(sm + L::BAR) + threadIdx.x, 1);
-  umma::fence_async_smem();
-}
-
-__device__ __forceinline__ void tcw_teardown(unsigned char* sm) {
-  using L = TcLayoutW;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    umma::fence_after();
-    umma::tmem_dealloc(*reinterpret_cast<uint32_t*>(sm + L::TMEM_SLOT), tcw_cols());
-  }
-}
-
-template <int K>
-__device__ __forceinline__ void tcw_put_row(unsigned char* sm, uint32_t hi_off, uint32_t lo_off, int row,
-                                            const float* v) {
-#pragma unroll
-  for (int c = 0; c < K / 8; ++c) {
-    __half2 hi[4], lo[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float2 x = make_float2(v[8 * c + 2 * i], v[8 * c + 2 * i + 1]);
-      hi[i] = __float22half2_rn(x);
-      float2 b = __half22float2(hi[i]);
-      lo[i] = __float22half2_rn(make_float2(x.x - b.x, x.y - b.y));
-    }
-    uint32_t o = umma::kmajor_off(row, 8 * c, K);
-    *reinterpret_cast<uint4*>(sm + hi_off + o) = *reinterpret_cast<uint4*>(hi);
-    *reinterpret_cast<uint4*>(sm + lo_off + o) = *reinterpret_cast<uint4*>(lo);
-  }
-}
-
-// one layer for the calling warp: lane 0 issues K/16 x 3 MMAs, the warp waits
-template <int K, int N>
-__device__ __forceinline__ void tcw_layer(unsigned char* sm, uint32_t a_hi, uint32_t a_lo, uint32_t b_hi,
-                                          uint32_t b_lo, uint32_t tmem_d, uint64_t* bar, uint32_t& phase,
-                                          long long* mma_cyc) {
-  umma::fence_async_smem();
-  umma::fence_before();
-  __syncwarp();
-  long long t0 = mma_cyc ? clock64() : 0;
-  if ((threadIdx.x & 31) == 0) {
-    umma::fence_after();
-    const uint32_t base = umma::smem_u32(sm);
-    constexpr uint32_t idesc = umma::idesc_f16(128, N);
-#pragma unroll
-    for (int kb = 0; kb < K / 16; ++kb) {
-      const uint32_t ko = kb * 256;
-      uint64_t ahi = umma::desc_kmajor(base + a_hi + ko, K), alo = umma::desc_kmajor(base + a_lo + ko, K);
-      uint64_t bhi = umma::desc_kmajor(base + b_hi + ko, K), blo = umma::desc_kmajor(base + b_lo + ko, K);
-      umma::mma_f16(tmem_d, ahi, bhi, idesc, kb > 0 ? 1u : 0u);
-      umma::mma_f16(tmem_d, alo, bhi, idesc, 1u);
-      umma::mma_f16(tmem_d, ahi, blo, idesc, 1u);
-    }
-    umma::commit(bar);
-  }
-  __syncwarp();
-  umma::mbar_wait(bar, phase);
-  phase ^= 1u;
-  umma::fence_after();
-  if (mma_cyc) *mma_cyc += clock64() - t0;
-}
-
-// MLP forward for the calling warp's 32 rows (thread = row); x: 16 inputs
-// (zeros for idle lanes), out: 33 raw outputs
-__device__ __forceinline__ void tcw_forward(unsigned char* sm, uint32_t& phase, const float* x, float* out,
-                                            long long* mma_cyc = nullptr) {
-  using L = TcLayoutW;
-  const int row = threadIdx.x;
-  const int warp = threadIdx.x >> 5;
-  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(sm + L::TMEM_SLOT);
-  const uint32_t tw = tmem + 64u * warp;                                 // this warp's columns
-  const uint32_t trow = tw + (static_cast<uint32_t>(warp * 32) << 16);  // this warp's lanes
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR) + warp;
-  const float* bias = reinterpret_cast<const float*>(sm + L::BIAS);
-  float v[L::NH];
-  float inv;
-#pragma unroll
-  for (int i = 0; i < L::NIN; ++i) v[i] = x[i];
-  tc_row_scale<L::NIN>(v, inv);
-  tcw_put_row<L::NIN>(sm, L::X_HI, L::X_LO, row, v);
-  tcw_layer<L::NIN, L::NH>(sm, L::X_HI, L::X_LO, L::B1_HI, L::B1_LO, tw, bar, phase, mma_cyc);
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    float a[32];
-    umma::ld_x32(trow + 32 * c, a);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      float h = a[i] * inv + bias[32 * c + i];
-      v[32 * c + i] = h > 0.0f ? h : 0.0f;
-    }
-  }
-  tc_row_scale<L::NH>(v, inv);
-  tcw_put_row<L::NH>(sm, L::H_HI, L::H_LO, row, v);
-  tcw_layer<L::NH, L::NH>(sm, L::H_HI, L::H_LO, L::B2_HI, L::B2_LO, tw, bar, phase, mma_cyc);
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    float a[32];
-    umma::ld_x32(trow + 32 * c, a);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      float h = a[i] * inv + bias[L::NH + 32 * c + i];
-      v[32 * c + i] = h > 0.0f ? h : 0.0f;
-    }
-  }
-  tc_row_scale<L::NH>(v, inv);
-  tcw_put_row<L::NH>(sm, L::H_HI, L::H_LO, row, v);
-  tcw_layer<L::NH, L::NO_PAD>(sm, L::H_HI, L::H_LO, L::B3_HI, L::B3_LO, tw, bar, phase, mma_cyc);
-  {
-    float a[32];
-    umma::ld_x32(trow, a);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) out[i] = a[i] * inv + bias[2 * L::NH + i];
-    float b[16];
-    umma::ld_x16(trow + 32, b);
-    out[32] = b[0] * inv + bias[2 * L::NH + 32];
-  }
-  umma::fence_before();
-}
-
 // Bilinear multi-resolution gather (guide_field.cpp:80-123) for the default
 // shape (4 levels x 4 features): one 16-byte load per lattice corner.
 __device__ __forceinline__ void tc_gather(const FieldView& f, double x, double y, float* in) {

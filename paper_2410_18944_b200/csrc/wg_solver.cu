@@ -192,13 +192,8 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
 
   // guided walks on the default field shape: tcgen05 MLP tile kernel, or the
   // bit-faithful CUDA-core MLP with 8 lanes per walk; otherwise generic
-  static const bool coop_env = [] {
-    const char* e = std::getenv("WOSTGPU_WALK");
-    return e && std::string(e) == "coop";
-  }();
-  const bool coop = dflt && s->mlp == WG_MLP_TENSOR && coop_env;
-  const bool tc = dflt && s->mlp == WG_MLP_TENSOR && !coop;
-  const bool g8 = dflt && !tc && !coop;
+  const bool tc = dflt && s->mlp == WG_MLP_TENSOR;
+  const bool g8 = dflt && !tc;
   int smem = (s->scene->smem_bytes > 0 ? ((s->scene->smem_bytes + 15) & ~15) : 0) +
              (guided ? ((int)sizeof(float) * s->field->view.mlp_count + 15) / 16 * 16 : 0);
   if (g8) smem = walk_g8_smem(a);
@@ -214,13 +209,11 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
     smem = walk_tc_smem(a);
     a.wblob = field_blob(s->field, s->stream);
   }
-  if (coop) smem = walk_coop_smem(a);
-  const int lanes_per_walk = g8 ? 8 : coop ? 32 : 1;
-  const int block = g8 ? 256 : tc ? walk_tc_block() : coop ? walk_coop_block() : 128;
-  const int per_sm = std::max(1, tc     ? walk_tc_blocks_per_sm(smem)
-                                 : coop ? walk_coop_blocks_per_sm(smem)
-                                 : g8   ? walk_g8_blocks_per_sm(smem)
-                                        : walk_blocks_per_sm(dflt, guided && !dflt, smem));
+  const int lanes_per_walk = g8 ? 8 : 1;
+  const int block = g8 ? 256 : tc ? walk_tc_block() : 128;
+  const int per_sm = std::max(1, tc   ? walk_tc_blocks_per_sm(smem)
+                                 : g8 ? walk_g8_blocks_per_sm(smem)
+                                      : walk_blocks_per_sm(dflt, guided && !dflt, smem));
   for (int32_t r0 = 0; r0 < rounds; r0 += chunk) {
     int32_t n = std::min(chunk, rounds - r0);
     a.wpp_first = wpp_first + r0;
@@ -279,7 +272,7 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
       }();
       const int nb = std::max(1, blocks);
       const int spill_want = spill_env >= 0 ? spill_env : s->scene->view.n_segs <= 16 ? 24 : 0;
-      const int spill_rows = walk_tc_warps() == 0 && a.small_mlp ? std::max(0, std::min(spill_want, 128)) : 0;
+      const int spill_rows = a.small_mlp ? std::max(0, std::min(spill_want, 128)) : 0;
       a.spill_rows = spill_rows;
       if (spill_rows > 0) {
         s->spill.alloc(sizeof(SpillLane) * nb * spill_rows);
@@ -309,8 +302,7 @@ void enqueue_rounds(wg_solver_s* s, uint64_t seed, uint64_t wpp_first, int32_t r
                    small_it > 0 ? q[7] / small_it : 0.0);
     }
     if (tc || wave) {
-    } else if (coop) CKL(launch_walks_coop(a, std::max(1, blocks), s->stream));
-    else if (g8) CKL(launch_walks_g8(a, std::max(1, blocks), s->stream));
+    } else if (g8) CKL(launch_walks_g8(a, std::max(1, blocks), s->stream));
     else CKL(launch_walks(a, dflt, guided && !dflt, std::max(1, blocks), s->stream));
     CK(cudaEventRecord(pool_event(s->ev_walk, s->n_walk_ev), s->stream));
     CKL(launch_welford(a.est, a.esc, s->n_points, n, s->stats.as<wg_point_stats>(), s->stream));
@@ -361,13 +353,9 @@ void enqueue_minibatch(wg_solver_s* s, const wg_train_config& tc, int b, double 
   ta.e_fraction = tc.e_fraction;
   ta.v_floor = tc.v_floor;
   ta.totals = s->totals.as<TrainTotals>();
-  // WOSTGPU_GRAD=cuda: CUDA-core fp64-loss gradient tile under tensor-core walks
-  // (experiments separating walk-side and training-side numerics)
-  static const bool force_cuda_grad = [] {
-    const char* e = std::getenv("WOSTGPU_GRAD");
-    return e && std::string(e) == "cuda";
-  }();
-  if (s->mlp == WG_MLP_TENSOR && tc_grad_available() && !force_cuda_grad) {
+  // tensor-core walks train on the tcgen05 gradient tile; the bit-faithful
+  // (MLP_EXACT) path on the CUDA-core fp64-loss tile
+  if (s->mlp == WG_MLP_TENSOR && tc_grad_available()) {
     ta.packed = field_blob(f, s->stream);
     CKL(launch_grad_tc(ta, s->stream));
   }
@@ -679,17 +667,75 @@ int wostgpu_train_round(wg_solver s, const wg_train_config* cfg, uint64_t round,
   });
 }
 
+// train_batch (guide_train.cpp:94-198) on host records with the reference's
+// own selection: usable records (pdf_mis >= floor) in a Fisher-Yates order
+// from Rng(mix(seed) ^ mix(round + 1), round), truncated to the cap, cut
+// into consecutive minibatches; one device gradient + Adam step per
+// minibatch over exactly the records the reference uses. (The device-side
+// rounds select by key thinning instead, wg_train.cu compact_kernel: the
+// host never waits there.)
 int wostgpu_train_batch(wg_solver s, const wg_guide_record* recs, int64_t n,
                         const wg_train_config* cfg, uint64_t round, wg_train_stats* stats) {
-  (void)round;
   return guarded([&] {
-    need(s->field != nullptr, WG_ERR_INVALID, "training needs a guiding field");
-    reset_run(s);
-    long long before = adam_steps(s);
-    import_records(s, recs, n, cfg->pdf_floor);
-    enqueue_train(s, *cfg);
-    wg_train_stats st = sync_collect(s, before);
+    check_trainable(s);
+    need(n >= 0 && (n == 0 || recs != nullptr), WG_ERR_INVALID, "records: null pointer");
+    need(n <= static_cast<int64_t>(UINT32_MAX), WG_ERR_INVALID, "too many records");
+    need(cfg->minibatch >= 1, WG_ERR_INVALID, "minibatch must be >= 1");
+    wg_train_stats st{};
     st.records_seen = n;
+    std::vector<uint32_t> order;
+    order.reserve(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      if (recs[i].pdf_mis < cfg->pdf_floor) ++st.skipped_low_pdf;
+      else order.push_back(static_cast<uint32_t>(i));
+    }
+    Pcg rng;
+    rng.seed(Pcg::mix(cfg->seed) ^ Pcg::mix(round + 1), round);
+    for (size_t i = order.size(); i > 1; --i) {
+      // Rng::uniform_index (rng.hpp:61-73): Lemire's bounded draw
+      const uint32_t m_n = static_cast<uint32_t>(i);
+      uint64_t m = static_cast<uint64_t>(rng.u32()) * m_n;
+      uint32_t lo = static_cast<uint32_t>(m);
+      if (lo < m_n) {
+        const uint32_t t = (0u - m_n) % m_n;
+        while (lo < t) {
+          m = static_cast<uint64_t>(rng.u32()) * m_n;
+          lo = static_cast<uint32_t>(m);
+        }
+      }
+      std::swap(order[i - 1], order[static_cast<size_t>(m >> 32)]);
+    }
+    if (static_cast<int64_t>(order.size()) > cfg->max_records_per_round)
+      order.resize(static_cast<size_t>(cfg->max_records_per_round));
+    if (order.empty()) {
+      s->have_records = false;
+      if (stats) *stats = st;
+      return;
+    }
+    reset_run(s);
+    const long long before = adam_steps(s);
+    import_records(s, recs, n, cfg->pdf_floor);
+    ensure_train_buffers(s, *cfg);
+    CK(cudaEventRecord(pool_event(s->ev_train, s->n_train_ev), s->stream));
+    const int64_t mb = cfg->minibatch;
+    for (int64_t b0 = 0; b0 < static_cast<int64_t>(order.size()); b0 += mb) {
+      const unsigned long long cnt = static_cast<unsigned long long>(
+          std::min<int64_t>(mb, static_cast<int64_t>(order.size()) - b0));
+      // pageable sources: the copies are staged before the calls return
+      CK(cudaMemcpyAsync(s->lists.p, order.data() + b0, sizeof(uint32_t) * cnt, cudaMemcpyHostToDevice,
+                         s->stream));
+      CK(cudaMemcpyAsync(&s->ctl.as<TrainCtl>()->mb_count[0], &cnt, sizeof(cnt), cudaMemcpyHostToDevice,
+                         s->stream));
+      enqueue_minibatch(s, *cfg, 0, 1.0 / static_cast<double>(cfg->minibatch));
+      enqueue_adam(s, *cfg);
+    }
+    CK(cudaEventRecord(pool_event(s->ev_train, s->n_train_ev), s->stream));
+    const wg_train_stats d = sync_collect(s, before);
+    st.records_consumed = d.records_consumed;
+    st.skipped_low_v = d.skipped_low_v;
+    st.steps = d.steps;
+    st.mean_grad_norm = d.mean_grad_norm;
+    st.seconds = d.seconds;
     s->have_records = false;
     if (stats) *stats = st;
   });

@@ -410,9 +410,12 @@ __global__ void adam_kernel(float* p, double* m, double* v, const float* g, int6
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     double gi = static_cast<double>(g[i]) * scale;
     local += gi * gi;
-    double mi = m[i] = b1 * m[i] + (1.0 - b1) * gi;
-    double vi = v[i] = b2 * v[i] + (1.0 - b2) * gi * gi;
-    double up = lr * (mi / bc1) / (sqrt(vi / bc2) + eps);
+    // the reference's operation order, each product rounded on its own (this
+    // translation unit may contract FMAs elsewhere): bit-equal moments and
+    // updates to GuidingField::adam_step given the same gradient
+    double mi = m[i] = __dadd_rn(__dmul_rn(b1, m[i]), __dmul_rn(1.0 - b1, gi));
+    double vi = v[i] = __dadd_rn(__dmul_rn(b2, v[i]), __dmul_rn(__dmul_rn(1.0 - b2, gi), gi));
+    double up = __dmul_rn(lr, mi / bc1) / __dadd_rn(sqrt(vi / bc2), eps);
     const float np = static_cast<float>(static_cast<double>(p[i]) - up);
     p[i] = np;
     if (blob != nullptr && i >= f.w1) wpack::pack_param(f, blob, i, np);

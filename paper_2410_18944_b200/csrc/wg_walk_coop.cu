@@ -432,9 +432,9 @@ __device__ __forceinline__ void c_mixture_sample(Pcg& rng, const Lobe& L, int la
 
 }  // namespace
 
-// kResume: finish the walks the lockstep kernel handed off (WalkArgs::spill)
-// instead of starting fresh ones
-template <bool kResume>
+// finish the walks the lockstep kernel handed off (WalkArgs::spill), one
+// warp per walk (a standalone warp-per-walk kernel that also started fresh
+// walks measured slower than the lockstep tiles on cfg 2)
 __device__ __forceinline__ void walk_coop_body(const WalkArgs& a, unsigned char* smem) {
   CoopW& W = *reinterpret_cast<CoopW*>(smem);
   float* hbuf = reinterpret_cast<float*>(smem + al16c(sizeof(CoopW))) + 64 * (threadIdx.x >> 5);
@@ -505,7 +505,7 @@ __device__ __forceinline__ void walk_coop_body(const WalkArgs& a, unsigned char*
     unsigned long long idx = 0;
     if (lane == 0) idx = atomicAdd(&a.counters[6], 1ull);  // work queue head
     idx = __shfl_sync(0xffffffffu, idx, 0);
-    if (kResume) {
+    {
       if (idx >= a.counters[7]) break;  // handed-off walks (written by the previous launch)
       if (collect && lane == 0)  // the previous walk's record block ends with it
         for (int i = 0; i < w.rec_left; ++i) a.recs[w.rec_base + (8 - w.rec_left) + i].flags = 0u;
@@ -529,29 +529,10 @@ __device__ __forceinline__ void walk_coop_body(const WalkArgs& a, unsigned char*
       w.last_rec = o.last_rec;
       w.on_n = o.on_n != 0;
       w.rec_ok = o.rec_ok != 0;
-    } else {
-    if (static_cast<int64_t>(idx) >= total) break;
-    w.round = static_cast<int>(static_cast<int64_t>(idx) / a.n_points);
-    w.point = static_cast<int64_t>(idx) - static_cast<int64_t>(w.round) * a.n_points;
-    w.x = a.points[2 * w.point];
-    w.y = a.points[2 * w.point + 1];
-    w.nx = w.ny = 0.0;
-    w.on_n = false;
-    w.seg = -1;
-    w.T = 1.0;
-    w.acc = 0.0;
-    w.R = 0.0;
-    w.depth = 0;
-    w.rng = Pcg::walk(a.seed, static_cast<uint64_t>(a.point_offset + w.point),
-                      a.wpp_first + static_cast<uint64_t>(w.round));
-    w.rec_ok = true;
-    w.last_rec = -1;
-    w.dacc = 0.0;
-    ++walks_done;
     }
 
     // a handed-off walk enters at its direction step (begin_step done)
-    for (bool go = kResume || c_begin(w, a, s, ss, collect, lane); go; go = c_begin(w, a, s, ss, collect, lane)) {
+    for (bool go = true; go; go = c_begin(w, a, s, ss, collect, lane)) {
       // field evaluation and Table-1 decode
       float xin[16];
       c_gather(f, w.x, w.y, xin);
@@ -658,39 +639,14 @@ __device__ __forceinline__ void walk_coop_body(const WalkArgs& a, unsigned char*
   if (lane == 0 && walks_done) atomicAdd(&a.counters[2], walks_done);
 }
 
-__global__ void __launch_bounds__(kCoopThreads, 2) walk_kernel_coop(WalkArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  walk_coop_body<false>(a, smem);
-}
-
 __global__ void __launch_bounds__(kCoopThreads, 2) walk_kernel_coop_resume(WalkArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  walk_coop_body<true>(a, smem);
+  walk_coop_body(a, smem);
 }
 
 int walk_coop_smem(const WalkArgs& a) {
   return static_cast<int>(al16c(sizeof(CoopW)) + sizeof(float) * 64 * kCoopWarps +
                           (a.scene_smem_bytes > 0 ? al16c(a.scene_smem_bytes) : 0));
-}
-
-int walk_coop_block() { return kCoopThreads; }
-
-int walk_coop_blocks_per_sm(int smem) {
-  int n = 0;
-  cudaFuncSetAttribute(walk_kernel_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, walk_kernel_coop, kCoopThreads, smem);
-  return n;
-}
-
-cudaError_t launch_walks_coop(const WalkArgs& a, int blocks, cudaStream_t st) {
-  const int smem = walk_coop_smem(a);
-  cudaError_t e = cudaFuncSetAttribute(walk_kernel_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  // per-launch work queue head (counters[6])
-  e = cudaMemsetAsync(a.counters + 6, 0, sizeof(unsigned long long), st);
-  if (e != cudaSuccess) return e;
-  walk_kernel_coop<<<blocks, kCoopThreads, smem, st>>>(a);
-  return cudaGetLastError();
 }
 
 // the lockstep kernel's handed-off tail walks (counters[7] of them, at most

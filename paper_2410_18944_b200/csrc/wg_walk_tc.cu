@@ -248,16 +248,14 @@ __device__ __forceinline__ bool t_begin(TLane& w, const WalkArgs& a, const Scene
 
 }  // namespace
 
-// kWarp = false: the CTA's 128 walks share one M = 128 tile and step in
-// lockstep (CTA barrier per step). kWarp = true: every warp runs its own MLP
-// chain (tcw_forward) and advances independently of the other warps.
-template <bool kWarp>
+// The CTA's 128 walks share one M = 128 tile and step in lockstep (CTA
+// barrier per step).
 __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* smem) {
   unsigned char* tc = smem;  // TcLayout block first (128-B aligned)
   SceneView s = a.scene;
   if (a.scene_smem_bytes > 0) {
     unsigned char* p =
-        smem + al16(kWarp ? TcLayoutW::BYTES : TcLayout::BYTES + (a.small_mlp ? sizeof(SmallMlp) : 0));
+        smem + al16(TcLayout::BYTES + (a.small_mlp ? sizeof(SmallMlp) : 0));
     size_t off = 0;
     auto carve = [&](size_t bytes) {
       unsigned char* q = p + off;
@@ -291,18 +289,14 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
     seg_counts[1] = nn;
   }
   SmallSegs ss{seg_lists, seg_lists + kSmallScene, 0, 0};
-  SmallMlp& small = *reinterpret_cast<SmallMlp*>(smem + TcLayout::BYTES);  // lockstep kernel only
-  if (kWarp) {
-    tcw_stage_weights(tc, a.field);
-  } else {
-    tc_fetch_weights(tc, a.wblob);
-    tc_setup(tc);
-    if (a.small_mlp) small_stage(small, a.field);
-  }
+  SmallMlp& small = *reinterpret_cast<SmallMlp*>(smem + TcLayout::BYTES);
+  tc_fetch_weights(tc, a.wblob);
+  tc_setup(tc);
+  if (a.small_mlp) small_stage(small, a.field);
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
-  if (!kWarp) tc_wait_weights(tc);
+  tc_wait_weights(tc);
   ss.nd = seg_counts[0];
   ss.nn = seg_counts[1];
 
@@ -331,7 +325,7 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
       if (threadIdx.x == 0) a.phase_prof[8 * blockIdx.x + 2] += static_cast<unsigned long long>(t_top - t_iter);
       t_iter = t_top;
     }
-    if (!kWarp && a.small_mlp && threadIdx.x == 0) small.slot_count = 0;  // consumed after the phase-A barrier
+    if (a.small_mlp && threadIdx.x == 0) small.slot_count = 0;  // consumed after the phase-A barrier
     // ---- phase A: every slot advances to a walk that needs a direction
     bool need = false;
     for (;;) {
@@ -363,9 +357,7 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
       }
     }
     int active = 0;
-    if (kWarp) {
-      if (!__any_sync(0xffffffffu, need)) break;
-    } else {
+    {
       active = __syncthreads_count(need);
       if (active == 0) break;
       // tail handoff (WalkArgs::spill): a few live walks left and no fresh
@@ -417,7 +409,7 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
     SUB_ADD(3, tg);
     SUB_T(tb);
     float raw[TcLayout::NO];
-    if (!kWarp && a.small_mlp && active <= kSmallRows) {  // tail iteration: CUDA-core rows (SmallMlp)
+    if (a.small_mlp && active <= kSmallRows) {  // tail iteration: CUDA-core rows (SmallMlp)
       int slot = -1;
       if (need) {
         slot = atomicAdd(&small.slot_count, 1);
@@ -434,8 +426,6 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
       if (need)
 #pragma unroll
         for (int i = 0; i < TcLayout::NO; ++i) raw[i] = small.r[slot][i];
-    } else if (kWarp) {
-      tcw_forward(tc, phase, xin, raw, a.phase_prof ? &bpa[0] : nullptr);
     } else {
       tc_forward(tc, phase, xin, raw, a.phase_prof ? bpa : nullptr);
     }
@@ -548,18 +538,12 @@ __device__ __forceinline__ void walk_tc_body(const WalkArgs& a, unsigned char* s
     }
   }
 #endif
-  if (kWarp) tcw_teardown(tc);
-  else tc_teardown(tc);
+  tc_teardown(tc);
 }
 
 __global__ void __launch_bounds__(128, 1) walk_kernel_tc(WalkArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
-  walk_tc_body<false>(a, smem);
-}
-
-__global__ void __launch_bounds__(128) walk_kernel_tcw(WalkArgs a) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  walk_tc_body<true>(a, smem);
+  walk_tc_body(a, smem);
 }
 
 // GuidingField::eval_batch on the tensor cores: persistent CTAs over 128-point tiles
@@ -586,21 +570,11 @@ __global__ void __launch_bounds__(128) field_eval_tc_kernel(FieldView f, int64_t
   tc_teardown(smem);
 }
 
-// warps per CTA of the warp-independent kernel (0 = lockstep 128-walk CTAs,
-// the default: measured faster on cfg 2, 0.85 vs 1.2 ms per round, because
-// the per-warp M = 128 MMAs quadruple tensor/smem traffic and the waiting
-// warps' mbarrier polling slows the running warps); WOSTGPU_TC_WARPS = 1/2/4
-// selects the warp-independent kernel for experiments
-int walk_tc_warps() {
-  static const int w = [] {
-    const char* e = std::getenv("WOSTGPU_TC_WARPS");
-    int v = e ? std::atoi(e) : 0;
-    return (v == 0 || v == 1 || v == 2 || v == 4) ? v : 0;
-  }();
-  return w;
-}
-
-int walk_tc_block() { return walk_tc_warps() == 0 ? 128 : 32 * walk_tc_warps(); }
+// lockstep 128-walk CTAs (a warp-independent variant with per-warp M = 128
+// MMAs measured slower on cfg 2, 0.85 vs 1.2 ms per round: 4x the tensor /
+// smem traffic, and the waiting warps' mbarrier polling slows the running
+// ones)
+int walk_tc_block() { return 128; }
 
 // ---- diagnostics of the fp32 mixture math (wostgpu_mixture32_*)
 __global__ void mix32_pdf_kernel(const float* raw, int64_t n, const double* nu, double* out) {
@@ -638,27 +612,24 @@ cudaError_t launch_mix32_sample(const float* raw, int64_t n, uint64_t seed, doub
 }
 
 int walk_tc_smem(const WalkArgs& a) {
-  size_t tile = walk_tc_warps() == 0 ? TcLayout::BYTES + (a.small_mlp ? sizeof(SmallMlp) : 0) : TcLayoutW::BYTES;
+  size_t tile = TcLayout::BYTES + (a.small_mlp ? sizeof(SmallMlp) : 0);
   return static_cast<int>(al16(tile) + (a.scene_smem_bytes > 0 ? al16(a.scene_smem_bytes) : 0));
 }
 
 int walk_tc_blocks_per_sm(int smem) {
   int n = 0;
-  const int warps = walk_tc_warps();
-  auto k = warps == 0 ? walk_kernel_tc : walk_kernel_tcw;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, walk_tc_block(), smem);
-  // 512 TMEM columns per SM: 128 per lockstep CTA, 64 per warp otherwise
-  const int tmem_cap = warps == 0 ? 4 : 512 / (64 * warps);
+  cudaFuncSetAttribute(walk_kernel_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, walk_kernel_tc, walk_tc_block(), smem);
+  // 512 TMEM columns per SM: 128 per lockstep CTA
+  const int tmem_cap = 4;
   return n < tmem_cap ? n : tmem_cap;
 }
 
 cudaError_t launch_walks_tc(const WalkArgs& a, int blocks, cudaStream_t st) {
   int smem = walk_tc_smem(a);
-  auto k = walk_tc_warps() == 0 ? walk_kernel_tc : walk_kernel_tcw;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(walk_kernel_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k<<<blocks, walk_tc_block(), smem, st>>>(a);
+  walk_kernel_tc<<<blocks, walk_tc_block(), smem, st>>>(a);
   return cudaGetLastError();
 }
 

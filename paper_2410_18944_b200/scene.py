@@ -71,6 +71,17 @@ class Value:
             if self.analytic_id == abi.ANALYTIC_X2_MINUS_Y2:
                 return x * x - y * y
             return x * x + y * y - 1.0
+        if self.type == abi.VALUE_RASTER:  # RasterGrid::at (scene.cpp:13-20): nearest cell, clamped
+            g = np.asarray(self.raster, dtype=np.float64)
+            h, w = g.shape
+            b = self.raster_bbox
+            u = (x - b[0]) / (b[2] - b[0])
+            v = (y - b[1]) / (b[3] - b[1])
+            i = min(max(int(u * w), 0), w - 1)
+            j = min(max(int(v * h), 0), h - 1)
+            return float(g[j, i])
+        if self.type == abi.VALUE_ZERO:
+            return 0.0
         raise NotImplementedError
 
 

@@ -7,7 +7,7 @@ import math
 import numpy as np
 
 from paper_2410_18944_b200 import abi
-from paper_2410_18944_b200.scene import Scene, Value
+from paper_2410_18944_b200.scene import Scene, Value, default_epsilon_shell
 
 M64 = (1 << 64) - 1
 
@@ -102,3 +102,33 @@ def polygon_scene(center, radius, n, kind, value, bbox):
 
 def probes(rng: Rng, n, lo, hi):
     return np.array([(rng.uniform(lo, hi), rng.uniform(lo, hi)) for _ in range(n)])
+
+
+# ---- scenes with Neumann flux and raster values (tests/test_gpu_values_train.py)
+BOX = (0.0, 0.0, 1.0, 1.0)
+
+
+def flux_scene():
+    """Unit square: Dirichlet x = 0 (g = 0) and x = 1 (g = y); Neumann y = 0
+    with constant flux h = 0.7 and y = 1 with linear flux h = 0.2 + 0.5 x."""
+    seg = np.array([[0, 0, 1, 0], [1, 0, 1, 1], [1, 1, 0, 1], [0, 1, 0, 0]], dtype=np.float64)
+    kind = np.array([abi.NEUMANN, abi.DIRICHLET, abi.NEUMANN, abi.DIRICHLET], dtype=np.int32)
+    values = [Value.constant(0.7), Value.linear(0.0, 0.0, 1.0), Value.linear(0.2, 0.5, 0.0), Value.constant(0.0)]
+    return Scene(BOX, default_epsilon_shell(BOX), seg, kind, np.array([0, 1, 2, 3], dtype=np.int32), values)
+
+
+def raster_scene():
+    """A 24-gon (radius 0.45) with raster Dirichlet values on half of its
+    edges, a linear value on the rest, and a raster source term."""
+    rng = np.random.default_rng(5)
+    g = Value(abi.VALUE_RASTER, raster=rng.uniform(-1.0, 2.0, (5, 7)), raster_bbox=(0.0, 0.0, 1.0, 1.0))
+    f = Value(abi.VALUE_RASTER, raster=rng.uniform(0.0, 3.0, (6, 6)), raster_bbox=(0.0, 0.0, 1.0, 1.0))
+    n = 24
+    ang = 2.0 * np.pi * np.arange(n) / n
+    pts = np.stack([0.5 + 0.45 * np.cos(ang), 0.5 + 0.45 * np.sin(ang)], 1)
+    seg = np.concatenate([pts, np.roll(pts, -1, 0)], 1)
+    kind = np.full(n, abi.DIRICHLET, dtype=np.int32)
+    vi = np.array([0 if i % 2 == 0 else 1 for i in range(n)], dtype=np.int32)
+    return Scene(BOX, default_epsilon_shell(BOX), seg, kind, vi, [g, Value.linear(0.5, 1.0, -1.0)], source=f)
+
+

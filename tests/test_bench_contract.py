@@ -26,7 +26,7 @@ def _run(*args):
 def test_reference_arm_cfg2():
     if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libwost_ref.so")):
         pytest.skip("oracle/_ref not built")
-    d = _run("--ref-rounds", "2")
+    d = _run("--workload", "cfg2", "--ref-rounds", "2")
     assert KEYS <= set(d), KEYS - set(d)
     assert d["impl"] == "reference" and d["metric"] == "guided WoSt walks/sec" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
@@ -34,7 +34,9 @@ def test_reference_arm_cfg2():
 
 
 def test_reference_arm_cfg4():
-    d = _run("--workload", "cfg4")
+    d = _run("--workload", "cfg4", "--ref-rounds", "2")
     assert KEYS <= set(d), KEYS - set(d)
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "port"
+    # the cfg 2 block: the reference's own run_solve
+    assert d["cfg2"]["cpu_baseline"]["kind"] == "reference" and d["cfg2"]["value"] > 0

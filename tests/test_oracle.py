@@ -102,6 +102,27 @@ def test_oracle_bit_exact_with_reference_library(orc, ref):
             assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
+def test_oracle_flux_and_raster_scenes_bit_exact_with_reference(orc, ref):
+    """Neumann flux (sample_neumann_contrib, wost.cpp:89-109) and raster
+    values / source (scene.cpp:13-20, 53-67): the restatement reproduces the
+    reference's walks bit for bit, uniform and guided."""
+    from fixtures import flux_scene, raster_scene
+    xy = cell_centers(20, 20, (0.1, 0.1, 0.9, 0.9))
+    for sc in (flux_scene(), raster_scene()):
+        ho, hr = orc.scene(sc), ref.scene(sc)
+        assert orc.fn("has_neumann_flux")(ho) == ref.fn("has_neumann_flux")(hr)
+        for mode in ("uniform", "learnable_mis"):
+            fo = orc.field(abi.field_config(), sc.bbox, 4) if mode != "uniform" else None
+            fr = ref.field(abi.field_config(), sc.bbox, 4) if mode != "uniform" else None
+            a = orc.walks(ho, fo, abi.solver_config(mode), xy, 6, 1)
+            b = ref.walks(hr, fr, abi.solver_config(mode), xy, 6, 1)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+            assert np.std(a[0]) > 0
+    # raster values evaluated on the host mirror RasterGrid::at
+    g = raster_scene().values[0]
+    assert g.eval(-0.3, 0.5) == g.raster[2, 0] and g.eval(0.999, 1.7) == g.raster[4, 6]
+
+
 # ---------------------------------------------------------------- unit KATs
 def test_bessel_known_answers(orc):
     # proj/tests/test_sphdist.cpp:62-76
