@@ -32,6 +32,10 @@ const char* wostgpu_last_error(void);
 /* binds the calling thread to `device` (one process per GPU) */
 int wostgpu_init(int device);
 int wostgpu_device_info(int* sm_count, int* cc_major, int* cc_minor);
+/* waits for all device work of the library and reports a pending device
+ * error; handles must be destroyed by the caller before (the CUDA context
+ * is shared with the host process, so it is not reset) */
+int wostgpu_shutdown(void);
 /* number of kernels this library launched since load (bench evidence) */
 int64_t wostgpu_kernel_launches(void);
 
@@ -79,6 +83,19 @@ int wostgpu_field_get_state(wg_field field, float* params, double* adam_m, doubl
                             int64_t* adam_steps);
 int wostgpu_field_set_state(wg_field field, const float* params, const double* adam_m,
                             const double* adam_v, int64_t adam_steps);
+/* get_param / set_param (guide_field.hpp:73-77) over a contiguous range */
+int wostgpu_field_get_params(wg_field field, int64_t offset, int64_t count, float* out);
+int wostgpu_field_set_params(wg_field field, int64_t offset, int64_t count, const float* in);
+/* GuidingField::eval_with_tape + backward (guide_field.cpp:223-243,
+ * 258-315) for n points: grad[n_params] += sum_i J(x_i)^T d_out[i x od], in
+ * fp64 as the reference (summation order across points differs: fp64
+ * atomics) */
+int wostgpu_field_backward(wg_field field, int64_t n, const double* xy, const double* d_out,
+                           double* grad);
+/* GuidingField::adam_step (guide_field.cpp:317-331) on an fp64 gradient,
+ * which is zeroed on return as in the reference */
+int wostgpu_field_adam_step(wg_field field, double* grad, double lr, double beta1, double beta2,
+                            double eps);
 /* GuidingField::eval_batch (guide_field.cpp:178-221, 251-256): row-major
  * [n x output_dim]. mlp = WG_MLP_EXACT reproduces the reference's fp32
  * accumulation order bit for bit (CUDA cores); WG_MLP_TENSOR runs the

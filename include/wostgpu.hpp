@@ -21,7 +21,10 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <utility>
+#include <variant>
 #include <vector>
+#include <algorithm>
 
 #include "wostgpu.h"
 
@@ -39,6 +42,10 @@ inline void check(int rc) {
   throw std::runtime_error(msg);
 }
 
+// wostgpu_shutdown: waits for the library's device work (call after the
+// last handle is destroyed)
+inline void shutdown() { check(wostgpu_shutdown()); }
+
 struct Vec2 {
   double x = 0.0, y = 0.0;
 };
@@ -55,19 +62,152 @@ enum class SamplerMode {
   LearnableMis = WG_MODE_LEARNABLE_MIS
 };
 
-// Scene description in the reference's shape (scene.hpp:70-96): values are
-// wg_value_spec (constant / linear / raster / preset analytic)
-struct BoundarySegment {
+// Scene description in the reference's shape (scene.hpp:17-96): named
+// values (Constant / Linear / Raster / Analytic), a source field, segments
+// that refer to values by name, validate() resolving value_index.
+//
+// Analytic values are std::function in the reference; a device cannot call
+// host code, so here they name one of the device's built-in analytic
+// functions (the preset ones, wostgpu_types.h): WG_ANALYTIC_X2_MINUS_Y2
+// (x^2 - y^2, harmonic-disk g, presets.cpp:191-192) and
+// WG_ANALYTIC_R2_MINUS_1 (|x|^2 - 1, const-source-disk g, presets.cpp:202-203).
+// An Analytic value with id 0 (an arbitrary host function) is rejected with
+// std::invalid_argument when the scene is uploaded.
+struct RasterGrid {  // scene.hpp:20-28
+  int width = 0, height = 0;
+  Bbox bbox;
+  std::vector<double> data;  // row-major, row 0 at bbox.min.y
+  double at(Vec2 p) const {  // scene.cpp:13-20, nearest cell, clamped
+    double u = (p.x - bbox.min.x) / (bbox.max.x - bbox.min.x);
+    double v = (p.y - bbox.min.y) / (bbox.max.y - bbox.min.y);
+    int i = std::clamp(static_cast<int>(u * width), 0, width - 1);
+    int j = std::clamp(static_cast<int>(v * height), 0, height - 1);
+    return data[static_cast<size_t>(j) * width + i];
+  }
+};
+
+struct ValueSpec {  // scene.hpp:31-54
+  struct Constant {
+    double v;
+  };
+  struct Linear {
+    double c0, cx, cy;
+  };
+  struct Raster {
+    RasterGrid grid;
+  };
+  struct Analytic {
+    int id = 0;  // WG_ANALYTIC_*
+    std::string name;
+  };
+  std::variant<Constant, Linear, Raster, Analytic> spec = Constant{0.0};
+  bool is_analytic() const { return std::holds_alternative<Analytic>(spec); }
+  double eval(Vec2 p) const {  // scene.cpp:22-37
+    if (auto* c = std::get_if<Constant>(&spec)) return c->v;
+    if (auto* l = std::get_if<Linear>(&spec)) return l->c0 + l->cx * p.x + l->cy * p.y;
+    if (auto* r = std::get_if<Raster>(&spec)) return r->grid.at(p);
+    const int id = std::get<Analytic>(spec).id;
+    if (id == WG_ANALYTIC_X2_MINUS_Y2) return p.x * p.x - p.y * p.y;
+    if (id == WG_ANALYTIC_R2_MINUS_1) return p.x * p.x + p.y * p.y - 1.0;
+    throw std::invalid_argument("analytic value without a device function id");
+  }
+  // the C-ABI spec; raster data is borrowed from this object
+  wg_value_spec c() const {
+    wg_value_spec o{};
+    o.type = WG_VALUE_CONSTANT;
+    if (auto* c = std::get_if<Constant>(&spec)) {
+      o.c0 = c->v;
+    } else if (auto* l = std::get_if<Linear>(&spec)) {
+      o.type = WG_VALUE_LINEAR;
+      o.c0 = l->c0;
+      o.cx = l->cx;
+      o.cy = l->cy;
+    } else if (auto* r = std::get_if<Raster>(&spec)) {
+      o.type = WG_VALUE_RASTER;
+      raster_c(r->grid, o);
+    } else {
+      const Analytic& a = std::get<Analytic>(spec);
+      if (a.id != WG_ANALYTIC_X2_MINUS_Y2 && a.id != WG_ANALYTIC_R2_MINUS_1)
+        throw std::invalid_argument("value '" + a.name + "': analytic values need a device function id");
+      o.type = WG_VALUE_ANALYTIC;
+      o.analytic_id = a.id;
+    }
+    return o;
+  }
+  static void raster_c(const RasterGrid& g, wg_value_spec& o) {
+    o.raster_w = g.width;
+    o.raster_h = g.height;
+    o.raster_bbox[0] = g.bbox.min.x;
+    o.raster_bbox[1] = g.bbox.min.y;
+    o.raster_bbox[2] = g.bbox.max.x;
+    o.raster_bbox[3] = g.bbox.max.y;
+    o.raster_data = g.data.data();
+  }
+};
+
+struct SourceField {  // scene.hpp:56-67
+  struct Zero {};
+  struct Constant {
+    double v;
+  };
+  struct Raster {
+    RasterGrid grid;
+  };
+  std::variant<Zero, Constant, Raster> spec;
+  bool is_zero() const { return std::holds_alternative<Zero>(spec); }
+  wg_value_spec c() const {
+    wg_value_spec o{};
+    o.type = WG_VALUE_ZERO;
+    if (auto* c = std::get_if<Constant>(&spec)) {
+      o.type = WG_VALUE_CONSTANT;
+      o.c0 = c->v;
+    } else if (auto* r = std::get_if<Raster>(&spec)) {
+      o.type = WG_VALUE_RASTER;
+      ValueSpec::raster_c(r->grid, o);
+    }
+    return o;
+  }
+};
+
+struct BoundarySegment {  // scene.hpp:69-74
   Vec2 a, b;
   BoundaryKind kind = BoundaryKind::Dirichlet;
-  int value_index = 0;
+  std::string value_ref;
+  int value_index = -1;  // resolved by Scene::validate
 };
-struct Scene {
+
+struct Scene {  // scene.hpp:76-96
   Bbox bbox;
   double epsilon_shell = 0.0;
-  std::vector<wg_value_spec> values;
-  wg_value_spec source{WG_VALUE_ZERO, 0, 0, 0, 0, 0, 0, {0, 0, 0, 0}, nullptr};
+  std::vector<std::pair<std::string, ValueSpec>> values;
+  SourceField source;
   std::vector<BoundarySegment> segments;
+
+  int find_value(const std::string& name) const {
+    for (size_t i = 0; i < values.size(); ++i)
+      if (values[i].first == name) return static_cast<int>(i);
+    return -1;
+  }
+  bool has_dirichlet() const {
+    for (const auto& g : segments)
+      if (g.kind == BoundaryKind::Dirichlet) return true;
+    return false;
+  }
+  // Scene::validate (scene.cpp:119-143): value references resolved here; the
+  // geometric and raster invariants are checked again by the device upload
+  // (wostgpu_scene_create) with the reference's messages
+  void validate() {
+    if (!(bbox.min.x < bbox.max.x && bbox.min.y < bbox.max.y)) throw SceneError("scene bbox is empty");
+    if (epsilon_shell <= 0.0)
+      throw SceneError("epsilon_shell must be > 0 (got " + std::to_string(epsilon_shell) + ")");
+    if (segments.empty()) throw SceneError("scene has no boundary segments");
+    for (size_t i = 0; i < segments.size(); ++i) {
+      BoundarySegment& g = segments[i];
+      g.value_index = find_value(g.value_ref);
+      if (g.value_index < 0)
+        throw SceneError("segment " + std::to_string(i) + ": value '" + g.value_ref + "' is not defined");
+    }
+  }
 };
 
 struct ClosestPoint {  // geom2d.hpp:30-34
@@ -145,18 +285,37 @@ struct FieldConfig {  // guide_field.hpp:13-25
 
 class Accel {  // geom2d.hpp:38-91, batched on the device
  public:
+  // Accel(const Scene&) (geom2d.cpp:80-107): the scene is uploaded with its
+  // values; segments whose value_index is unresolved are resolved by name
   explicit Accel(const Scene& s) {
     std::vector<double> seg;
     std::vector<int32_t> kind, vi;
     for (const auto& g : s.segments) {
       seg.insert(seg.end(), {g.a.x, g.a.y, g.b.x, g.b.y});
       kind.push_back(static_cast<int32_t>(g.kind));
-      vi.push_back(g.value_index);
+      const int idx = g.value_index >= 0 ? g.value_index : s.find_value(g.value_ref);
+      if (idx < 0) throw SceneError("value '" + g.value_ref + "' is not defined");
+      vi.push_back(idx);
     }
+    std::vector<wg_value_spec> vals;
+    for (const auto& nv : s.values) vals.push_back(nv.second.c());
+    const wg_value_spec src = s.source.c();
     double bb[4] = {s.bbox.min.x, s.bbox.min.y, s.bbox.max.x, s.bbox.max.y};
     check(wostgpu_scene_create(seg.data(), kind.data(), vi.data(), static_cast<int32_t>(kind.size()),
-                               s.values.data(), static_cast<int32_t>(s.values.size()), &s.source, bb,
-                               s.epsilon_shell, &h_));
+                               vals.data(), static_cast<int32_t>(vals.size()), &src, bb, s.epsilon_shell,
+                               &h_));
+  }
+  // batched queries (the C-ABI entries; one CUDA thread per query)
+  void closest_point_batch(std::span<const Vec2> xs, unsigned kinds, std::span<ClosestPoint> out) const {
+    const size_t n = xs.size();
+    std::vector<double> pt(2 * n), d(n);
+    std::vector<int32_t> sg(n);
+    check(wostgpu_closest_point(h_, static_cast<int64_t>(n), &xs.data()->x, kinds, pt.data(), d.data(),
+                                sg.data()));
+    for (size_t i = 0; i < n; ++i) out[i] = {{pt[2 * i], pt[2 * i + 1]}, d[i], sg[i]};
+  }
+  void star_radius_batch(std::span<const Vec2> xs, double r_min, double* r) const {
+    check(wostgpu_star_radius(h_, static_cast<int64_t>(xs.size()), &xs.data()->x, r_min, r));
   }
   ~Accel() { wostgpu_scene_destroy(h_); }
   Accel(const Accel&) = delete;
@@ -227,6 +386,34 @@ class GuidingField {  // guide_field.hpp:37-96
     check(wostgpu_field_get_state(h_, nullptr, nullptr, nullptr, &s));
     return s;
   }
+  // GuidingField::eval (guide_field.cpp:178-221): the reference's fp32 MLP
+  // arithmetic bit for bit (one point; batch with eval_batch)
+  void eval(Vec2 x, double* out) const { check(wostgpu_field_eval_batch(h_, 1, &x.x, out, WG_MLP_EXACT)); }
+  // eval_with_tape / backward (guide_field.cpp:223-243, 258-315): the tape
+  // keeps the point; backward re-runs the fp64 forward on the device and
+  // accumulates J^T d_out into grad
+  struct Tape {
+    Vec2 x;
+  };
+  void eval_with_tape(Vec2 x, double* out, Tape& tape) const {
+    tape.x = x;
+    eval(x, out);
+  }
+  void backward(const Tape& tape, const double* d_out, std::vector<double>& grad) const {
+    if (grad.size() != param_count()) throw std::invalid_argument("backward: gradient size mismatch");
+    check(wostgpu_field_backward(h_, 1, &tape.x.x, d_out, grad.data()));
+  }
+  // GuidingField::adam_step (guide_field.cpp:317-331); zeroes grad
+  void adam_step(std::vector<double>& grad, double lr, double beta1, double beta2, double eps) {
+    if (grad.size() != param_count()) throw std::invalid_argument("adam_step: gradient size mismatch");
+    check(wostgpu_field_adam_step(h_, grad.data(), lr, beta1, beta2, eps));
+  }
+  float get_param(size_t i) const {
+    float v = 0.0f;
+    check(wostgpu_field_get_params(h_, static_cast<int64_t>(i), 1, &v));
+    return v;
+  }
+  void set_param(size_t i, float v) { check(wostgpu_field_set_params(h_, static_cast<int64_t>(i), 1, &v)); }
   // row-major [points x output_dim] (guide_field.cpp:251-256)
   void eval_batch(std::span<const Vec2> xs, double* out, int mlp = WG_MLP_EXACT) const {
     check(wostgpu_field_eval_batch(h_, static_cast<int64_t>(xs.size()), &xs.data()->x, out, mlp));
@@ -320,11 +507,19 @@ class StepContext {
   wg_solver h_ = nullptr;
 };
 
+// SolveScratch (wost.hpp:147-154): the reference reuses its host wavefront
+// buffers across rounds; the device solver (StepContext) owns its walk
+// queues and record arena, so the scratch object carries nothing and the
+// parameter is accepted for source compatibility
+struct SolveScratch {};
+
 // solve_batch (wost.hpp:160-163): one walk per point for wpp round
 // `wpp_index`, Welford statistics updated in place, records appended
 inline void solve_batch(const StepContext& ctx, std::span<const Vec2> points,
                         std::span<PointStats> stats, uint64_t seed, uint64_t wpp_index,
-                        bool collect_records, std::vector<GuideRecord>* records) {
+                        bool collect_records, std::vector<GuideRecord>* records,
+                        SolveScratch* scratch = nullptr) {
+  (void)scratch;
   if (points.size() != stats.size()) throw std::invalid_argument("points and stats differ in size");
   check(wostgpu_solve_batch(ctx.handle(), static_cast<int64_t>(points.size()), &points.data()->x,
                             stats.data(), seed, wpp_index, collect_records ? 1 : 0));

@@ -340,6 +340,21 @@ void* ref_field_load(const char* path) {
   return rc == WG_OK ? f : nullptr;
 }
 int64_t ref_field_adam_steps(void* fp) { return static_cast<GuidingField*>(fp)->adam_steps(); }
+// GuidingField::eval_with_tape + backward (proj/src/guide_field.cpp:223-243,
+// 258-315) summed over n points, in point order
+void ref_field_backward(void* fp, int64_t n, const double* xy, const double* d_out, double* grad) {
+  auto* f = static_cast<GuidingField*>(fp);
+  const int od = f->config().output_dim();
+  std::vector<double> g(grad, grad + f->param_count());
+  std::vector<double> out(od);
+  GuidingField::Tape tape;
+  for (int64_t i = 0; i < n; ++i) {
+    f->eval_with_tape({xy[2 * i], xy[2 * i + 1]}, out.data(), tape);
+    f->backward(tape, d_out + i * od, g);
+  }
+  std::copy(g.begin(), g.end(), grad);
+}
+
 // GuidingField::adam_step (proj/src/guide_field.cpp:317-331) on a given
 // gradient (which the reference zeroes on return)
 void ref_field_adam_step(void* fp, const double* grad, double lr, double beta1, double beta2, double eps) {

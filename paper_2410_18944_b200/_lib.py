@@ -73,6 +73,11 @@ _SIGS = {
     "wostgpu_train_batch": (C.c_int, [VP, VP, C.c_int64, C.POINTER(abi.TrainConfig), C.c_uint64,
                                       C.POINTER(abi.TrainStats)]),
     "wostgpu_field_grad": (C.c_int, [VP, VP, C.c_int64, C.POINTER(abi.TrainConfig), D]),
+    "wostgpu_field_get_params": (C.c_int, [VP, C.c_int64, C.c_int64, F32]),
+    "wostgpu_field_set_params": (C.c_int, [VP, C.c_int64, C.c_int64, F32]),
+    "wostgpu_field_backward": (C.c_int, [VP, C.c_int64, D, D, D]),
+    "wostgpu_field_adam_step": (C.c_int, [VP, D, C.c_double, C.c_double, C.c_double, C.c_double]),
+    "wostgpu_shutdown": (C.c_int, []),
     "wostgpu_train_prepare": (C.c_int, [VP, C.POINTER(abi.TrainConfig), I64]),
     "wostgpu_train_select": (C.c_int, [VP, C.POINTER(abi.TrainConfig), C.c_int64, I32]),
     "wostgpu_train_minibatch_grad": (C.c_int, [VP, C.POINTER(abi.TrainConfig), C.c_int32, F32]),

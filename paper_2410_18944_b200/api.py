@@ -154,6 +154,32 @@ class GuidingField:
         check(load().wostgpu_field_set_state(self.h, p.ctypes.data_as(C.POINTER(C.c_float)),
                                               _d(m), _d(v), steps))
 
+    def get_param(self, i):
+        """GuidingField::get_param (guide_field.hpp:73-77)."""
+        out = np.zeros(1, dtype=np.float32)
+        check(load().wostgpu_field_get_params(self.h, int(i), 1, out.ctypes.data_as(C.POINTER(C.c_float))))
+        return float(out[0])
+
+    def set_param(self, i, value):
+        """GuidingField::set_param (guide_field.hpp:73-77)."""
+        v = np.array([value], dtype=np.float32)
+        check(load().wostgpu_field_set_params(self.h, int(i), 1, v.ctypes.data_as(C.POINTER(C.c_float))))
+
+    def backward(self, xy, d_out, grad=None):
+        """eval_with_tape + backward (guide_field.cpp:223-243, 258-315) for
+        every point: grad += sum_i J(x_i)^T d_out[i] (fp64); returns grad."""
+        xy = _xy(xy)
+        d_out = np.ascontiguousarray(d_out, dtype=np.float64).reshape(len(xy), self.output_dim)
+        g = np.zeros(self.n_params) if grad is None else grad
+        assert g.dtype == np.float64 and g.shape == (self.n_params,) and g.flags.c_contiguous
+        check(load().wostgpu_field_backward(self.h, len(xy), _d(xy), _d(d_out), _d(g)))
+        return g
+
+    def adam_step(self, grad, lr, beta1, beta2, eps):
+        """GuidingField::adam_step (guide_field.cpp:317-331); zeroes grad."""
+        assert grad.dtype == np.float64 and grad.shape == (self.n_params,) and grad.flags.c_contiguous
+        check(load().wostgpu_field_adam_step(self.h, _d(grad), lr, beta1, beta2, eps))
+
     # WGF1 checkpoints, byte-compatible with GuidingField::save / load
     # (guide_field.cpp:333-411); see include/wostgpu.hpp for the layout
     def save(self, path):

@@ -139,9 +139,10 @@ __device__ __forceinline__ bool ray_tri(D3 o, D3 d, D3 a, D3 b, D3 c, double* t)
   return true;
 }
 
-// slab test against [0, t_hi] with precomputed inverse direction
+// slab test against [0, t_hi] with precomputed inverse direction; on a hit
+// *t_in is the entry parameter (>= 0)
 __device__ __forceinline__ bool ray_box(D3 o, D3 inv, const bool* dz, const float4& lo,
-                                        const float4& hi, double t_hi) {
+                                        const float4& hi, double t_hi, double* t_in) {
   double t0 = 0.0, t1 = t_hi;
   const double oo[3] = {o.x, o.y, o.z}, iv[3] = {inv.x, inv.y, inv.z};
   const double l[3] = {lo.x, lo.y, lo.z}, h[3] = {hi.x, hi.y, hi.z};
@@ -161,8 +162,22 @@ __device__ __forceinline__ bool ray_box(D3 o, D3 inv, const bool* dz, const floa
     t1 = fmin(t1, tb);
     if (t0 > t1) return false;
   }
+  *t_in = t0;
   return true;
 }
+
+// Traversal stack entry: a node still to visit and a LOWER bound of its key
+// (box distance^2 or ray entry t) rounded down to fp32. A popped entry whose
+// bound already exceeds the current best is dropped without loading the
+// node; a bound that passes only visits a node the exact test might have
+// skipped, so results (minima over (key, id)) are unchanged. The descent
+// keeps the nearer child's box in registers, so each level costs one round
+// of (two independent) node loads.
+struct StackEnt {
+  int node;
+  float key;
+};
+constexpr int kStack = 64;
 
 struct CP3 {
   D3 p;
@@ -173,14 +188,14 @@ struct CP3 {
 
 __device__ __forceinline__ void cp_bvh(const Node3* nodes, const Tri3* tris, D3 x, CP3& best) {
   if (!nodes) return;
-  int stack[64];
+  StackEnt stack[kStack];
   int sp = 0;
-  stack[sp++] = 0;
-  while (sp) {
-    float4 lo, hi;
-    ld_node(nodes + stack[--sp], lo, hi);
-    if (box_d2(lo, hi, x) > best.d2) continue;
-    int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
+  float4 lo, hi;
+  ld_node(nodes, lo, hi);
+  if (box_d2(lo, hi, x) > best.d2) return;
+  for (;;) {
+    const int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
+    bool descend = false;
     if (b < 0) {
       for (int i = a; i < a - b; ++i) {
         const Tri3& t = tris[i];
@@ -195,19 +210,31 @@ __device__ __forceinline__ void cp_bvh(const Node3* nodes, const Tri3* tris, D3 
           best.local = i;
         }
       }
-      continue;
-    }
-    float4 alo, ahi, blo, bhi;
-    ld_node(nodes + a, alo, ahi);
-    ld_node(nodes + b, blo, bhi);
-    double da = box_d2(alo, ahi, x), db = box_d2(blo, bhi, x);
-    if (da <= db) {  // nearer child on top
-      stack[sp++] = b;
-      stack[sp++] = a;
     } else {
-      stack[sp++] = a;
-      stack[sp++] = b;
+      float4 alo, ahi, blo, bhi;
+      ld_node(nodes + a, alo, ahi);
+      ld_node(nodes + b, blo, bhi);
+      const double da = box_d2(alo, ahi, x), db = box_d2(blo, bhi, x);
+      const bool a_near = da <= db;
+      const double dn = a_near ? da : db, df = a_near ? db : da;
+      if (df <= best.d2) stack[sp++] = {a_near ? b : a, __double2float_rd(df)};
+      if (dn <= best.d2) {
+        lo = a_near ? alo : blo;
+        hi = a_near ? ahi : bhi;
+        descend = true;
+      }
     }
+    if (descend) continue;
+    int next = -1;
+    while (sp) {
+      const StackEnt e = stack[--sp];
+      if (static_cast<double>(e.key) <= best.d2) {
+        next = e.node;
+        break;
+      }
+    }
+    if (next < 0) return;
+    ld_node(nodes + next, lo, hi);
   }
 }
 
@@ -249,14 +276,14 @@ __device__ __forceinline__ double closest_silhouette_d2(const Scene3View& s, D3 
   const Node3* nodes = s.node[2];
   if (!nodes) return dinf();
   double best = bound2;
-  int stack[64];
+  StackEnt stack[kStack];
   int sp = 0;
-  stack[sp++] = 0;
-  while (sp) {
-    float4 lo, hi;
-    ld_node(nodes + stack[--sp], lo, hi);
-    if (box_d2(lo, hi, x) >= best) continue;
-    int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
+  float4 lo, hi;
+  ld_node(nodes, lo, hi);
+  if (box_d2(lo, hi, x) >= best) return best;
+  for (;;) {
+    const int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
+    bool descend = false;
     if (b < 0) {
       for (int i = a; i < a - b; ++i) {
         const Edge3& e = s.edge[i];
@@ -264,21 +291,32 @@ __device__ __forceinline__ double closest_silhouette_d2(const Scene3View& s, D3 
         D3 dq = sub(x, closest_on_seg(x, ld3(e.a), ld3(e.b)));
         best = fmin(best, dot(dq, dq));
       }
-      continue;
-    }
-    float4 alo, ahi, blo, bhi;
-    ld_node(nodes + a, alo, ahi);
-    ld_node(nodes + b, blo, bhi);
-    double da = box_d2(alo, ahi, x), db = box_d2(blo, bhi, x);
-    if (da <= db) {
-      stack[sp++] = b;
-      stack[sp++] = a;
     } else {
-      stack[sp++] = a;
-      stack[sp++] = b;
+      float4 alo, ahi, blo, bhi;
+      ld_node(nodes + a, alo, ahi);
+      ld_node(nodes + b, blo, bhi);
+      const double da = box_d2(alo, ahi, x), db = box_d2(blo, bhi, x);
+      const bool a_near = da <= db;
+      const double dn = a_near ? da : db, df = a_near ? db : da;
+      if (df < best) stack[sp++] = {a_near ? b : a, __double2float_rd(df)};
+      if (dn < best) {
+        lo = a_near ? alo : blo;
+        hi = a_near ? ahi : bhi;
+        descend = true;
+      }
     }
+    if (descend) continue;
+    int next = -1;
+    while (sp) {
+      const StackEnt e = stack[--sp];
+      if (static_cast<double>(e.key) < best) {
+        next = e.node;
+        break;
+      }
+    }
+    if (next < 0) return best;
+    ld_node(nodes + next, lo, hi);
   }
-  return best;
 }
 
 __device__ __forceinline__ double closest_silhouette(const Scene3View& s, D3 x) {
@@ -301,14 +339,15 @@ __device__ __forceinline__ void ray_bvh(const Node3* nodes, const Tri3* tris, in
   inv.x = dz[0] ? 0.0 : 1.0 / d.x;
   inv.y = dz[1] ? 0.0 : 1.0 / d.y;
   inv.z = dz[2] ? 0.0 : 1.0 / d.z;
-  int stack[64];
+  StackEnt stack[kStack];
   int sp = 0;
-  stack[sp++] = 0;
-  while (sp) {
-    float4 lo, hi;
-    ld_node(nodes + stack[--sp], lo, hi);
-    if (!ray_box(o, inv, dz, lo, hi, fmin(t_max, h.t))) continue;
-    int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
+  float4 lo, hi;
+  double tin;
+  ld_node(nodes, lo, hi);
+  if (!ray_box(o, inv, dz, lo, hi, fmin(t_max, h.t), &tin)) return;
+  for (;;) {
+    const int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
+    bool descend = false;
     if (b < 0) {
       for (int i = a; i < a - b; ++i) {
         const Tri3& t = tris[i];
@@ -324,10 +363,41 @@ __device__ __forceinline__ void ray_bvh(const Node3* nodes, const Tri3* tris, in
           h.kind = kind;
         }
       }
-      continue;
+    } else {
+      float4 alo, ahi, blo, bhi;
+      ld_node(nodes + a, alo, ahi);
+      ld_node(nodes + b, blo, bhi);
+      const double tb_ = fmin(t_max, h.t);
+      double ta = 0.0, tb = 0.0;
+      const bool ha = ray_box(o, inv, dz, alo, ahi, tb_, &ta);
+      const bool hb = ray_box(o, inv, dz, blo, bhi, tb_, &tb);
+      // nearer entry first (the first hit prunes the farther child sooner)
+      const bool a_first = ha && (!hb || ta <= tb);
+      if (ha && hb) {
+        stack[sp++] = {a_first ? b : a, __double2float_rd(a_first ? tb : ta)};
+        lo = a_first ? alo : blo;
+        hi = a_first ? ahi : bhi;
+        descend = true;
+      } else if (ha || hb) {
+        lo = ha ? alo : blo;
+        hi = ha ? ahi : bhi;
+        descend = true;
+      }
     }
-    stack[sp++] = b;
-    stack[sp++] = a;
+    if (descend) continue;
+    int next = -1;
+    while (sp) {
+      const StackEnt e = stack[--sp];
+      // entries are boxes hit within the bound at push time; the bound only
+      // shrinks (a hit at t < entry key cannot be beaten inside the box,
+      // except by a tie, so test with <=)
+      if (static_cast<double>(e.key) <= fmin(t_max, h.t)) {
+        next = e.node;
+        break;
+      }
+    }
+    if (next < 0) return;
+    ld_node(nodes + next, lo, hi);
   }
 }
 

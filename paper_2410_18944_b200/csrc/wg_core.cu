@@ -143,7 +143,124 @@ void field_layout(wg_field_s* f) {
   for (int i = 0; i < 4; ++i) v.bbox[i] = f->bbox[i];
 }
 
+// ---- GuidingField facade kernels (fp64, the reference's operation order;
+// this translation unit compiles with -fmad=false)
+constexpr int kTapeMax = 256;  // guide_field.cpp:260 (d_h2 / d_h1 / d_in of 256)
+
+// y[j] = b[j] + sum_i x[i] w[i][j], rows in pairs (guide_field.cpp:129-145)
+__device__ void affine64(const double* x, int rows, const float* w, const float* b, int cols, double* y) {
+  for (int j = 0; j < cols; ++j) y[j] = b[j];
+  int i = 0;
+  for (; i + 2 <= rows; i += 2) {
+    const double x0 = x[i], x1 = x[i + 1];
+    const float* w0 = w + static_cast<size_t>(i) * cols;
+    const float* w1 = w0 + cols;
+    for (int j = 0; j < cols; ++j) y[j] += x0 * w0[j] + x1 * w1[j];
+  }
+  for (; i < rows; ++i) {
+    const double xi = x[i];
+    const float* wr = w + static_cast<size_t>(i) * cols;
+    for (int j = 0; j < cols; ++j) y[j] += xi * wr[j];
+  }
+}
+
+// GuidingField::eval_with_tape + backward (guide_field.cpp:223-243, 258-315)
+// for one point per thread: grad += J(x)^T d_out, fp64 atomics
+__global__ void field_backward_kernel(FieldView f, int64_t n, const double* xy, const double* d_out,
+                                      double* grad) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const float* P = f.p;
+  double input[kTapeMax], h1pre[kTapeMax], h2pre[kTapeMax], h1[kTapeMax], h2[kTapeMax];
+  int64_t cidx[4 * WG_MAX_LEVELS];
+  double cw[4 * WG_MAX_LEVELS];
+  // gather_input (guide_field.cpp:80-123)
+  const double u = sclamp((xy[2 * t] - f.bbox[0]) / (f.bbox[2] - f.bbox[0]), 0.0, 1.0);
+  const double v = sclamp((xy[2 * t + 1] - f.bbox[1]) / (f.bbox[3] - f.bbox[1]), 0.0, 1.0);
+  for (int l = 0; l < f.levels; ++l) {
+    const int res = f.res[l];
+    const double px = u * (res - 1), py = v * (res - 1);
+    const int ix = imin(static_cast<int>(px), res - 2), iy = imin(static_cast<int>(py), res - 2);
+    const double fx = px - ix, fy = py - iy;
+    const int64_t c00 = f.lvl_off[l] + (static_cast<int64_t>(iy) * res + ix) * f.F;
+    const int64_t c10 = c00 + f.F, c01 = c00 + static_cast<int64_t>(res) * f.F, c11 = c01 + f.F;
+    const double w00 = (1.0 - fx) * (1.0 - fy), w10 = fx * (1.0 - fy), w01 = (1.0 - fx) * fy, w11 = fx * fy;
+    cidx[4 * l + 0] = c00;
+    cidx[4 * l + 1] = c10;
+    cidx[4 * l + 2] = c01;
+    cidx[4 * l + 3] = c11;
+    cw[4 * l + 0] = w00;
+    cw[4 * l + 1] = w10;
+    cw[4 * l + 2] = w01;
+    cw[4 * l + 3] = w11;
+    for (int i = 0; i < f.F; ++i)
+      input[l * f.F + i] = w00 * P[c00 + i] + w10 * P[c10 + i] + w01 * P[c01 + i] + w11 * P[c11 + i];
+  }
+  const int in = f.in, hid = f.hid, od = f.od;
+  affine64(input, in, P + f.w1, P + f.b1, hid, h1pre);
+  for (int i = 0; i < hid; ++i) h1[i] = h1pre[i] > 0.0 ? h1pre[i] : 0.0;
+  affine64(h1, hid, P + f.w2, P + f.b2, hid, h2pre);
+  for (int i = 0; i < hid; ++i) h2[i] = h2pre[i] > 0.0 ? h2pre[i] : 0.0;
+  // backward: d_h2 reuses h1pre's storage after its mask is read, etc.
+  const double* dout = d_out + t * od;
+  double* d_h2 = h2pre;  // masked in place below
+  for (int j = 0; j < od; ++j) atomicAdd(grad + f.b3 + j, dout[j]);
+  for (int i = 0; i < hid; ++i) {
+    const float* wr = P + f.w3 + static_cast<size_t>(i) * od;
+    double* gw = grad + f.w3 + static_cast<size_t>(i) * od;
+    double acc = 0.0;
+    for (int j = 0; j < od; ++j) {
+      atomicAdd(gw + j, h2[i] * dout[j]);
+      acc += wr[j] * dout[j];
+    }
+    d_h2[i] = h2pre[i] > 0.0 ? acc : 0.0;
+  }
+  double* d_h1 = h2;  // h2 is no longer needed
+  for (int j = 0; j < hid; ++j) atomicAdd(grad + f.b2 + j, d_h2[j]);
+  for (int i = 0; i < hid; ++i) {
+    const float* wr = P + f.w2 + static_cast<size_t>(i) * hid;
+    double* gw = grad + f.w2 + static_cast<size_t>(i) * hid;
+    double acc = 0.0;
+    for (int j = 0; j < hid; ++j) {
+      atomicAdd(gw + j, h1[i] * d_h2[j]);
+      acc += wr[j] * d_h2[j];
+    }
+    d_h1[i] = h1pre[i] > 0.0 ? acc : 0.0;
+  }
+  double* d_in = h1pre;
+  for (int j = 0; j < hid; ++j) atomicAdd(grad + f.b1 + j, d_h1[j]);
+  for (int i = 0; i < in; ++i) {
+    const float* wr = P + f.w1 + static_cast<size_t>(i) * hid;
+    double* gw = grad + f.w1 + static_cast<size_t>(i) * hid;
+    double acc = 0.0;
+    for (int j = 0; j < hid; ++j) {
+      atomicAdd(gw + j, input[i] * d_h1[j]);
+      acc += wr[j] * d_h1[j];
+    }
+    d_in[i] = acc;
+  }
+  for (int l = 0; l < f.levels; ++l)
+    for (int c = 0; c < 4; ++c)
+      for (int i = 0; i < f.F; ++i) atomicAdd(grad + cidx[4 * l + c] + i, cw[4 * l + c] * d_in[l * f.F + i]);
+}
+
+// GuidingField::adam_step (guide_field.cpp:317-331) on an fp64 gradient
+__global__ void field_adam64_kernel(float* p, double* m, double* v, const double* g, int64_t n, double lr,
+                                    double b1, double b2, double eps, long long step) {
+  const double bc1 = 1.0 - pow(b1, static_cast<double>(step));
+  const double bc2 = 1.0 - pow(b2, static_cast<double>(step));
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double gi = g[i];
+    const double mi = m[i] = b1 * m[i] + (1.0 - b1) * gi;
+    const double vi = v[i] = b2 * v[i] + (1.0 - b2) * gi * gi;
+    const double up = lr * (mi / bc1) / (sqrt(vi / bc2) + eps);
+    p[i] = static_cast<float>(static_cast<double>(p[i]) - up);
+  }
+}
+
 }  // namespace
+
 
 extern "C" {
 
@@ -503,6 +620,67 @@ int wostgpu_field_eval_batch(wg_field f, int64_t n, const double* xy, double* ou
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(out, dout.p, sizeof(double) * n * f->view.od, cudaMemcpyDeviceToHost));
   });
+}
+
+int wostgpu_field_get_params(wg_field f, int64_t offset, int64_t count, float* out) {
+  return guarded([&] {
+    need(f != nullptr && offset >= 0 && count >= 0 && offset + count <= f->n_params, WG_ERR_INVALID,
+         "parameter range out of bounds");
+    if (count == 0) return;
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(out, f->p.as<float>() + offset, sizeof(float) * count, cudaMemcpyDeviceToHost));
+  });
+}
+
+int wostgpu_field_set_params(wg_field f, int64_t offset, int64_t count, const float* in) {
+  return guarded([&] {
+    need(f != nullptr && offset >= 0 && count >= 0 && offset + count <= f->n_params, WG_ERR_INVALID,
+         "parameter range out of bounds");
+    if (count == 0) return;
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(f->p.as<float>() + offset, in, sizeof(float) * count, cudaMemcpyHostToDevice));
+    f->pack_dirty = true;
+  });
+}
+
+int wostgpu_field_backward(wg_field f, int64_t n, const double* xy, const double* d_out, double* grad) {
+  return guarded([&] {
+    need(f != nullptr && f->sdim == 2, WG_ERR_INVALID, "field_backward: 2D field expected");
+    need(f->view.in <= kTapeMax && f->view.hid <= kTapeMax, WG_ERR_NOT_BUILT, "field too wide for the tape");
+    if (n == 0) return;
+    DBuf dxy, dd, dg;
+    dxy.upload(xy, 2 * n);
+    dd.upload(d_out, static_cast<size_t>(n) * f->view.od);
+    dg.upload(grad, static_cast<size_t>(f->n_params));
+    field_backward_kernel<<<static_cast<unsigned>((n + 63) / 64), 64>>>(f->view, n, dxy.as<double>(),
+                                                                         dd.as<double>(), dg.as<double>());
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(grad, dg.p, sizeof(double) * f->n_params, cudaMemcpyDeviceToHost));
+  });
+}
+
+int wostgpu_field_adam_step(wg_field f, double* grad, double lr, double beta1, double beta2, double eps) {
+  return guarded([&] {
+    need(f != nullptr && grad != nullptr, WG_ERR_INVALID, "null argument");
+    CK(cudaDeviceSynchronize());
+    long long steps = 0;
+    CK(cudaMemcpy(&steps, f->adam.p, sizeof(long long), cudaMemcpyDeviceToHost));
+    ++steps;
+    DBuf dg;
+    dg.upload(grad, static_cast<size_t>(f->n_params));
+    field_adam64_kernel<<<sm_count() * 4, 256>>>(f->p.as<float>(), f->m.as<double>(), f->v.as<double>(),
+                                                  dg.as<double>(), f->n_params, lr, beta1, beta2, eps, steps);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(f->adam.p, &steps, sizeof(long long), cudaMemcpyHostToDevice));
+    f->pack_dirty = true;
+    for (int64_t i = 0; i < f->n_params; ++i) grad[i] = 0.0;  // as adam_step leaves it
+  });
+}
+
+int wostgpu_shutdown(void) {
+  return guarded([&] { CK(cudaDeviceSynchronize()); });
 }
 
 int wostgpu_normalize_params(int64_t n, const double* raw, int32_t k, int32_t dim, wg_mixture* out) {

@@ -30,20 +30,14 @@ int main(int argc, char** argv) {
   Scene s;
   s.bbox = {{0, 0}, {1, 1}};
   s.epsilon_shell = 1e-3 * std::sqrt(2.0);
-  auto constant = [](double v) {
-    wg_value_spec c{};
-    c.type = WG_VALUE_CONSTANT;
-    c.c0 = v;
-    return c;
-  };
-  wg_value_spec lin{};
-  lin.type = WG_VALUE_LINEAR;
-  lin.cy = 1.0;
-  s.values = {constant(0.0), lin, constant(0.0)};
-  s.segments = {{{0, 0}, {0, 1}, BoundaryKind::Dirichlet, 0},
-                {{1, 0}, {1, 1}, BoundaryKind::Dirichlet, 1},
-                {{0, 0}, {1, 0}, BoundaryKind::Neumann, 2},
-                {{0, 1}, {1, 1}, BoundaryKind::Neumann, 2}};
+  s.values = {{"zero", ValueSpec{ValueSpec::Constant{0.0}}},
+              {"y", ValueSpec{ValueSpec::Linear{0.0, 0.0, 1.0}}},
+              {"insulated", ValueSpec{ValueSpec::Constant{0.0}}}};
+  s.segments = {{{0, 0}, {0, 1}, BoundaryKind::Dirichlet, "zero"},
+                {{1, 0}, {1, 1}, BoundaryKind::Dirichlet, "y"},
+                {{0, 0}, {1, 0}, BoundaryKind::Neumann, "insulated"},
+                {{0, 1}, {1, 1}, BoundaryKind::Neumann, "insulated"}};
+  s.validate();
   Accel accel(s);
   std::vector<Vec2> pts;
   std::vector<double> ref;
@@ -66,7 +60,8 @@ int main(int argc, char** argv) {
   SolverConfig uc;
   StepContext uctx(accel, nullptr, uc);
   std::vector<PointStats> us(pts.size());
-  for (int b = 0; b < wpp; ++b) solve_batch(uctx, pts, us, 1, b, false, nullptr);
+  SolveScratch scratch;
+  for (int b = 0; b < wpp; ++b) solve_batch(uctx, pts, us, 1, b, false, nullptr, &scratch);
 
   FieldConfig fc;
   GuidingField field(fc, s.bbox, 1);

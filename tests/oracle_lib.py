@@ -94,6 +94,9 @@ class Oracle:
                 self.lib.ref_field_load.argtypes = [C.c_char_p]
                 self.lib.ref_field_adam_steps.restype = C.c_int64
                 self.lib.ref_field_adam_steps.argtypes = [VP]
+            if hasattr(self.lib, "ref_field_backward"):
+                self.lib.ref_field_backward.restype = None
+                self.lib.ref_field_backward.argtypes = [VP, C.c_int64, D, D, D]
             if hasattr(self.lib, "ref_field_adam_step"):
                 self.lib.ref_field_adam_step.restype = None
                 self.lib.ref_field_adam_step.argtypes = [VP, D, C.c_double, C.c_double, C.c_double,

@@ -472,3 +472,52 @@ def test_tail_handoff_records_and_estimate(gpu, rows):
     # 64 wpp guided on the strip: relMSE ~0.01-0.026 over training-noise
     # (fp32 atomics), uniform ~0.066 at the same samples
     assert d["relmse"] < 0.5 * d["relmse_uniform"], d
+
+
+def test_cpp_batched_accel_queries_match_oracle(gpu, orc, tmp_path):
+    """The batched Accel C-ABI entries called from C++ (tests/cpp/accel_queries.cpp)
+    on a 500-segment random scene with mixed kinds: closest point (3 kind
+    masks), closest silhouette, first ray hit and star radius bit-exact
+    against the oracle (proj/src/geom2d.cpp:142-255)."""
+    import subprocess
+    from test_host import build_cpp
+    exe = build_cpp(tmp_path, "accel_queries")
+    sc = random_scene(Rng(55, 1), 500)
+    xy = probes(Rng(55, 9), 3000, -0.2, 1.2)
+    rng = np.random.default_rng(4)
+    ang = rng.uniform(0, 2 * np.pi, len(xy))
+    d = np.stack([np.cos(ang), np.sin(ang)], 1)
+    tmax = np.where(rng.random(len(xy)) < 0.3, np.inf, rng.uniform(0.01, 1.0, len(xy)))
+    fin, fout = tmp_path / "in.bin", tmp_path / "out.bin"
+    with open(fin, "wb") as f:
+        f.write(np.array([sc.n_segments, len(xy)], dtype=np.int32).tobytes())
+        for a in (sc.seg.astype(np.float64), sc.kind.astype(np.int32), xy, d, tmax):
+            f.write(np.ascontiguousarray(a).tobytes())
+    subprocess.run([exe, str(fin), str(fout)], check=True, timeout=300)
+    buf = open(fout, "rb").read()
+    n = len(xy)
+    off = 0
+
+    def take(dt, count):
+        nonlocal off
+        a = np.frombuffer(buf, dt, count, off)
+        off += a.nbytes
+        return a
+
+    ho = orc.scene(sc)
+    for kinds in (1, 2, 3):
+        pt, dist, seg = take("<f8", 2 * n).reshape(n, 2), take("<f8", n), take("<i4", n)
+        po, do, so = orc.closest_point(ho, xy, kinds)
+        assert np.array_equal(pt, po) and np.array_equal(dist, do) and np.array_equal(seg, so)
+    assert np.array_equal(take("<f8", n), orc.closest_silhouette(ho, xy))
+    t, hp, nrm = take("<f8", n), take("<f8", 2 * n).reshape(n, 2), take("<f8", 2 * n).reshape(n, 2)
+    hs, hk = take("<i4", n), take("<i4", n)
+    to, po, no, so, ko = orc.ray_first_hit(ho, xy, d, tmax, 3)
+    assert np.array_equal(hs, so) and np.array_equal(t, to)
+    hit = so >= 0
+    assert hit.mean() > 0.2
+    assert np.array_equal(hp[hit], po[hit]) and np.array_equal(nrm[hit], no[hit]) and np.array_equal(hk[hit], ko[hit])
+    r = take("<f8", n)
+    ok = np.isfinite(r)
+    assert ok.mean() > 0.9
+    assert np.array_equal(r[ok], orc.star_radius(ho, xy[ok], 0.0))

@@ -163,3 +163,31 @@ def test_train_batch_accounting_matches_reference(gpu, ref, cap, mb):
     # Adam moves each parameter by ~lr * sign(mean gradient); fp32 vs fp64
     # sums flip signs only for gradients near 0
     assert np.median(d) < 1e-3 * lr and np.mean(d > 0.1 * lr) < 0.01, (np.median(d), np.mean(d > 0.1 * lr))
+
+
+def test_field_backward_adam_and_param_access_match_reference(gpu, ref):
+    """GuidingField facade entries against the reference's own methods:
+    eval_with_tape + backward (guide_field.cpp:223-315) summed over points
+    (fp64; the device sums points in another order), adam_step on that fp64
+    gradient (guide_field.cpp:317-331), get_param / set_param."""
+    cfg = abi.field_config()
+    fo = ref.field(cfg, BOX, 31)
+    fg = api.GuidingField(cfg, BOX, 31)
+    rng = np.random.default_rng(2)
+    xy = np.ascontiguousarray(rng.uniform(-0.1, 1.1, (300, 2)))
+    d_out = np.ascontiguousarray(rng.standard_normal((300, fg.output_dim)))
+    gr = np.zeros(fg.n_params)
+    ref.lib.ref_field_backward(fo, len(xy), abi.ptr(xy), abi.ptr(d_out), abi.ptr(gr))
+    gg = fg.backward(xy, d_out)
+    assert np.count_nonzero(gr) > 1000
+    np.testing.assert_allclose(gg, gr, rtol=1e-12, atol=1e-13 * np.abs(gr).max())
+    g1, g2 = gr.copy(), gr.copy()
+    ref.lib.ref_field_adam_step(fo, abi.ptr(g1), 1e-2, 0.9, 0.99, 1e-8)
+    fg.adam_step(g2, 1e-2, 0.9, 0.99, 1e-8)
+    assert not g2.any()  # zeroed, as the reference leaves it
+    pr, pg = ref.field_params(fo), fg.params()
+    assert (pr == pg).mean() >= 0.9999
+    ulp = np.abs(pr.view(np.int32).astype(np.int64) - pg.view(np.int32).astype(np.int64))
+    assert ulp.max() <= 1
+    fg.set_param(fg.n_params - 1, 0.25)
+    assert fg.get_param(fg.n_params - 1) == 0.25 and fg.params()[-1] == np.float32(0.25)

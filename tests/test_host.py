@@ -113,16 +113,21 @@ def test_ctypes_struct_layouts_match_header(tmp_path):
     assert C.sizeof(abi.GuideRecord3) == abi.GUIDE_RECORD3_DTYPE.itemsize
 
 
-def build_facade_demo(out_dir):
-    """Compile tests/cpp/facade_demo.cpp (the C++ drop-in facade) with g++."""
+def build_cpp(out_dir, name):
+    """Compile tests/cpp/<name>.cpp (a C++ caller of the facade / C-ABI) with g++."""
     import subprocess
-    exe = os.path.join(str(out_dir), "facade_demo")
+    exe = os.path.join(str(out_dir), name)
     lib_dir = os.path.dirname(_lib.LIB_PATH)
     subprocess.run(["/usr/bin/g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
-                    os.path.join(ROOT, "tests", "cpp", "facade_demo.cpp"), "-o", exe, "-L", lib_dir,
+                    os.path.join(ROOT, "tests", "cpp", name + ".cpp"), "-o", exe, "-L", lib_dir,
                     "-lwostgpu", f"-Wl,-rpath,{lib_dir}"], check=True)
     return exe
 
 
+def build_facade_demo(out_dir):
+    return build_cpp(out_dir, "facade_demo")
+
+
 def test_cpp_facade_compiles_and_links(tmp_path):
     assert os.path.exists(build_facade_demo(tmp_path))
+    assert os.path.exists(build_cpp(tmp_path, "accel_queries"))
