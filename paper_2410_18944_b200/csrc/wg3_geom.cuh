@@ -27,15 +27,33 @@ namespace wg3 {
 
 using wg::dinf;
 
+// Pinned fp64 arithmetic: every product and sum rounded on its own, in the
+// oracle's order, in every translation unit. Kernels compiled with FMA
+// contraction (the tensor-core walk TUs) would otherwise fuse these
+// differently in different kernels (a product kept in a register in one,
+// stored to a wavefront lane in another), so the wavefront and lockstep
+// paths could part ways on a walk by one rounding.
+#ifdef __CUDA_ARCH__
+__device__ __forceinline__ double pm(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double pa(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double ps(double a, double b) { return __dsub_rn(a, b); }
+#else
+inline double pm(double a, double b) { return a * b; }
+inline double pa(double a, double b) { return a + b; }
+inline double ps(double a, double b) { return a - b; }
+#endif
+
 struct D3 {
   double x, y, z;
 };
-__host__ __device__ __forceinline__ D3 add(D3 a, D3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
-__host__ __device__ __forceinline__ D3 sub(D3 a, D3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
-__host__ __device__ __forceinline__ D3 scl(D3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
-__host__ __device__ __forceinline__ double dot(D3 a, D3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__host__ __device__ __forceinline__ D3 add(D3 a, D3 b) { return {pa(a.x, b.x), pa(a.y, b.y), pa(a.z, b.z)}; }
+__host__ __device__ __forceinline__ D3 sub(D3 a, D3 b) { return {ps(a.x, b.x), ps(a.y, b.y), ps(a.z, b.z)}; }
+__host__ __device__ __forceinline__ D3 scl(D3 a, double s) { return {pm(a.x, s), pm(a.y, s), pm(a.z, s)}; }
+__host__ __device__ __forceinline__ double dot(D3 a, D3 b) {
+  return pa(pa(pm(a.x, b.x), pm(a.y, b.y)), pm(a.z, b.z));
+}
 __host__ __device__ __forceinline__ D3 cross(D3 a, D3 b) {
-  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+  return {ps(pm(a.y, b.z), pm(a.z, b.y)), ps(pm(a.z, b.x), pm(a.x, b.z)), ps(pm(a.x, b.y), pm(a.y, b.x))};
 }
 
 struct __align__(16) Node3 {
@@ -81,7 +99,7 @@ __device__ __forceinline__ double box_d2(const float4& lo, const float4& hi, D3 
   double dx = fmax(fmax((double)lo.x - p.x, 0.0), p.x - (double)hi.x);
   double dy = fmax(fmax((double)lo.y - p.y, 0.0), p.y - (double)hi.y);
   double dz = fmax(fmax((double)lo.z - p.z, 0.0), p.z - (double)hi.z);
-  return dx * dx + dy * dy + dz * dz;
+  return pa(pa(pm(dx, dx), pm(dy, dy)), pm(dz, dz));
 }
 
 // closest point on triangle abc (oracle/wost3d.inc closest_on_tri)
@@ -92,7 +110,7 @@ __device__ __forceinline__ D3 closest_on_tri(D3 p, D3 a, D3 b, D3 c) {
   D3 bp = sub(p, b);
   double d3 = dot(ab, bp), d4 = dot(ac, bp);
   if (d3 >= 0.0 && d4 <= d3) return b;
-  double vc = d1 * d4 - d3 * d2;
+  double vc = ps(pm(d1, d4), pm(d3, d2));
   if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {
     double v = d1 / (d1 - d3);
     return add(a, scl(ab, v));
@@ -100,18 +118,18 @@ __device__ __forceinline__ D3 closest_on_tri(D3 p, D3 a, D3 b, D3 c) {
   D3 cp = sub(p, c);
   double d5 = dot(ab, cp), d6 = dot(ac, cp);
   if (d6 >= 0.0 && d5 <= d6) return c;
-  double vb = d5 * d2 - d1 * d6;
+  double vb = ps(pm(d5, d2), pm(d1, d6));
   if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
     double w = d2 / (d2 - d6);
     return add(a, scl(ac, w));
   }
-  double va = d3 * d6 - d5 * d4;
+  double va = ps(pm(d3, d6), pm(d5, d4));
   if (va <= 0.0 && (d4 - d3) >= 0.0 && (d5 - d6) >= 0.0) {
     double w = (d4 - d3) / ((d4 - d3) + (d5 - d6));
     return add(b, scl(sub(c, b), w));
   }
   double den = 1.0 / (va + vb + vc);
-  double v = vb * den, w = vc * den;
+  double v = pm(vb, den), w = pm(vc, den);
   return add(add(a, scl(ab, v)), scl(ac, w));
 }
 
@@ -421,7 +439,7 @@ __device__ __forceinline__ D3 hit_normal(const Scene3View& s, const Hit3& h, D3 
 
 __device__ __forceinline__ double value_at(const wg_value3_spec& v, D3 p) {
   if (v.type == WG_VALUE_CONSTANT) return v.c0;
-  return v.c0 + v.cx * p.x + v.cy * p.y + v.cz * p.z;
+  return pa(pa(pa(v.c0, pm(v.cx, p.x)), pm(v.cy, p.y)), pm(v.cz, p.z));
 }
 
 __device__ __forceinline__ bool bbox_contains(const Scene3View& s, D3 p, double pad) {

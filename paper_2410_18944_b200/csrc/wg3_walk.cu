@@ -23,6 +23,7 @@
 
 #include "wg3_runtime.hpp"
 #include "wg3_walk_common.cuh"
+#include "wg_wpack.cuh"
 
 namespace wg3 {
 
@@ -527,11 +528,8 @@ void enqueue3_rounds(wg_solver3_s* s, uint64_t seed, uint64_t wpp_first, int32_t
     // per training round); lockstep tiles below that (128^2 training rounds:
     // the wavefront's per-iteration launches dominate). WOSTGPU_WALK3 =
     // wave / lockstep forces one.
-    static const int force = [] {
-      const char* e = std::getenv("WOSTGPU_WALK3");
-      if (!e) return 0;
-      return std::string(e) == "wave" ? 1 : std::string(e) == "lockstep" ? 2 : 0;
-    }();
+    const char* fe = std::getenv("WOSTGPU_WALK3");
+    const int force = !fe ? 0 : std::string(fe) == "wave" ? 1 : std::string(fe) == "lockstep" ? 2 : 0;
     const bool wave = force == 1 || (force == 0 && s->n_points * n >= 65536);
     if (tc && wave) {
       const int64_t slots = std::min<int64_t>(s->n_points * n, (int64_t)sms * 16 * 128);
@@ -548,7 +546,9 @@ void enqueue3_rounds(wg_solver3_s* s, uint64_t seed, uint64_t wpp_first, int32_t
       if (!s->h_qlen) CK(cudaMallocHost(&s->h_qlen, 4 * sizeof(unsigned int)));
       Wave3 v{s->w_lanes.as<Lane3>(), s->w_dirs.as<Dir3>(), s->w_rec.as<int32_t>(), s->w_state.as<uint8_t>(),
               s->w_queue.as<int32_t>(), s->w_qlen.as<unsigned int>(), s->w_next.as<unsigned long long>(),
-              slots};
+              slots, nullptr};
+      s->w_blob.alloc(wg::wpack::FWD_BYTES);
+      v.wblob = s->w_blob.as<unsigned char>();
       int64_t launched = 0;
       CK(launch_walks3_wave(a, v, sms, s->h_qlen, &launched, s->st));
       g_launches += launched;

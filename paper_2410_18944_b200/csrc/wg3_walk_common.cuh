@@ -6,6 +6,9 @@
 // plus the record layout and the walk-lane state. Contract: oracle/wost3d.inc.
 #pragma once
 
+#include <cooperative_groups.h>
+#include <cooperative_groups/reduce.h>
+
 #include "wg3_field.cuh"
 #include "wg3_mix.cuh"
 #include "wg_kernels.cuh"
@@ -85,6 +88,16 @@ struct Lane3 {
   int64_t point, rec_base;
 };
 
+// next walk id from the hand-out counter, one atomic per group of lanes
+// claiming together
+__device__ __forceinline__ unsigned long long claim_walk(unsigned long long* counter) {
+  namespace cg = cooperative_groups;
+  const cg::coalesced_group g = cg::coalesced_threads();
+  unsigned long long base = 0;
+  if (g.thread_rank() == 0) base = atomicAdd(counter, static_cast<unsigned long long>(g.size()));
+  return g.shfl(base, 0) + g.thread_rank();
+}
+
 __device__ __forceinline__ void lane3_init(Lane3& w, const Walk3Args& a, int64_t id) {
   w.round = static_cast<int>(id / a.n_points);
   w.point = id - static_cast<int64_t>(w.round) * a.n_points;
@@ -111,11 +124,20 @@ __device__ __forceinline__ void finish3(Lane3& w, const Walk3Args& a, bool escap
   a.est[slot] = escaped ? 0.0 : w.acc;
   a.esc[slot] = escaped ? 1 : 0;
   if (a.steps) a.steps[slot] = w.depth;
-  atomicAdd(&a.counters[0], static_cast<unsigned long long>(w.depth));
-  if (escaped) atomicAdd(&a.counters[1], 1ull);
+  // step / escape totals: one atomic per group of lanes finishing together
+  // (a same-address atomic per walk serialises at L2)
+  namespace cg = cooperative_groups;
+  const cg::coalesced_group g = cg::coalesced_threads();
+  const unsigned long long steps = cg::reduce(g, static_cast<unsigned long long>(w.depth),
+                                              cg::plus<unsigned long long>());
+  const unsigned long long esc = cg::reduce(g, escaped ? 1ull : 0ull, cg::plus<unsigned long long>());
+  if (g.thread_rank() == 0) {
+    atomicAdd(&a.counters[0], steps);
+    if (esc) atomicAdd(&a.counters[1], esc);
+  }
   if (collect) {
     a.rec_tail[slot] = w.last_rec;
-    a.rec_term[slot] = escaped ? 0.0 : w.T * terminal + w.dacc;
+    a.rec_term[slot] = escaped ? 0.0 : pa(pm(w.T, terminal), w.dacc);
   }
   w.alive = false;
 }
@@ -131,7 +153,7 @@ __device__ __forceinline__ bool step_begin(Lane3& w, const Walk3Args& a, bool co
   const double dd = cd.tri >= 0 ? sqrt(cd.d2) : dinf();
   if (cd.tri >= 0 && dd <= a.sp.eps) {
     const double g = value_at(s.values[s.tri[0][cd.local].value], cd.p);
-    w.acc += w.T * g;
+    w.acc = pa(w.acc, pm(w.T, g));
     finish3(w, a, false, g, collect);
     return false;
   }
@@ -168,7 +190,7 @@ __device__ __forceinline__ bool step_begin(Lane3& w, const Walk3Args& a, bool co
       const D3 y = add(w.x, scl(dir, r));
       const Hit3 h = ray_first_hit(s, w.x, dir, r, WG_KIND_ALL, -1);
       const double wt = h.tri >= 0 ? 0.0 : R * R / 6.0;
-      if (wt != 0.0) contrib -= wt * (bbox_contains(s, y, 0.0) ? value_at(s.source, y) : 0.0);
+      if (wt != 0.0) contrib = ps(contrib, pm(wt, bbox_contains(s, y, 0.0) ? value_at(s.source, y) : 0.0));
     }
     if (s.has_flux) {  // sample_neumann_contrib (wost.cpp:89-109), d = 3
       const D3 dir = uniform_sample(w.rng, w.on_n, w.n);
@@ -185,8 +207,8 @@ __device__ __forceinline__ bool step_begin(Lane3& w, const Walk3Args& a, bool co
       }
       contrib += add_;
     }
-    w.acc += w.T * contrib;
-    w.dacc += w.T * contrib;
+    w.acc = pa(w.acc, pm(w.T, contrib));
+    w.dacc = pa(w.dacc, pm(w.T, contrib));
   }
   if (collect && w.rec_ok) {  // trace push (wost.cpp:206-214), chunks of 8 slots
     if (w.rec_left == 0) {
@@ -313,6 +335,7 @@ struct Wave3 {
   unsigned int* qlen;    // [2] queue lengths (double-buffered by iteration parity)
   unsigned long long* next_walk;  // walk-id hand-out counter
   int64_t slots;
+  unsigned char* wblob;  // [wg::wpack::FWD_BYTES] split-fp16 MLP weights, packed per call
 };
 // returns the number of kernels launched in *launches
 cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& w, int sms, unsigned int* h_qlen,

@@ -171,9 +171,13 @@ __global__ void __launch_bounds__(128, WG3_GEOM_MINB) wave_geom_kernel(Walk3Args
   const unsigned long long total = static_cast<unsigned long long>(a.n_points) * a.n_rounds;
   unsigned int* qlen = v.qlen + parity;
   unsigned long long started = 0;
+  // every walk id handed out: empty slots stay empty without touching their
+  // lane or the counter (the drain of a round; a stale read only costs work)
+  const bool exhausted = *reinterpret_cast<volatile unsigned long long*>(v.next_walk) >= total;
   for (int64_t slot = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; slot < v.slots;
        slot += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const uint8_t st = v.state[slot];
+    if (st != SLOT_NEED_MOVE && exhausted) continue;
     Lane3 w;
     // a collecting slot carries its record chunk (rec_base / rec_left) from
     // walk to walk, so the lane is loaded even when the slot is empty
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(128, WG3_GEOM_MINB) wave_geom_kernel(Walk3Args
     int rec = -1;
     for (int tries = 0; tries < 4 && !need; ++tries) {
       if (!w.alive) {
-        const unsigned long long id = atomicAdd(v.next_walk, 1ull);
+        const unsigned long long id = claim_walk(v.next_walk);
         if (id >= total) break;
         lane3_init(w, a, static_cast<int64_t>(id));
         if (!collect) {
@@ -209,12 +213,27 @@ __global__ void __launch_bounds__(128, WG3_GEOM_MINB) wave_geom_kernel(Walk3Args
   if ((threadIdx.x & 31) == 0 && started) atomicAdd(&a.counters[2], started);
 }
 
+// the field's MLP weights as the split-fp16 blob the direction kernel
+// fetches with one bulk copy (the wg_wpack.cuh forward layout; W3 has 41
+// outputs here): once per wavefront call, the weights are fixed during it
+__global__ void pack3_weights_kernel(Field3View f, unsigned char* blob) {
+  // blob = shared-memory image of [B1_HI, BAR)
+  wg::tc_stage_weights_raw(blob - wg::TcLayout::B1_HI, f.p, f.w1, f.b1, f.w2, f.b2, f.w3, f.b3, OD);
+}
+
 __global__ void __launch_bounds__(128, WG3_DIR_MINB) wave_dir_kernel(Walk3Args a, Wave3 v, int parity) {
   extern __shared__ __align__(128) unsigned char smem[];
   if (blockIdx.x == 0 && threadIdx.x == 0) v.qlen[parity ^ 1] = 0u;  // next geometry pass's queue
   const unsigned int n = v.qlen[parity];
   if (static_cast<unsigned int>(blockIdx.x) * 128u >= n) return;
-  tc3_prologue(smem, a.f);
+  // weights: one TMA bulk copy of the packed blob, overlapped with the TMEM
+  // allocation
+  wg::tc_fetch_weights(smem, v.wblob);
+  wg::tc_setup(smem);
+  wg::umma::fence_before();
+  __syncthreads();
+  wg::umma::fence_after();
+  wg::tc_wait_weights(smem);
   uint32_t phase = 0;
   for (unsigned int t = blockIdx.x; t * 128u < n; t += gridDim.x) {
     const unsigned int row = t * 128u + threadIdx.x;
@@ -260,6 +279,8 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsi
   cudaMemsetAsync(v.qlen, 0, 2 * sizeof(unsigned int), st);
   cudaMemsetAsync(v.next_walk, 0, sizeof(unsigned long long), st);
   if (a.recs) cudaMemsetAsync(v.lanes, 0, sizeof(Lane3) * static_cast<size_t>(v.slots), st);
+  pack3_weights_kernel<<<1, 256, 0, st>>>(a.f, v.wblob);
+  *launches += 1;
   const int geom_blocks = static_cast<int>((v.slots + 127) / 128);
   const int dir_blocks = sms * 3;
   for (int it = 0;; ++it) {

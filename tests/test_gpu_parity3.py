@@ -361,3 +361,29 @@ def test_field3_checkpoint_round_trip(gpu, tmp_path):
     assert a[3] == b[3] and a[3] >= 3
     x = probes3(9, 500)
     assert np.array_equal(f.eval_batch(x), g.eval_batch(x))
+
+
+@pytest.mark.parametrize("name", ["box-strip-vlin-obstacle", "box-strip-vlin"])
+@pytest.mark.parametrize("collect", [False, True])
+def test_wavefront_walks_equal_lockstep_per_walk(gpu, monkeypatch, name, collect):
+    """The wavefront pair (geometry pass + tensor-core direction pass)
+    against the lockstep tensor-core kernel: the
+    same PCG32 streams, the same tcgen05 MLP rows and the same exact
+    geometry minima, so every walk's estimate, escape flag and step count
+    is identical; with record collection the record counts match too."""
+    sc = make_preset3(name, n=24).scene
+    f = GuidingField3(abi.field_config3(), BOX, 8)
+    p = f.params() + np.float32(0.3) * np.random.default_rng(9).standard_normal(f.n_params).astype(np.float32)
+    f.set_params(p)
+    x = _outside_obstacle(probes3(21, 6000, 0.03, 0.97))
+    out = []
+    for mode in ("lockstep", "wave"):
+        monkeypatch.setenv("WOSTGPU_WALK3", mode)
+        s = Solver3(Accel3(sc), f, abi.solver_config("learnable_mis"), MLP_TENSOR)
+        s.set_points(x)
+        s.solve_rounds(4, 3, 1, collect=collect)
+        out.append(s.walks() + ((len(s.records()),) if collect else (0,)))
+    (ea, sa, na, ra), (eb, sb, nb, rb) = out
+    assert np.array_equal(sa, sb) and np.array_equal(na, nb)
+    assert np.array_equal(ea, eb)
+    assert ra == rb and (ra > 0) == collect
