@@ -8,7 +8,7 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 \
-           --expt-relaxed-constexpr -Xptxas -warn-spills
+           --expt-relaxed-constexpr -Xptxas -warn-spills $(EXTRA)
 PKG := paper_2410_18944_b200
 SRC := $(wildcard $(PKG)/csrc/*.cu)
 HDR := $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.hpp) include/wostgpu.h include/wostgpu3.h include/wostgpu_types.h

@@ -184,6 +184,13 @@ __device__ __forceinline__ bool ray_box(D3 o, D3 inv, const bool* dz, const floa
   return true;
 }
 
+#ifdef WG3_COUNT  // diagnostic build: traversal work per query type
+__device__ unsigned long long g3cnt[16];
+#define WG3_CNT(i, v) atomicAdd(&g3cnt[i], static_cast<unsigned long long>(v))
+#else
+#define WG3_CNT(i, v)
+#endif
+
 // Traversal stack entry: a node still to visit and a LOWER bound of its key
 // (box distance^2 or ray entry t) rounded down to fp32. A popped entry whose
 // bound already exceeds the current best is dropped without loading the
@@ -206,6 +213,11 @@ struct CP3 {
 
 __device__ __forceinline__ void cp_bvh(const Node3* nodes, const Tri3* tris, D3 x, CP3& best) {
   if (!nodes) return;
+#ifdef WG3_COUNT
+  int n_in = 0, n_pr = 0;
+  WG3_CNT(0, 1);
+  struct Flush { int& a; int& b; __device__ ~Flush() { WG3_CNT(1, a); WG3_CNT(2, b); } } fl{n_in, n_pr};
+#endif
   StackEnt stack[kStack];
   int sp = 0;
   float4 lo, hi;
@@ -215,6 +227,9 @@ __device__ __forceinline__ void cp_bvh(const Node3* nodes, const Tri3* tris, D3 
     const int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
     bool descend = false;
     if (b < 0) {
+#ifdef WG3_COUNT
+      n_pr += -b;
+#endif
       for (int i = a; i < a - b; ++i) {
         const Tri3& t = tris[i];
         D3 q = closest_on_tri(x, ld3(t.a), ld3(t.b), ld3(t.c));
@@ -229,6 +244,9 @@ __device__ __forceinline__ void cp_bvh(const Node3* nodes, const Tri3* tris, D3 
         }
       }
     } else {
+#ifdef WG3_COUNT
+      ++n_in;
+#endif
       float4 alo, ahi, blo, bhi;
       ld_node(nodes + a, alo, ahi);
       ld_node(nodes + b, blo, bhi);
@@ -294,6 +312,11 @@ __device__ __forceinline__ double closest_silhouette_d2(const Scene3View& s, D3 
   const Node3* nodes = s.node[2];
   if (!nodes) return dinf();
   double best = bound2;
+#ifdef WG3_COUNT
+  int n_in = 0, n_pr = 0;
+  WG3_CNT(3, 1);
+  struct Flush { int& a; int& b; __device__ ~Flush() { WG3_CNT(4, a); WG3_CNT(5, b); } } fl{n_in, n_pr};
+#endif
   StackEnt stack[kStack];
   int sp = 0;
   float4 lo, hi;
@@ -303,6 +326,9 @@ __device__ __forceinline__ double closest_silhouette_d2(const Scene3View& s, D3 
     const int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
     bool descend = false;
     if (b < 0) {
+#ifdef WG3_COUNT
+      n_pr += -b;
+#endif
       for (int i = a; i < a - b; ++i) {
         const Edge3& e = s.edge[i];
         if (!is_silhouette(e, x, s.sil_tol)) continue;
@@ -314,6 +340,9 @@ __device__ __forceinline__ double closest_silhouette_d2(const Scene3View& s, D3 
       ld_node(nodes + a, alo, ahi);
       ld_node(nodes + b, blo, bhi);
       const double da = box_d2(alo, ahi, x), db = box_d2(blo, bhi, x);
+#ifdef WG3_COUNT
+      ++n_in;
+#endif
       const bool a_near = da <= db;
       const double dn = a_near ? da : db, df = a_near ? db : da;
       if (df < best) stack[sp++] = {a_near ? b : a, __double2float_rd(df)};
@@ -357,6 +386,11 @@ __device__ __forceinline__ void ray_bvh(const Node3* nodes, const Tri3* tris, in
   inv.x = dz[0] ? 0.0 : 1.0 / d.x;
   inv.y = dz[1] ? 0.0 : 1.0 / d.y;
   inv.z = dz[2] ? 0.0 : 1.0 / d.z;
+#ifdef WG3_COUNT
+  int n_in = 0, n_pr = 0;
+  WG3_CNT(6, 1);
+  struct Flush { int& a; int& b; __device__ ~Flush() { WG3_CNT(7, a); WG3_CNT(8, b); } } fl{n_in, n_pr};
+#endif
   StackEnt stack[kStack];
   int sp = 0;
   float4 lo, hi;
@@ -367,6 +401,9 @@ __device__ __forceinline__ void ray_bvh(const Node3* nodes, const Tri3* tris, in
     const int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
     bool descend = false;
     if (b < 0) {
+#ifdef WG3_COUNT
+      n_pr += -b;
+#endif
       for (int i = a; i < a - b; ++i) {
         const Tri3& t = tris[i];
         int id = t.id;
@@ -385,6 +422,9 @@ __device__ __forceinline__ void ray_bvh(const Node3* nodes, const Tri3* tris, in
       float4 alo, ahi, blo, bhi;
       ld_node(nodes + a, alo, ahi);
       ld_node(nodes + b, blo, bhi);
+#ifdef WG3_COUNT
+      ++n_in;
+#endif
       const double tb_ = fmin(t_max, h.t);
       double ta = 0.0, tb = 0.0;
       const bool ha = ray_box(o, inv, dz, alo, ahi, tb_, &ta);

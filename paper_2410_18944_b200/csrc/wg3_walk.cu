@@ -539,6 +539,7 @@ void enqueue3_rounds(wg_solver3_s* s, uint64_t seed, uint64_t wpp_first, int32_t
         s->w_rec.alloc(sizeof(int32_t) * slots);
         s->w_state.alloc(slots);
         s->w_queue.alloc(sizeof(int32_t) * slots);
+        s->w_perm.alloc(sizeof(int32_t) * slots);
         s->w_slots = slots;
       }
       s->w_qlen.alloc(2 * sizeof(unsigned int));
@@ -549,6 +550,9 @@ void enqueue3_rounds(wg_solver3_s* s, uint64_t seed, uint64_t wpp_first, int32_t
               slots, nullptr};
       s->w_blob.alloc(wg::wpack::FWD_BYTES);
       v.wblob = s->w_blob.as<unsigned char>();
+      s->w_bins.alloc(sizeof(unsigned int) * (kSortBins + 3));
+      v.perm = s->w_perm.as<int32_t>();
+      v.bins = s->w_bins.as<unsigned int>();
       int64_t launched = 0;
       CK(launch_walks3_wave(a, v, sms, s->h_qlen, &launched, s->st));
       g_launches += launched;

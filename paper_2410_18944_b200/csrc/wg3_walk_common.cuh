@@ -98,6 +98,16 @@ __device__ __forceinline__ unsigned long long claim_walk(unsigned long long* cou
   return g.shfl(base, 0) + g.thread_rank();
 }
 
+// slot of a queue with a shared length counter, one atomic per group of
+// lanes appending together
+__device__ __forceinline__ unsigned int claim_queue(unsigned int* len) {
+  namespace cg = cooperative_groups;
+  const cg::coalesced_group g = cg::coalesced_threads();
+  unsigned int base = 0;
+  if (g.thread_rank() == 0) base = atomicAdd(len, g.size());
+  return g.shfl(base, 0) + g.thread_rank();
+}
+
 __device__ __forceinline__ void lane3_init(Lane3& w, const Walk3Args& a, int64_t id) {
   w.round = static_cast<int>(id / a.n_points);
   w.point = id - static_cast<int64_t>(w.round) * a.n_points;
@@ -336,7 +346,14 @@ struct Wave3 {
   unsigned long long* next_walk;  // walk-id hand-out counter
   int64_t slots;
   unsigned char* wblob;  // [wg::wpack::FWD_BYTES] split-fp16 MLP weights, packed per call
+  int32_t* perm;         // [slots] geometry-pass order: slots grouped by spatial cell
+  unsigned int* bins;    // [kSortBins + 3] cell histogram / offsets, [+1] entries in perm, [+2] skip
 };
+#ifndef WG3_SORT_BITS
+#define WG3_SORT_BITS 4
+#endif
+constexpr int kSortBits = WG3_SORT_BITS;              // per axis
+constexpr int kSortBins = 1 << (3 * kSortBits);       // + 1 bin for slots without a pending move
 // returns the number of kernels launched in *launches
 cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& w, int sms, unsigned int* h_qlen,
                                int64_t* launches, cudaStream_t st);
