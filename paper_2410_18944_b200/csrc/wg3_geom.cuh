@@ -27,20 +27,22 @@ namespace wg3 {
 
 using wg::dinf;
 
-// Pinned fp64 arithmetic: every product and sum rounded on its own, in the
-// oracle's order, in every translation unit. Kernels compiled with FMA
-// contraction (the tensor-core walk TUs) would otherwise fuse these
+// Pinned fp64 arithmetic in translation units that contract FMAs (the
+// tensor-core walk TU defines WG3_PIN_FP): every product and sum rounded on
+// its own, in the oracle's order. Contraction would otherwise fuse these
 // differently in different kernels (a product kept in a register in one,
 // stored to a wavefront lane in another), so the wavefront and lockstep
-// paths could part ways on a walk by one rounding.
-#ifdef __CUDA_ARCH__
+// paths could part ways on a walk by one rounding. The -fmad=false TUs get
+// the same roundings from plain operators (pinning them there measured 7.7%
+// slower on uniform walks); pinning costs the wavefront 2.7% (cfg 4 shape).
+#if defined(__CUDA_ARCH__) && defined(WG3_PIN_FP)
 __device__ __forceinline__ double pm(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double pa(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double ps(double a, double b) { return __dsub_rn(a, b); }
 #else
-inline double pm(double a, double b) { return a * b; }
-inline double pa(double a, double b) { return a + b; }
-inline double ps(double a, double b) { return a - b; }
+__host__ __device__ inline double pm(double a, double b) { return a * b; }
+__host__ __device__ inline double pa(double a, double b) { return a + b; }
+__host__ __device__ inline double ps(double a, double b) { return a - b; }
 #endif
 
 struct D3 {
@@ -157,10 +159,9 @@ __device__ __forceinline__ bool ray_tri(D3 o, D3 d, D3 a, D3 b, D3 c, double* t)
   return true;
 }
 
-// slab test against [0, t_hi] with precomputed inverse direction; on a hit
-// *t_in is the entry parameter (>= 0)
+// slab test against [0, t_hi] with precomputed inverse direction
 __device__ __forceinline__ bool ray_box(D3 o, D3 inv, const bool* dz, const float4& lo,
-                                        const float4& hi, double t_hi, double* t_in) {
+                                        const float4& hi, double t_hi) {
   double t0 = 0.0, t1 = t_hi;
   const double oo[3] = {o.x, o.y, o.z}, iv[3] = {inv.x, inv.y, inv.z};
   const double l[3] = {lo.x, lo.y, lo.z}, h[3] = {hi.x, hi.y, hi.z};
@@ -180,29 +181,8 @@ __device__ __forceinline__ bool ray_box(D3 o, D3 inv, const bool* dz, const floa
     t1 = fmin(t1, tb);
     if (t0 > t1) return false;
   }
-  *t_in = t0;
   return true;
 }
-
-#ifdef WG3_COUNT  // diagnostic build: traversal work per query type
-__device__ unsigned long long g3cnt[16];
-#define WG3_CNT(i, v) atomicAdd(&g3cnt[i], static_cast<unsigned long long>(v))
-#else
-#define WG3_CNT(i, v)
-#endif
-
-// Traversal stack entry: a node still to visit and a LOWER bound of its key
-// (box distance^2 or ray entry t) rounded down to fp32. A popped entry whose
-// bound already exceeds the current best is dropped without loading the
-// node; a bound that passes only visits a node the exact test might have
-// skipped, so results (minima over (key, id)) are unchanged. The descent
-// keeps the nearer child's box in registers, so each level costs one round
-// of (two independent) node loads.
-struct StackEnt {
-  int node;
-  float key;
-};
-constexpr int kStack = 64;
 
 struct CP3 {
   D3 p;
@@ -213,23 +193,15 @@ struct CP3 {
 
 __device__ __forceinline__ void cp_bvh(const Node3* nodes, const Tri3* tris, D3 x, CP3& best) {
   if (!nodes) return;
-#ifdef WG3_COUNT
-  int n_in = 0, n_pr = 0;
-  WG3_CNT(0, 1);
-  struct Flush { int& a; int& b; __device__ ~Flush() { WG3_CNT(1, a); WG3_CNT(2, b); } } fl{n_in, n_pr};
-#endif
-  StackEnt stack[kStack];
+  int stack[64];
   int sp = 0;
-  float4 lo, hi;
-  ld_node(nodes, lo, hi);
-  if (box_d2(lo, hi, x) > best.d2) return;
-  for (;;) {
-    const int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
-    bool descend = false;
+  stack[sp++] = 0;
+  while (sp) {
+    float4 lo, hi;
+    ld_node(nodes + stack[--sp], lo, hi);
+    if (box_d2(lo, hi, x) > best.d2) continue;
+    int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
     if (b < 0) {
-#ifdef WG3_COUNT
-      n_pr += -b;
-#endif
       for (int i = a; i < a - b; ++i) {
         const Tri3& t = tris[i];
         D3 q = closest_on_tri(x, ld3(t.a), ld3(t.b), ld3(t.c));
@@ -243,34 +215,19 @@ __device__ __forceinline__ void cp_bvh(const Node3* nodes, const Tri3* tris, D3 
           best.local = i;
         }
       }
+      continue;
+    }
+    float4 alo, ahi, blo, bhi;
+    ld_node(nodes + a, alo, ahi);
+    ld_node(nodes + b, blo, bhi);
+    double da = box_d2(alo, ahi, x), db = box_d2(blo, bhi, x);
+    if (da <= db) {  // nearer child on top
+      stack[sp++] = b;
+      stack[sp++] = a;
     } else {
-#ifdef WG3_COUNT
-      ++n_in;
-#endif
-      float4 alo, ahi, blo, bhi;
-      ld_node(nodes + a, alo, ahi);
-      ld_node(nodes + b, blo, bhi);
-      const double da = box_d2(alo, ahi, x), db = box_d2(blo, bhi, x);
-      const bool a_near = da <= db;
-      const double dn = a_near ? da : db, df = a_near ? db : da;
-      if (df <= best.d2) stack[sp++] = {a_near ? b : a, __double2float_rd(df)};
-      if (dn <= best.d2) {
-        lo = a_near ? alo : blo;
-        hi = a_near ? ahi : bhi;
-        descend = true;
-      }
+      stack[sp++] = a;
+      stack[sp++] = b;
     }
-    if (descend) continue;
-    int next = -1;
-    while (sp) {
-      const StackEnt e = stack[--sp];
-      if (static_cast<double>(e.key) <= best.d2) {
-        next = e.node;
-        break;
-      }
-    }
-    if (next < 0) return;
-    ld_node(nodes + next, lo, hi);
   }
 }
 
@@ -312,58 +269,36 @@ __device__ __forceinline__ double closest_silhouette_d2(const Scene3View& s, D3 
   const Node3* nodes = s.node[2];
   if (!nodes) return dinf();
   double best = bound2;
-#ifdef WG3_COUNT
-  int n_in = 0, n_pr = 0;
-  WG3_CNT(3, 1);
-  struct Flush { int& a; int& b; __device__ ~Flush() { WG3_CNT(4, a); WG3_CNT(5, b); } } fl{n_in, n_pr};
-#endif
-  StackEnt stack[kStack];
+  int stack[64];
   int sp = 0;
-  float4 lo, hi;
-  ld_node(nodes, lo, hi);
-  if (box_d2(lo, hi, x) >= best) return best;
-  for (;;) {
-    const int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
-    bool descend = false;
+  stack[sp++] = 0;
+  while (sp) {
+    float4 lo, hi;
+    ld_node(nodes + stack[--sp], lo, hi);
+    if (box_d2(lo, hi, x) >= best) continue;
+    int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
     if (b < 0) {
-#ifdef WG3_COUNT
-      n_pr += -b;
-#endif
       for (int i = a; i < a - b; ++i) {
         const Edge3& e = s.edge[i];
         if (!is_silhouette(e, x, s.sil_tol)) continue;
         D3 dq = sub(x, closest_on_seg(x, ld3(e.a), ld3(e.b)));
         best = fmin(best, dot(dq, dq));
       }
+      continue;
+    }
+    float4 alo, ahi, blo, bhi;
+    ld_node(nodes + a, alo, ahi);
+    ld_node(nodes + b, blo, bhi);
+    double da = box_d2(alo, ahi, x), db = box_d2(blo, bhi, x);
+    if (da <= db) {
+      stack[sp++] = b;
+      stack[sp++] = a;
     } else {
-      float4 alo, ahi, blo, bhi;
-      ld_node(nodes + a, alo, ahi);
-      ld_node(nodes + b, blo, bhi);
-      const double da = box_d2(alo, ahi, x), db = box_d2(blo, bhi, x);
-#ifdef WG3_COUNT
-      ++n_in;
-#endif
-      const bool a_near = da <= db;
-      const double dn = a_near ? da : db, df = a_near ? db : da;
-      if (df < best) stack[sp++] = {a_near ? b : a, __double2float_rd(df)};
-      if (dn < best) {
-        lo = a_near ? alo : blo;
-        hi = a_near ? ahi : bhi;
-        descend = true;
-      }
+      stack[sp++] = a;
+      stack[sp++] = b;
     }
-    if (descend) continue;
-    int next = -1;
-    while (sp) {
-      const StackEnt e = stack[--sp];
-      if (static_cast<double>(e.key) < best) {
-        next = e.node;
-        break;
-      }
-    }
-    if (next < 0) return best;
-    ld_node(nodes + next, lo, hi);
   }
+  return best;
 }
 
 __device__ __forceinline__ double closest_silhouette(const Scene3View& s, D3 x) {
@@ -386,24 +321,15 @@ __device__ __forceinline__ void ray_bvh(const Node3* nodes, const Tri3* tris, in
   inv.x = dz[0] ? 0.0 : 1.0 / d.x;
   inv.y = dz[1] ? 0.0 : 1.0 / d.y;
   inv.z = dz[2] ? 0.0 : 1.0 / d.z;
-#ifdef WG3_COUNT
-  int n_in = 0, n_pr = 0;
-  WG3_CNT(6, 1);
-  struct Flush { int& a; int& b; __device__ ~Flush() { WG3_CNT(7, a); WG3_CNT(8, b); } } fl{n_in, n_pr};
-#endif
-  StackEnt stack[kStack];
+  int stack[64];
   int sp = 0;
-  float4 lo, hi;
-  double tin;
-  ld_node(nodes, lo, hi);
-  if (!ray_box(o, inv, dz, lo, hi, fmin(t_max, h.t), &tin)) return;
-  for (;;) {
-    const int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
-    bool descend = false;
+  stack[sp++] = 0;
+  while (sp) {
+    float4 lo, hi;
+    ld_node(nodes + stack[--sp], lo, hi);
+    if (!ray_box(o, inv, dz, lo, hi, fmin(t_max, h.t))) continue;
+    int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
     if (b < 0) {
-#ifdef WG3_COUNT
-      n_pr += -b;
-#endif
       for (int i = a; i < a - b; ++i) {
         const Tri3& t = tris[i];
         int id = t.id;
@@ -418,44 +344,10 @@ __device__ __forceinline__ void ray_bvh(const Node3* nodes, const Tri3* tris, in
           h.kind = kind;
         }
       }
-    } else {
-      float4 alo, ahi, blo, bhi;
-      ld_node(nodes + a, alo, ahi);
-      ld_node(nodes + b, blo, bhi);
-#ifdef WG3_COUNT
-      ++n_in;
-#endif
-      const double tb_ = fmin(t_max, h.t);
-      double ta = 0.0, tb = 0.0;
-      const bool ha = ray_box(o, inv, dz, alo, ahi, tb_, &ta);
-      const bool hb = ray_box(o, inv, dz, blo, bhi, tb_, &tb);
-      // nearer entry first (the first hit prunes the farther child sooner)
-      const bool a_first = ha && (!hb || ta <= tb);
-      if (ha && hb) {
-        stack[sp++] = {a_first ? b : a, __double2float_rd(a_first ? tb : ta)};
-        lo = a_first ? alo : blo;
-        hi = a_first ? ahi : bhi;
-        descend = true;
-      } else if (ha || hb) {
-        lo = ha ? alo : blo;
-        hi = ha ? ahi : bhi;
-        descend = true;
-      }
+      continue;
     }
-    if (descend) continue;
-    int next = -1;
-    while (sp) {
-      const StackEnt e = stack[--sp];
-      // entries are boxes hit within the bound at push time; the bound only
-      // shrinks (a hit at t < entry key cannot be beaten inside the box,
-      // except by a tie, so test with <=)
-      if (static_cast<double>(e.key) <= fmin(t_max, h.t)) {
-        next = e.node;
-        break;
-      }
-    }
-    if (next < 0) return;
-    ld_node(nodes + next, lo, hi);
+    stack[sp++] = b;
+    stack[sp++] = a;
   }
 }
 

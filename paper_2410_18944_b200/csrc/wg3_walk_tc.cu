@@ -15,6 +15,7 @@
 // Weights are split into fp16 hi/lo once per CTA from the fp32 parameters.
 // This translation unit may contract FMAs (Makefile FAST_TUS): its results
 // are compared with the oracle statistically, the exact kernel bit for bit.
+#define WG3_PIN_FP 1  // pinned geometry arithmetic (wg3_geom.cuh)
 #include "wg3_mix32.cuh"
 #include "wg3_walk_common.cuh"
 #include "wg_mlp_tc.cuh"
@@ -455,15 +456,3 @@ cudaError_t launch_field3_eval_tc(const Field3View& f, int64_t n, const double* 
 }
 
 }  // namespace wg3
-
-#ifdef WG3_COUNT
-extern "C" int wostgpu_debug_counts3(unsigned long long* out, int reset) {
-  cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, wg3::g3cnt, sizeof(unsigned long long) * 16);
-  if (reset) {
-    unsigned long long z[16] = {};
-    cudaMemcpyToSymbol(wg3::g3cnt, z, sizeof(z));
-  }
-  return 0;
-}
-#endif
