@@ -221,6 +221,12 @@ int wostgpu_run_profile(wg_solver solver, double* walk_ms, double* train_ms, int
 /* NCCL communicator for gradient allreduce (one rank per GPU). Rank 0 calls
  * wostgpu_comm_unique_id and broadcasts the 128 bytes out of band. */
 int wostgpu_comm_unique_id(char id[128]);
+/* Record arena capacity (records per collecting round) of the following
+ * calls, at least n. A training round whose records overflow the arena
+ * fails its call with WG_ERR_RUNTIME (and doubles the arena) instead of
+ * training on a short-walk-biased subset; the default holds 256 records per
+ * point. */
+int wostgpu_solver_reserve_records(wg_solver solver, int64_t n);
 int wostgpu_solver_attach_comm(wg_solver solver, const char id[128], int32_t nranks,
                                int32_t rank);
 

@@ -101,6 +101,8 @@ int wostgpu_solver3_run(wg_solver3 solver, uint64_t seed, int32_t wpp, int64_t t
 int wostgpu_solver3_run_profile(wg_solver3 solver, double* walk_ms, double* train_ms,
                                 int64_t* walks, int64_t* steps, int64_t* escaped,
                                 int64_t* train_steps);
+/* as wostgpu_solver_reserve_records (default: 48 records per point) */
+int wostgpu_solver3_reserve_records(wg_solver3 solver, int64_t n);
 int wostgpu_solver3_attach_comm(wg_solver3 solver, const char id[128], int32_t nranks,
                                 int32_t rank);
 

@@ -78,6 +78,8 @@ _SIGS = {
     "wostgpu_field_backward": (C.c_int, [VP, C.c_int64, D, D, D]),
     "wostgpu_field_adam_step": (C.c_int, [VP, D, C.c_double, C.c_double, C.c_double, C.c_double]),
     "wostgpu_shutdown": (C.c_int, []),
+    "wostgpu_solver_reserve_records": (C.c_int, [VP, C.c_int64]),
+    "wostgpu_solver3_reserve_records": (C.c_int, [VP, C.c_int64]),
     "wostgpu_train_prepare": (C.c_int, [VP, C.POINTER(abi.TrainConfig), I64]),
     "wostgpu_train_select": (C.c_int, [VP, C.POINTER(abi.TrainConfig), C.c_int64, I32]),
     "wostgpu_train_minibatch_grad": (C.c_int, [VP, C.POINTER(abi.TrainConfig), C.c_int32, F32]),

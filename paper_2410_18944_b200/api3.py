@@ -264,5 +264,11 @@ class Solver3:
         out["walk_ms"], out["train_ms"] = w.value, t.value
         return out
 
+    def reserve_records(self, n):
+        """Record arena of at least n records per collecting round (a round
+        that overflows the arena fails its call instead of training on a
+        short-walk-biased subset)."""
+        check(load().wostgpu_solver3_reserve_records(self.h, int(n)))
+
     def attach_comm(self, unique_id: bytes, nranks, rank):
         check(load().wostgpu_solver3_attach_comm(self.h, unique_id, nranks, rank))

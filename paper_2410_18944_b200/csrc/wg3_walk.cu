@@ -679,10 +679,15 @@ wg_train_stats sync3(wg_solver3_s* s, long long steps_before) {
   CK(cudaStreamSynchronize(s->st));
   unsigned long long c[C_N];
   CK(cudaMemcpy(c, s->counters.p, sizeof(c), cudaMemcpyDeviceToHost));
-  if (c[C_REC_OVERFLOW] > 0) {
+  if (c[C_REC_OVERFLOW] > 0) {  // as in 2D (wg_solver.cu sync_collect): fail, grow for the next call
     s->rec_cap_min = std::max<int64_t>(s->rec_cap_min, 2 * s->rec_cap);
-    std::fprintf(stderr, "wostgpu: 3D record arena overflow (%llu chunks dropped, capacity %lld); the next call uses %lld\n",
-                 c[C_REC_OVERFLOW], static_cast<long long>(s->rec_cap), static_cast<long long>(s->rec_cap_min));
+    char msg[256];
+    std::snprintf(msg, sizeof(msg),
+                  "3D record arena overflow in a training round (%llu record chunks dropped, capacity %lld "
+                  "records); the arena now holds %lld records: rerun, or reserve more with "
+                  "wostgpu_solver3_reserve_records",
+                  c[C_REC_OVERFLOW], static_cast<long long>(s->rec_cap), static_cast<long long>(s->rec_cap_min));
+    throw wgrt::WgError(WG_ERR_RUNTIME, msg);
   }
   Ev3& e = events()[s];
   s->last_walk_ms = static_cast<float>(ev_ms(e.walk, e.nw));
@@ -1030,6 +1035,13 @@ int wostgpu_solver3_run_profile(wg_solver3 s, double* walk_ms, double* train_ms,
     if (steps) *steps = s->prof_steps;
     if (escaped) *escaped = s->prof_escaped;
     if (train_steps) *train_steps = s->prof_train_steps;
+  });
+}
+
+int wostgpu_solver3_reserve_records(wg_solver3 s, int64_t n) {
+  return guarded([&] {
+    need(n >= 0, WG_ERR_INVALID, "record count must be >= 0");
+    s->rec_cap_min = std::max<int64_t>(s->rec_cap_min, n);
   });
 }
 

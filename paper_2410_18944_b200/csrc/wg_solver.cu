@@ -441,12 +441,19 @@ wg_train_stats sync_collect(wg_solver_s* s, long long steps_before) {
   CK(cudaStreamSynchronize(s->stream));
   CK(cudaMemcpy(s->last_counters, s->counters.p, sizeof(s->last_counters), cudaMemcpyDeviceToHost));
   if (s->last_counters[C_REC_OVERFLOW] > 0) {
+    // a collecting round filled the record arena: its walks stopped recording,
+    // which would have trained on a short-walk-biased set. Fail the call (the
+    // arena is doubled for the next one; wostgpu_solver_reserve_records
+    // pre-sizes it) instead of returning a silently biased field.
     s->rec_capacity_min = std::max<int64_t>(s->rec_capacity_min, 2 * s->rec_capacity);
-    std::fprintf(stderr,
-                 "wostgpu: record arena overflow (%llu chunks dropped, capacity %lld); the next call "
-                 "uses %lld records\n",
-                 s->last_counters[C_REC_OVERFLOW], static_cast<long long>(s->rec_capacity),
-                 static_cast<long long>(s->rec_capacity_min));
+    char msg[256];
+    std::snprintf(msg, sizeof(msg),
+                  "record arena overflow in a training round (%llu record chunks dropped, capacity %lld "
+                  "records); the arena now holds %lld records: rerun, or reserve more with "
+                  "wostgpu_solver_reserve_records",
+                  s->last_counters[C_REC_OVERFLOW], static_cast<long long>(s->rec_capacity),
+                  static_cast<long long>(s->rec_capacity_min));
+    throw wgrt::WgError(WG_ERR_RUNTIME, msg);
   }
   s->last_walk_ms = pool_ms(s->ev_walk, s->n_walk_ev);
   s->last_train_ms = pool_ms(s->ev_train, s->n_train_ev);
@@ -839,6 +846,13 @@ int wostgpu_comm_unique_id(char id[128]) {
     NCK(nccl().getUniqueId(&u));
     static_assert(sizeof(u) == 128, "nccl id size");
     std::memcpy(id, &u, 128);
+  });
+}
+
+int wostgpu_solver_reserve_records(wg_solver s, int64_t n) {
+  return guarded([&] {
+    need(n >= 0, WG_ERR_INVALID, "record count must be >= 0");
+    s->rec_capacity_min = std::max<int64_t>(s->rec_capacity_min, n);
   });
 }
 

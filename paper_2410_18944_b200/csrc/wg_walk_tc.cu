@@ -8,7 +8,8 @@
 //   B. CTA-wide: grid gather on CUDA cores, then the 3-layer MLP as 27
 //      single-thread tcgen05.mma issues into TMEM (wg_mlp_tc.cuh);
 //   C. per thread: Table-1 normalisation + one-sample MIS / vMF / reflected
-//      sampling in fp64 (wg_sphdist.cuh) and finish_step (wost.cpp:218-264).
+//      sampling in fp32 (normalize32 / mis_draw32, wg_mix32.cuh; the
+//      selection probability c stays fp64) and finish_step (wost.cpp:218-264).
 // Walk state stays in registers; the scene and the split fp16 weights stay in
 // shared memory for the whole launch. Statistics go through the same
 // [round][point] estimate buffer + Welford pass as the other walk kernels.
