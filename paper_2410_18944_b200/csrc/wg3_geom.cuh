@@ -97,6 +97,26 @@ __device__ __forceinline__ void ld_node(const Node3* n, float4& lo, float4& hi) 
   hi = __ldg(q + 1);
 }
 
+// fp32 lower bound of box_d2 for BVH pruning: the point as an fp32
+// interval [lo, hi] (rounded outward), per-axis gaps and the sum rounded
+// down, compared with the best distance rounded up. A box is skipped only if
+// it is certainly farther than the best, so the search returns the same
+// minimum as the fp64 test (it may visit a few more boxes); 4 fp32 ops per
+// axis instead of two f32->f64 conversions and four fp64 ops.
+struct PtBox {
+  float xl, xu, yl, yu, zl, zu;
+};
+__device__ __forceinline__ PtBox pt_box(D3 p) {
+  return {__double2float_rd(p.x), __double2float_ru(p.x), __double2float_rd(p.y),
+          __double2float_ru(p.y), __double2float_rd(p.z), __double2float_ru(p.z)};
+}
+__device__ __forceinline__ float box_d2_lb(const float4& lo, const float4& hi, const PtBox& p) {
+  const float dx = fmaxf(fmaxf(__fsub_rd(lo.x, p.xu), __fsub_rd(p.xl, hi.x)), 0.0f);
+  const float dy = fmaxf(fmaxf(__fsub_rd(lo.y, p.yu), __fsub_rd(p.yl, hi.y)), 0.0f);
+  const float dz = fmaxf(fmaxf(__fsub_rd(lo.z, p.zu), __fsub_rd(p.zl, hi.z)), 0.0f);
+  return __fadd_rd(__fadd_rd(__fmul_rd(dx, dx), __fmul_rd(dy, dy)), __fmul_rd(dz, dz));
+}
+
 __device__ __forceinline__ double box_d2(const float4& lo, const float4& hi, D3 p) {
   double dx = fmax(fmax((double)lo.x - p.x, 0.0), p.x - (double)hi.x);
   double dy = fmax(fmax((double)lo.y - p.y, 0.0), p.y - (double)hi.y);
@@ -193,13 +213,15 @@ struct CP3 {
 
 __device__ __forceinline__ void cp_bvh(const Node3* nodes, const Tri3* tris, D3 x, CP3& best) {
   if (!nodes) return;
+  const PtBox pb = pt_box(x);
+  float bf = __double2float_ru(best.d2);
   int stack[64];
   int sp = 0;
   stack[sp++] = 0;
   while (sp) {
     float4 lo, hi;
     ld_node(nodes + stack[--sp], lo, hi);
-    if (box_d2(lo, hi, x) > best.d2) continue;
+    if (box_d2_lb(lo, hi, pb) > bf) continue;
     int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
     if (b < 0) {
       for (int i = a; i < a - b; ++i) {
@@ -213,6 +235,7 @@ __device__ __forceinline__ void cp_bvh(const Node3* nodes, const Tri3* tris, D3 
           best.p = q;
           best.tri = id;
           best.local = i;
+          bf = __double2float_ru(d2);
         }
       }
       continue;
@@ -220,7 +243,7 @@ __device__ __forceinline__ void cp_bvh(const Node3* nodes, const Tri3* tris, D3 
     float4 alo, ahi, blo, bhi;
     ld_node(nodes + a, alo, ahi);
     ld_node(nodes + b, blo, bhi);
-    double da = box_d2(alo, ahi, x), db = box_d2(blo, bhi, x);
+    const float da = box_d2_lb(alo, ahi, pb), db = box_d2_lb(blo, bhi, pb);
     if (da <= db) {  // nearer child on top
       stack[sp++] = b;
       stack[sp++] = a;
@@ -269,13 +292,15 @@ __device__ __forceinline__ double closest_silhouette_d2(const Scene3View& s, D3 
   const Node3* nodes = s.node[2];
   if (!nodes) return dinf();
   double best = bound2;
+  const PtBox pb = pt_box(x);
+  float bf = __double2float_ru(best);
   int stack[64];
   int sp = 0;
   stack[sp++] = 0;
   while (sp) {
     float4 lo, hi;
     ld_node(nodes + stack[--sp], lo, hi);
-    if (box_d2(lo, hi, x) >= best) continue;
+    if (box_d2_lb(lo, hi, pb) >= bf) continue;
     int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
     if (b < 0) {
       for (int i = a; i < a - b; ++i) {
@@ -284,12 +309,13 @@ __device__ __forceinline__ double closest_silhouette_d2(const Scene3View& s, D3 
         D3 dq = sub(x, closest_on_seg(x, ld3(e.a), ld3(e.b)));
         best = fmin(best, dot(dq, dq));
       }
+      bf = __double2float_ru(best);
       continue;
     }
     float4 alo, ahi, blo, bhi;
     ld_node(nodes + a, alo, ahi);
     ld_node(nodes + b, blo, bhi);
-    double da = box_d2(alo, ahi, x), db = box_d2(blo, bhi, x);
+    const float da = box_d2_lb(alo, ahi, pb), db = box_d2_lb(blo, bhi, pb);
     if (da <= db) {
       stack[sp++] = b;
       stack[sp++] = a;
