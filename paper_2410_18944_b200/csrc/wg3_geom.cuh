@@ -339,21 +339,52 @@ struct Hit3 {
   int kind;
 };
 
+// fp32 slab test against the box grown by `pad` on every side: with pad at
+// least 2^-20 of the scene's coordinate scale it dominates the fp32
+// rounding of (bound - origin) * (1 / d), so a box the segment [0, t_hi]
+// truly meets is never rejected (the search visits a superset and the
+// fp64 ray-triangle tests decide); 2 fp32 ops per slab instead of fp64
+__device__ __forceinline__ bool ray_box_f(const float3& o, const float3& inv, const bool* dz, const float4& lo,
+                                          const float4& hi, float t_hi, float pad) {
+  float t0 = 0.0f, t1 = t_hi;
+  const float oo[3] = {o.x, o.y, o.z}, iv[3] = {inv.x, inv.y, inv.z};
+  const float l[3] = {lo.x - pad, lo.y - pad, lo.z - pad}, h[3] = {hi.x + pad, hi.y + pad, hi.z + pad};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (dz[a]) {
+      if (oo[a] < l[a] || oo[a] > h[a]) return false;
+      continue;
+    }
+    float ta = (l[a] - oo[a]) * iv[a], tb = (h[a] - oo[a]) * iv[a];
+    if (ta > tb) {
+      const float s = ta;
+      ta = tb;
+      tb = s;
+    }
+    t0 = fmaxf(t0, ta);
+    t1 = fminf(t1, tb);
+    if (t0 > t1) return false;
+  }
+  return true;
+}
+
 __device__ __forceinline__ void ray_bvh(const Node3* nodes, const Tri3* tris, int kind, D3 o, D3 d,
-                                        double t_max, double t_eps, int exclude, Hit3& h) {
+                                        double t_max, double t_eps, int exclude, Hit3& h, float pad) {
   if (!nodes) return;
-  D3 inv;
   bool dz[3] = {d.x == 0.0, d.y == 0.0, d.z == 0.0};
-  inv.x = dz[0] ? 0.0 : 1.0 / d.x;
-  inv.y = dz[1] ? 0.0 : 1.0 / d.y;
-  inv.z = dz[2] ? 0.0 : 1.0 / d.z;
+  const float3 of = make_float3(static_cast<float>(o.x), static_cast<float>(o.y), static_cast<float>(o.z));
+  const float3 invf = make_float3(dz[0] ? 0.0f : static_cast<float>(1.0 / d.x),
+                                  dz[1] ? 0.0f : static_cast<float>(1.0 / d.y),
+                                  dz[2] ? 0.0f : static_cast<float>(1.0 / d.z));
+  // t bound rounded up, padded like the boxes
+  float tb_f = __double2float_ru(fmin(t_max, h.t)) * (1.0f + 0x1.0p-20f);
   int stack[64];
   int sp = 0;
   stack[sp++] = 0;
   while (sp) {
     float4 lo, hi;
     ld_node(nodes + stack[--sp], lo, hi);
-    if (!ray_box(o, inv, dz, lo, hi, fmin(t_max, h.t))) continue;
+    if (!ray_box_f(of, invf, dz, lo, hi, tb_f, pad)) continue;
     int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
     if (b < 0) {
       for (int i = a; i < a - b; ++i) {
@@ -368,6 +399,7 @@ __device__ __forceinline__ void ray_bvh(const Node3* nodes, const Tri3* tris, in
           h.tri = id;
           h.local = i;
           h.kind = kind;
+          tb_f = __double2float_ru(fmin(t_max, h.t)) * (1.0f + 0x1.0p-20f);
         }
       }
       continue;
@@ -377,11 +409,19 @@ __device__ __forceinline__ void ray_bvh(const Node3* nodes, const Tri3* tris, in
   }
 }
 
+// box growth of the fp32 slab test: 2^-20 of the scene's coordinate scale
+__device__ __forceinline__ float ray_pad(const Scene3View& s) {
+  double m = s.diag;
+  for (int i = 0; i < 6; ++i) m = fmax(m, fabs(s.bbox[i]));
+  return static_cast<float>(m * 0x1.0p-20);
+}
+
 __device__ __forceinline__ Hit3 ray_first_hit(const Scene3View& s, D3 o, D3 d, double t_max,
                                               unsigned kinds, int exclude) {
   Hit3 h{dinf(), -1, -1, -1};
-  if (kinds & WG_KIND_DIRICHLET) ray_bvh(s.node[0], s.tri[0], 0, o, d, t_max, s.t_eps, exclude, h);
-  if (kinds & WG_KIND_NEUMANN) ray_bvh(s.node[1], s.tri[1], 1, o, d, t_max, s.t_eps, exclude, h);
+  const float pad = ray_pad(s);
+  if (kinds & WG_KIND_DIRICHLET) ray_bvh(s.node[0], s.tri[0], 0, o, d, t_max, s.t_eps, exclude, h, pad);
+  if (kinds & WG_KIND_NEUMANN) ray_bvh(s.node[1], s.tri[1], 1, o, d, t_max, s.t_eps, exclude, h, pad);
   return h;
 }
 
