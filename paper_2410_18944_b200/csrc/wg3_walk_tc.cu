@@ -391,14 +391,9 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsi
   // 4 bits per axis: 5 bits measured no faster (3.27 s; training 0.99 s)
   const int sort_period = a.recs ? 2 : 1;
   const int geom_blocks = static_cast<int>((v.slots + 127) / 128);
-  // persistent direction CTAs: exactly the resident count (2 per SM at 197
-  // registers), looping over the queue's tiles
-  static const int dir_per_sm = [smem] {
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, wave_dir_kernel, 128, smem);
-    return b < 1 ? 1 : b;
-  }();
-  const int dir_blocks = sms * dir_per_sm;  // cfg 4 frozen rounds: 2.84 vs 2.91 s at 3 per SM
+  // persistent direction CTAs, 2 per SM (197 registers; cfg 4 frozen rounds
+  // 2.84 s vs 2.91 s at 3 per SM and 3.07 s at 1)
+  const int dir_blocks = sms * 2;
   for (int it = 0;; ++it) {
     const int par = it & 1;
     if (sort_period > 0 && it > 0 && it % sort_period == 0) {
