@@ -19,6 +19,7 @@ struct Field3View {
   int32_t w1, b1, w2, b2, w3, b3;
   int32_t mlp_count;
   double bbox[6];
+  double inv_ext[3];  // 1 / (bbox max - min) per axis (tensor-core gather)
 };
 
 __device__ __forceinline__ void field3_gather(const Field3View& f, double x, double y, double z,

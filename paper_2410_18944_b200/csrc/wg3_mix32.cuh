@@ -138,13 +138,31 @@ __device__ __forceinline__ D3 reflected_sample3f(wg::Pcg& rng, const Mix3f& m, D
   return nu;
 }
 
+// uniform_sample (wg3_mix.cuh) with the same draws, the azimuth's sine and
+// cosine in fp32 (sincospif) instead of fp64 sin / cos, renormalised in fp64
+__device__ __forceinline__ D3 uniform_sample3f(wg::Pcg& rng, bool on_n, D3 n) {
+  D3 nu{0.0, 0.0, 1.0};
+  for (int it = 0; it < kMaxProposals; ++it) {
+    const double z = 1.0 - 2.0 * rng.uni();
+    const float s = sqrtf(fmaxf(0.0f, static_cast<float>((1.0 - z) * (1.0 + z))));
+    float sp, cp;
+    sincospif(static_cast<float>(2.0 * rng.uni()), &sp, &cp);
+    nu = unit3(D3{static_cast<double>(s * cp), static_cast<double>(s * sp), z});
+    if (!on_n) return nu;
+    const double d = dot(nu, n);
+    if (d > 0.0) return nu;
+    if (d < 0.0) return {-nu.x, -nu.y, -nu.z};
+  }
+  return nu;
+}
+
 // mis_sample (sphdist.cpp:254-270) with the fp32 mixture; c is the (possibly
 // mode-overridden) selection probability
 __device__ __forceinline__ Mis3 mis_sample3f(wg::Pcg& rng, const Mix3f& m, double c, bool on_n, D3 n, bool refl) {
   Mis3 o;
   const bool guided = rng.uni() < c;
   if (guided) o.nu = on_n && refl ? reflected_sample3f(rng, m, n) : mixture_sample3f(rng, m);
-  else o.nu = uniform_sample(rng, on_n, n);
+  else o.nu = uniform_sample3f(rng, on_n, n);
   o.pg = on_n && refl ? reflected_pdf3f(m, o.nu, n) : mixture_pdf3f(m, o.nu);
   o.pu = uniform_pdf(o.nu, on_n, n);
   o.pmis = c * o.pg + (1.0 - c) * o.pu;

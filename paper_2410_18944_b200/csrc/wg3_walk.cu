@@ -398,6 +398,7 @@ void field3_layout(wg_field_s* f) {
   need(off < (int64_t(1) << 31), WG_ERR_INVALID, "3D field: parameter count exceeds int32");
   f->n_params = off;
   for (int i = 0; i < 6; ++i) v.bbox[i] = f->bbox3[i];
+  for (int i = 0; i < 3; ++i) v.inv_ext[i] = 1.0 / (f->bbox3[i + 3] - f->bbox3[i]);
 }
 
 wg::SolverParams params3(const wg_solver3_s* s) {

@@ -35,9 +35,10 @@ __device__ __forceinline__ Dir3 sample_guided_f(Lane3& w, const Walk3Args& a, co
 }
 
 __device__ __forceinline__ void gather3_tc(const Field3View& f, D3 x, float* in) {
-  const float u = static_cast<float>(wg::sclamp((x.x - f.bbox[0]) / (f.bbox[3] - f.bbox[0]), 0.0, 1.0));
-  const float v = static_cast<float>(wg::sclamp((x.y - f.bbox[1]) / (f.bbox[4] - f.bbox[1]), 0.0, 1.0));
-  const float q = static_cast<float>(wg::sclamp((x.z - f.bbox[2]) / (f.bbox[5] - f.bbox[2]), 0.0, 1.0));
+  // reciprocal extents (no fp64 division on the direction kernel's path)
+  const float u = static_cast<float>(wg::sclamp((x.x - f.bbox[0]) * f.inv_ext[0], 0.0, 1.0));
+  const float v = static_cast<float>(wg::sclamp((x.y - f.bbox[1]) * f.inv_ext[1], 0.0, 1.0));
+  const float q = static_cast<float>(wg::sclamp((x.z - f.bbox[2]) * f.inv_ext[2], 0.0, 1.0));
 #pragma unroll
   for (int l = 0; l < 4; ++l) {
     const int res = f.res[l];
