@@ -79,6 +79,7 @@ static_assert(sizeof(Edge3) == 104, "Edge3 layout");
 struct Scene3View {
   const Node3* node[3];  // Dirichlet, Neumann, silhouette edges (nullptr if empty)
   const Tri3* tri[2];    // leaf-ordered triangles per kind
+  const float4* tbox;    // [2 per Dirichlet triangle] fp32 box {lo, hi}, outward-rounded
   const Edge3* edge;     // leaf-ordered edges
   const wg_value3_spec* values;
   double bbox[6];
@@ -211,7 +212,8 @@ struct CP3 {
   int local;  // leaf-order index within its kind's triangle array
 };
 
-__device__ __forceinline__ void cp_bvh(const Node3* nodes, const Tri3* tris, D3 x, CP3& best) {
+__device__ __forceinline__ void cp_bvh(const Node3* nodes, const Tri3* tris, D3 x, CP3& best,
+                                       const float4* tbox = nullptr) {
   if (!nodes) return;
   const PtBox pb = pt_box(x);
   float bf = __double2float_ru(best.d2);
@@ -225,6 +227,9 @@ __device__ __forceinline__ void cp_bvh(const Node3* nodes, const Tri3* tris, D3 
     int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
     if (b < 0) {
       for (int i = a; i < a - b; ++i) {
+        // the triangle's own fp32 box bounds its distance from below: skip
+        // the fp64 closest-point test when the box is certainly farther
+        if (tbox && box_d2_lb(tbox[2 * i], tbox[2 * i + 1], pb) > bf) continue;
         const Tri3& t = tris[i];
         D3 q = closest_on_tri(x, ld3(t.a), ld3(t.b), ld3(t.c));
         D3 dq = sub(x, q);
@@ -265,14 +270,14 @@ __device__ __forceinline__ CP3 closest_dirichlet_seeded(const Scene3View& s, D3 
     D3 dq = sub(x, q);
     best = {q, dot(dq, dq), t.id, seed};
   }
-  cp_bvh(s.node[0], s.tri[0], x, best);
+  cp_bvh(s.node[0], s.tri[0], x, best, s.tbox);
   return best;
 }
 
 // Accel::closest_point analogue: (point, distance, triangle id) or id -1, d = inf
 __device__ __forceinline__ CP3 closest_point(const Scene3View& s, D3 x, unsigned kinds) {
   CP3 best{{0.0, 0.0, 0.0}, dinf(), -1, -1};
-  if (kinds & WG_KIND_DIRICHLET) cp_bvh(s.node[0], s.tri[0], x, best);
+  if (kinds & WG_KIND_DIRICHLET) cp_bvh(s.node[0], s.tri[0], x, best, s.tbox);
   if (kinds & WG_KIND_NEUMANN) cp_bvh(s.node[1], s.tri[1], x, best);
   return best;
 }

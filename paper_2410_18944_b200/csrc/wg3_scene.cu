@@ -341,6 +341,23 @@ int wostgpu_scene3_create(const double* tri, const int32_t* kind, const int32_t*
         s->tri[k].upload(leaf.data(), leaf.size());
         v.node[k] = s->node[k].as<Node3>();
         v.tri[k] = s->tri[k].as<Tri3>();
+        if (k == 0) {  // fp32 boxes of the Dirichlet triangles, rounded outward (closest-point prefilter)
+          std::vector<float> tb(8 * leaf.size());
+          for (size_t i = 0; i < leaf.size(); ++i) {
+            for (int a = 0; a < 3; ++a) {
+              const double lo = std::min({leaf[i].a[a], leaf[i].b[a], leaf[i].c[a]});
+              const double hi = std::max({leaf[i].a[a], leaf[i].b[a], leaf[i].c[a]});
+              float fl = static_cast<float>(lo), fh = static_cast<float>(hi);
+              if (static_cast<double>(fl) > lo) fl = std::nextafter(fl, -INFINITY);
+              if (static_cast<double>(fh) < hi) fh = std::nextafter(fh, INFINITY);
+              tb[8 * i + a] = fl;
+              tb[8 * i + 4 + a] = fh;
+            }
+            tb[8 * i + 3] = tb[8 * i + 7] = 0.0f;
+          }
+          s->tbox.upload(tb.data(), tb.size());
+          v.tbox = reinterpret_cast<const float4*>(s->tbox.as<float>());
+        }
       }
     }
     std::vector<Edge3> edges = silhouette_edges(tris, &s->n_always, &s->n_crease);
