@@ -2,7 +2,7 @@
 report of ONE kernel launch, as JSON (committed under profiles/ and read by
 bench.py for roofline.traffic).
 
-usage: python tools/ncu_counters.py REPORT.ncu-rep KERNEL_NAME "capture command" > profiles/x.json
+usage: python tools/ncu_counters.py REPORT.ncu-rep KERNEL_NAME "capture command" ["config"] > profiles/x.json
 """
 import csv
 import io
@@ -19,8 +19,11 @@ KEYS = {
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_active_pct",
     "sm__inst_executed.sum.per_cycle_active": "ipc_per_sm_sum",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput_pct",
+    "smsp__thread_inst_executed_per_inst_executed.ratio": "active_threads_per_warp",
+    "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
 }
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "sector": 1, "us": 1e-6, "ms": 1e-3,
+SCALE = {"byte": 1, "":1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "sector": 1, "us": 1e-6, "ms": 1e-3,
          "ns": 1e-9, "s": 1, "%": 1, "inst/cycle": 1}
 
 
@@ -38,6 +41,8 @@ def main():
         sys.exit(f"no launch of {kernel} in {rep}")
     vals = match[-1]
     res = {"kernel": kernel, "report": rep, "capture": cmd}
+    if len(sys.argv) > 4:
+        res["config"] = sys.argv[4]
     for k, name in KEYS.items():
         if k in h:
             i = h.index(k)
