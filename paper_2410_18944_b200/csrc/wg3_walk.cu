@@ -621,6 +621,31 @@ void ensure3_train(wg_solver3_s* s, const wg_train_config& tc) {
 void enqueue3_minibatch(wg_solver3_s* s, const wg_train_config& tc, int b, double inv_count) {
   wg_field_s* f = s->field;
   CK(cudaMemsetAsync(s->grad.p, 0, sizeof(float) * (f->n_params + 1), s->st));
+  if (s->mlp == WG_MLP_TENSOR) {
+    // tcgen05 training tile (wg_train_tc.cu): forward, loss gradient and
+    // backward of 128 records per tile on the tensor cores; the split-fp16
+    // weight blob is packed from the current parameters (Adam moved them
+    // since the previous minibatch)
+    s->g_blob.alloc(wg::wpack::BYTES);
+    CKL(wg::launch_pack3_full(f->view3, s->g_blob.as<unsigned char>(), s->st));
+    wg::TrainArgs3 g{};
+    g.f = f->view3;
+    g.recs = s->recs.as<DevRecord3>();
+    g.list = s->lists.as<uint32_t>() + static_cast<int64_t>(b) * s->list_cap;
+    g.count = &s->ctl.as<wg::TrainCtl>()->mb_count[b];
+    g.list_cap = s->list_cap;
+    g.grad = s->grad.as<float>();
+    g.n_params = f->n_params;
+    g.inv_count = inv_count;
+    g.reflect = tc.reflect;
+    g.learn_selection = tc.learn_selection;
+    g.e_fraction = tc.e_fraction;
+    g.v_floor = tc.v_floor;
+    g.totals = s->totals.as<wg::TrainTotals>();
+    g.packed = s->g_blob.as<unsigned char>();
+    CKL(wg::launch_grad3_tc(g, s->st));
+    return;
+  }
   Grad3Args g{};
   g.f = f->view3;
   g.recs = s->recs.as<DevRecord3>();

@@ -12,6 +12,7 @@
 #include "wg3_field.cuh"
 #include "wg3_mix.cuh"
 #include "wg_kernels.cuh"
+#include "wg_train.cuh"
 
 namespace wg3 {
 
@@ -354,6 +355,30 @@ struct Wave3 {
 #endif
 constexpr int kSortBits = WG3_SORT_BITS;              // per axis
 constexpr int kSortBins = 1 << (3 * kSortBits);       // + 1 bin for slots without a pending move
+}  // namespace wg3
+
+namespace wg {
+// 3D minibatch gradient on the tensor cores (wg_train_tc.cu grad3_tc_kernel;
+// the fields of TrainArgs with the 3D field and records)
+struct TrainArgs3 {
+  wg3::Field3View f;
+  const wg3::DevRecord3* recs;
+  const uint32_t* list;
+  const unsigned long long* count;
+  int64_t list_cap;
+  float* grad;  // [n_params + 1]; grad[n_params] = record count
+  int64_t n_params;
+  double inv_count;
+  int32_t reflect, learn_selection;
+  double e_fraction, v_floor;
+  TrainTotals* totals;
+  const unsigned char* packed;  // split-fp16 blob of the 3D field (launch_pack3_full)
+};
+cudaError_t launch_grad3_tc(const TrainArgs3& a, cudaStream_t st);
+cudaError_t launch_pack3_full(const wg3::Field3View& f, unsigned char* blob, cudaStream_t st);
+}  // namespace wg
+
+namespace wg3 {
 // returns the number of kernels launched in *launches
 cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& w, int sms, unsigned int* h_qlen,
                                int64_t* launches, cudaStream_t st);

@@ -24,6 +24,7 @@
 // so the fp16 split keeps ~22 bits. Weight / bias gradients leave TMEM once per
 // tile by atomics; dX goes to the grid corners by atomics. The split weight
 // tiles arrive as the field's packed blob (wg_wpack.cuh) in one bulk copy.
+#include "wg3_walk_common.cuh"
 #include "wg_loss.cuh"
 #include "wg_mlp_tc.cuh"
 #include "wg_train.cuh"
@@ -184,9 +185,135 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
 
 }  // namespace
 
-__global__ void __launch_bounds__(128, 1) grad_tc_kernel(TrainArgs a) {
+// ---- the two field dimensions: gather / corner scatter / loss gradient
+// (2D: bilinear 4 corners per level, 33 outputs, fp32 loss record_dy32;
+// 3D: trilinear 8 corners per level, 41 outputs, fp64 loss record_dy3).
+// The scatter recomputes the corners from the record's position instead of
+// keeping them in registers through the tile.
+struct Tc2 {
+  using Args = TrainArgs;
+  using Rec = DevRecord;
+  static constexpr int OD = 33;
+  __device__ static void gather(const FieldView& f, const Rec& r, float* x) {
+    const double ex = f.bbox[2] - f.bbox[0], ey = f.bbox[3] - f.bbox[1];
+    const float u = static_cast<float>(sclamp((static_cast<double>(r.x) - f.bbox[0]) / ex, 0.0, 1.0));
+    const float v = static_cast<float>(sclamp((static_cast<double>(r.y) - f.bbox[1]) / ey, 0.0, 1.0));
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int res = f.res[l];
+      const float px = u * static_cast<float>(res - 1), py = v * static_cast<float>(res - 1);
+      const int ix = imin(static_cast<int>(px), res - 2), iy = imin(static_cast<int>(py), res - 2);
+      const float fx = px - ix, fy = py - iy;
+      const int c00 = f.lvl_off[l] + (iy * res + ix) * 4;
+      const float w0 = (1.0f - fx) * (1.0f - fy), w1 = fx * (1.0f - fy), w2 = (1.0f - fx) * fy, w3 = fx * fy;
+      const float4 e0 = __ldg(reinterpret_cast<const float4*>(f.p + c00));
+      const float4 e1 = __ldg(reinterpret_cast<const float4*>(f.p + c00 + 4));
+      const float4 e2 = __ldg(reinterpret_cast<const float4*>(f.p + c00 + res * 4));
+      const float4 e3 = __ldg(reinterpret_cast<const float4*>(f.p + c00 + res * 4 + 4));
+      x[4 * l + 0] = w0 * e0.x + w1 * e1.x + w2 * e2.x + w3 * e3.x;
+      x[4 * l + 1] = w0 * e0.y + w1 * e1.y + w2 * e2.y + w3 * e3.y;
+      x[4 * l + 2] = w0 * e0.z + w1 * e1.z + w2 * e2.z + w3 * e3.z;
+      x[4 * l + 3] = w0 * e0.w + w1 * e1.w + w2 * e2.w + w3 * e3.w;
+    }
+  }
+  __device__ static void scatter(const FieldView& f, const Rec& r, const float* dx, float sc, float* grad) {
+    const double ex = f.bbox[2] - f.bbox[0], ey = f.bbox[3] - f.bbox[1];
+    const float u = static_cast<float>(sclamp((static_cast<double>(r.x) - f.bbox[0]) / ex, 0.0, 1.0));
+    const float v = static_cast<float>(sclamp((static_cast<double>(r.y) - f.bbox[1]) / ey, 0.0, 1.0));
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {  // guide_field.cpp:305-314
+      const int res = f.res[l];
+      const float px = u * static_cast<float>(res - 1), py = v * static_cast<float>(res - 1);
+      const int ix = imin(static_cast<int>(px), res - 2), iy = imin(static_cast<int>(py), res - 2);
+      const float fx = px - ix, fy = py - iy;
+      const int c00 = f.lvl_off[l] + (iy * res + ix) * 4;
+      const int ci[4] = {c00, c00 + 4, c00 + res * 4, c00 + res * 4 + 4};
+      const float wc[4] = {(1.0f - fx) * (1.0f - fy), fx * (1.0f - fy), (1.0f - fx) * fy, fx * fy};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float w = wc[c] * sc;
+        red_add_v4(grad + ci[c], w * dx[4 * l], w * dx[4 * l + 1], w * dx[4 * l + 2], w * dx[4 * l + 3]);
+      }
+    }
+  }
+  __device__ static bool dy(const float* y, const Rec& r, const Args& a, float* d) {
+    return record_dy32(y, r, a, d);
+  }
+};
+
+struct Tc3 {
+  using Args = TrainArgs3;
+  using Rec = wg3::DevRecord3;
+  static constexpr int OD = wg3::OD;  // 41
+  __device__ static void cell(const wg3::Field3View& f, const Rec& r, float& u, float& v, float& q) {
+    u = static_cast<float>(sclamp((static_cast<double>(r.x) - f.bbox[0]) * f.inv_ext[0], 0.0, 1.0));
+    v = static_cast<float>(sclamp((static_cast<double>(r.y) - f.bbox[1]) * f.inv_ext[1], 0.0, 1.0));
+    q = static_cast<float>(sclamp((static_cast<double>(r.z) - f.bbox[2]) * f.inv_ext[2], 0.0, 1.0));
+  }
+  __device__ static void gather(const wg3::Field3View& f, const Rec& r, float* x) {
+    float u, v, q;
+    cell(f, r, u, v, q);
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int res = f.res[l];
+      const float rm = static_cast<float>(res - 1);
+      const float px = u * rm, py = v * rm, pz = q * rm;
+      const int ix = imin(static_cast<int>(px), res - 2), iy = imin(static_cast<int>(py), res - 2),
+                iz = imin(static_cast<int>(pz), res - 2);
+      const float fx = px - ix, fy = py - iy, fz = pz - iz, gx = 1.0f - fx, gy = 1.0f - fy, gz = 1.0f - fz;
+      const int c0 = f.lvl_off[l] + ((iz * res + iy) * res + ix) * 4, sy = res * 4, sz = res * res * 4;
+      const int ci[8] = {c0, c0 + 4, c0 + sy, c0 + sy + 4, c0 + sz, c0 + sz + 4, c0 + sz + sy, c0 + sz + sy + 4};
+      const float w8[8] = {gx * gy * gz, fx * gy * gz, gx * fy * gz, fx * fy * gz,
+                           gx * gy * fz, fx * gy * fz, gx * fy * fz, fx * fy * fz};
+      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4 e = __ldg(reinterpret_cast<const float4*>(f.p + ci[c]));
+        acc[0] = fmaf(w8[c], e.x, acc[0]);
+        acc[1] = fmaf(w8[c], e.y, acc[1]);
+        acc[2] = fmaf(w8[c], e.z, acc[2]);
+        acc[3] = fmaf(w8[c], e.w, acc[3]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) x[4 * l + i] = acc[i];
+    }
+  }
+  __device__ static void scatter(const wg3::Field3View& f, const Rec& r, const float* dx, float sc, float* grad) {
+    float u, v, q;
+    cell(f, r, u, v, q);
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int res = f.res[l];
+      const float rm = static_cast<float>(res - 1);
+      const float px = u * rm, py = v * rm, pz = q * rm;
+      const int ix = imin(static_cast<int>(px), res - 2), iy = imin(static_cast<int>(py), res - 2),
+                iz = imin(static_cast<int>(pz), res - 2);
+      const float fx = px - ix, fy = py - iy, fz = pz - iz, gx = 1.0f - fx, gy = 1.0f - fy, gz = 1.0f - fz;
+      const int c0 = f.lvl_off[l] + ((iz * res + iy) * res + ix) * 4, sy = res * 4, sz = res * res * 4;
+      const int ci[8] = {c0, c0 + 4, c0 + sy, c0 + sy + 4, c0 + sz, c0 + sz + 4, c0 + sz + sy, c0 + sz + sy + 4};
+      const float w8[8] = {gx * gy * gz, fx * gy * gz, gx * fy * gz, fx * fy * gz,
+                           gx * gy * fz, fx * gy * fz, gx * fy * fz, fx * fy * fz};
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float w = w8[c] * sc;
+        red_add_v4(grad + ci[c], w * dx[4 * l], w * dx[4 * l + 1], w * dx[4 * l + 2], w * dx[4 * l + 3]);
+      }
+    }
+  }
+  __device__ static bool dy(const float* y, const Rec& r, const Args& a, float* d) {
+    const bool on_n = (r.flags & REC_ON_NEUMANN) != 0;
+    return wg3::record_dy3<wg3::K8>(y, wg3::D3{r.nux, r.nuy, r.nuz}, wg3::D3{r.nx, r.ny, r.nz}, on_n, r.target,
+                                    r.pdf_mis, r.pdf_u, a.reflect != 0, a.learn_selection != 0, a.e_fraction,
+                                    a.v_floor, a.inv_count, d);
+  }
+};
+
+template <class P>
+__device__ __forceinline__ void grad_tc_body(const typename P::Args& a) {
   extern __shared__ __align__(128) unsigned char sm[];
-  const FieldView& f = a.f;
+  const auto& f = a.f;
+  constexpr int OD = P::OD;
+  static_assert(OD <= 48, "outputs fit the N = 48 tile");
   const int t = threadIdx.x, warp = t >> 5;
   const int64_t count = static_cast<int64_t>(min(*a.count, static_cast<unsigned long long>(a.list_cap)));
   const int64_t tiles = (count + TM - 1) / TM;
@@ -218,43 +345,13 @@ __global__ void __launch_bounds__(128, 1) grad_tc_kernel(TrainArgs a) {
     __syncthreads();
     const int64_t ri = tile * TM + t;
     const bool live = ri < count;
-    DevRecord r{};
+    typename P::Rec r{};
     if (live) r = a.recs[a.list[ri]];
-    // ---- gather (guide_field.cpp:80-123), corners kept for the scatter
+    // ---- gather (guide_field.cpp:80-123)
     float x[16];
-    int cidx[16];
-    float cw[16];
-    {
-      double ex = f.bbox[2] - f.bbox[0], ey = f.bbox[3] - f.bbox[1];
-      float u = static_cast<float>(sclamp((static_cast<double>(r.x) - f.bbox[0]) / ex, 0.0, 1.0));
-      float v = static_cast<float>(sclamp((static_cast<double>(r.y) - f.bbox[1]) / ey, 0.0, 1.0));
-#pragma unroll
-      for (int l = 0; l < 4; ++l) {
-        int res = f.res[l];
-        float px = u * static_cast<float>(res - 1), py = v * static_cast<float>(res - 1);
-        int ix = imin(static_cast<int>(px), res - 2), iy = imin(static_cast<int>(py), res - 2);
-        float fx = px - ix, fy = py - iy;
-        int c00 = f.lvl_off[l] + (iy * res + ix) * 4;
-        cidx[4 * l] = c00;
-        cidx[4 * l + 1] = c00 + 4;
-        cidx[4 * l + 2] = c00 + res * 4;
-        cidx[4 * l + 3] = c00 + res * 4 + 4;
-        cw[4 * l] = (1.0f - fx) * (1.0f - fy);
-        cw[4 * l + 1] = fx * (1.0f - fy);
-        cw[4 * l + 2] = (1.0f - fx) * fy;
-        cw[4 * l + 3] = fx * fy;
-        float4 e0 = __ldg(reinterpret_cast<const float4*>(f.p + cidx[4 * l]));
-        float4 e1 = __ldg(reinterpret_cast<const float4*>(f.p + cidx[4 * l + 1]));
-        float4 e2 = __ldg(reinterpret_cast<const float4*>(f.p + cidx[4 * l + 2]));
-        float4 e3 = __ldg(reinterpret_cast<const float4*>(f.p + cidx[4 * l + 3]));
-        x[4 * l + 0] = cw[4 * l] * e0.x + cw[4 * l + 1] * e1.x + cw[4 * l + 2] * e2.x + cw[4 * l + 3] * e3.x;
-        x[4 * l + 1] = cw[4 * l] * e0.y + cw[4 * l + 1] * e1.y + cw[4 * l + 2] * e2.y + cw[4 * l + 3] * e3.y;
-        x[4 * l + 2] = cw[4 * l] * e0.z + cw[4 * l + 1] * e1.z + cw[4 * l + 2] * e2.z + cw[4 * l + 3] * e3.z;
-        x[4 * l + 3] = cw[4 * l] * e0.w + cw[4 * l + 1] * e1.w + cw[4 * l + 2] * e2.w + cw[4 * l + 3] * e3.w;
-      }
-      if (!live)
-        for (int i = 0; i < 16; ++i) x[i] = 0.0f;
-    }
+    P::gather(f, r, x);
+    if (!live)
+      for (int i = 0; i < 16; ++i) x[i] = 0.0f;
     float inv_x, inv_h1, inv_h2, inv_dy, inv_d2, inv_d1;
     float row[KH];
     // ---- X | 1
@@ -331,14 +428,14 @@ __global__ void __launch_bounds__(128, 1) grad_tc_kernel(TrainArgs a) {
       float y[48];
       ld_row<48>(trow + C128, y);
 #pragma unroll
-      for (int j = 0; j < 33; ++j) y[j] = y[j] * inv_h2 + bias[128 + j];
-      float dy[33];
-      bool used = live && record_dy32(y, r, a, dy);
+      for (int j = 0; j < OD; ++j) y[j] = y[j] * inv_h2 + bias[128 + j];
+      float dy[OD];
+      bool used = live && P::dy(y, r, a, dy);
       if (used) ++consumed;
       else if (live) ++skipped;
 #pragma unroll
-      for (int j = 0; j < 48; ++j) row[j] = (used && j < 33) ? dy[j] : 0.0f;
-      float s = tile_scale(sm, 3, row, 33, inv_dy);
+      for (int j = 0; j < 48; ++j) row[j] = (used && j < OD) ? dy[j] : 0.0f;
+      float s = tile_scale(sm, 3, row, OD, inv_dy);
 #pragma unroll
       for (int j = 0; j < 48; ++j) row[j] *= s;
       put_row<KY>(sm, S_YH, S_YL, t, row);
@@ -354,7 +451,7 @@ __global__ void __launch_bounds__(128, 1) grad_tc_kernel(TrainArgs a) {
       umma::commit(reinterpret_cast<uint64_t*>(sm + S_BAR));
     }
     wait_mma(sm, phase);
-    flush_dw<48>(sm, trow + CW3, t, 64, 64, 33, inv_h2 * inv_dy, inv_dy, a.grad, f.w3, f.b3);
+    flush_dw<48>(sm, trow + CW3, t, 64, 64, OD, inv_h2 * inv_dy, inv_dy, a.grad, f.w3, f.b3);
     {
       float d[64];
       ld_row<64>(trow + C0, d);
@@ -406,16 +503,7 @@ __global__ void __launch_bounds__(128, 1) grad_tc_kernel(TrainArgs a) {
     {
       float dx[16];
       ld_row<16>(trow + C128, dx);
-      if (live) {  // grid corners (guide_field.cpp:305-314)
-#pragma unroll
-        for (int l = 0; l < 4; ++l)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const float wc = cw[4 * l + c] * inv_d1;
-            red_add_v4(a.grad + cidx[4 * l + c], wc * dx[4 * l], wc * dx[4 * l + 1], wc * dx[4 * l + 2],
-                       wc * dx[4 * l + 3]);
-          }
-      }
+      if (live) P::scatter(f, r, dx, inv_d1, a.grad);  // grid corners (guide_field.cpp:305-314)
     }
     umma::fence_before();
     __syncthreads();  // TMEM / smem reuse by the next tile
@@ -436,11 +524,15 @@ __global__ void __launch_bounds__(128, 1) grad_tc_kernel(TrainArgs a) {
   }
 }
 
+// named kernels for profiles / launch lists
+__global__ void __launch_bounds__(128, 1) grad_tc_kernel(TrainArgs a);
+__global__ void __launch_bounds__(128, 1) grad3_tc_kernel(TrainArgs3 a);
+
 bool tc_grad_available() { return true; }
 
-cudaError_t launch_grad_tc(const TrainArgs& a, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(grad_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(SMEM_BYTES));
+template <class P, class Args>
+cudaError_t launch_tc_tile(void (*k)(Args), const Args& a, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SMEM_BYTES));
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -448,10 +540,44 @@ cudaError_t launch_grad_tc(const TrainArgs& a, cudaStream_t st) {
   if (a.packed == nullptr) return cudaErrorInvalidValue;
   int64_t tiles = (a.list_cap + TM - 1) / TM;
   int blocks = static_cast<int>(tiles < sms ? tiles : sms);
-  grad_tc_kernel<<<blocks, TM, SMEM_BYTES, st>>>(a);
+  k<<<blocks, TM, SMEM_BYTES, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_grad_tc(const TrainArgs& a, cudaStream_t st) { return launch_tc_tile<Tc2>(grad_tc_kernel, a, st); }
+
+// the 3D minibatch gradient on the tensor cores (the tcgen05 counterpart of
+// wg3_walk.cu's CUDA-core grad3_tile_kernel)
+cudaError_t launch_grad3_tc(const TrainArgs3& a, cudaStream_t st) { return launch_tc_tile<Tc3>(grad3_tc_kernel, a, st); }
+
+// the whole split-fp16 blob (forward + backward tiles, wg_wpack.cuh layout)
+// of a 3D field: W3 has 41 outputs (zero padding to N = 48 from the memset)
+__global__ void pack3_full_kernel(wg3::Field3View f, unsigned char* blob) {
+  tc_stage_weights_raw(blob - TcLayout::B1_HI, f.p, f.w1, f.b1, f.w2, f.b2, f.w3, f.b3, wg3::OD);
+  for (int e = threadIdx.x; e < 16 * 64; e += blockDim.x) {  // C1[k][n] = W1[k][n]
+    const int k = e / 64, n = e % 64;
+    wpack::put(blob, wpack::C1H, wpack::C1L, k, n, 64, f.p[f.w1 + e]);
+  }
+  for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
+    const int k = e / 64, n = e % 64;
+    wpack::put(blob, wpack::C2H, wpack::C2L, k, n, 64, f.p[f.w2 + e]);
+  }
+  for (int e = threadIdx.x; e < 64 * wg3::OD; e += blockDim.x) {
+    const int k = e / wg3::OD, n = e % wg3::OD;
+    wpack::put(blob, wpack::C3H, wpack::C3L, k, n, 48, f.p[f.w3 + e]);
+  }
+}
+
+cudaError_t launch_pack3_full(const wg3::Field3View& f, unsigned char* blob, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(blob, 0, wpack::BYTES, st);
+  if (e != cudaSuccess) return e;
+  pack3_full_kernel<<<1, 256, 0, st>>>(f, blob);
   return cudaGetLastError();
 }
 
 size_t grad_tc_pack_bytes() { return wpack::BYTES; }
+
+__global__ void __launch_bounds__(128, 1) grad_tc_kernel(TrainArgs a) { grad_tc_body<Tc2>(a); }
+__global__ void __launch_bounds__(128, 1) grad3_tc_kernel(TrainArgs3 a) { grad_tc_body<Tc3>(a); }
 
 }  // namespace wg

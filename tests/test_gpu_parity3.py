@@ -143,9 +143,12 @@ def test_records_match_oracle(gpu, o3):
     o3.field_destroy(fo)
 
 
-def test_field_grad_matches_oracle(gpu, o3):
-    """CUDA-core 3D training tile (fp32 MLP, fp64 loss) against the oracle's
-    fp64 gradient of the same minibatch."""
+@pytest.mark.parametrize("mlp", [MLP_EXACT, MLP_TENSOR])
+def test_field_grad_matches_oracle(gpu, o3, mlp):
+    """3D training tiles against the oracle's fp64 gradient of the same
+    minibatch: the CUDA-core tile (fp32 MLP, fp64 loss; MLP_EXACT) and the
+    tcgen05 tile (grad3_tc_kernel: split-fp16 forward / backward / weight
+    gradients in TMEM, fp64 loss at the outputs; MLP_TENSOR)."""
     sc = make_preset3("box-strip-vlin-obstacle", n=8).scene
     cfg_f = abi.field_config3()
     fo, fg = o3.field(cfg_f, BOX, 29), GuidingField3(cfg_f, BOX, 29)
@@ -154,7 +157,7 @@ def test_field_grad_matches_oracle(gpu, o3):
     recs = o3.walk_records(ho, fo, cfg, _outside_obstacle(probes3(3, 600, 0.05, 0.95)), 3, 0)
     tc = abi.train_config()
     g_o = o3.field_grad(fo, recs, tc)
-    sol = Solver3(Accel3(sc), fg, cfg)
+    sol = Solver3(Accel3(sc), fg, cfg, mlp)
     g_g = sol.field_grad(recs, tc)
     scale = np.abs(g_o).max()
     assert scale > 0
