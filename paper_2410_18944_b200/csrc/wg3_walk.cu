@@ -364,7 +364,7 @@ using namespace wg3;
 
 namespace {
 
-enum { C_STEPS = 0, C_ESCAPED = 1, C_WALKS = 2, C_REC_OVERFLOW = 3, C_SCENE_ERR = 4, C_N = 8 };
+enum { C_STEPS = 0, C_ESCAPED = 1, C_WALKS = 2, C_REC_OVERFLOW = 3, C_SCENE_ERR = 4, C_WAVE_LAUNCHES = 5, C_N = 8 };
 
 void field3_layout(wg_field_s* f) {
   const wg_field_config& c = f->cfg;
@@ -705,6 +705,9 @@ wg_train_stats sync3(wg_solver3_s* s, long long steps_before) {
   CK(cudaStreamSynchronize(s->st));
   unsigned long long c[C_N];
   CK(cudaMemcpy(c, s->counters.p, sizeof(c), cudaMemcpyDeviceToHost));
+  // kernels the device-side wavefront loops launched (counted on the device)
+  g_launches += static_cast<int64_t>(c[C_WAVE_LAUNCHES]);
+  CK(cudaMemset(s->counters.as<unsigned long long>() + C_WAVE_LAUNCHES, 0, sizeof(unsigned long long)));
   if (c[C_REC_OVERFLOW] > 0) {  // as in 2D (wg_solver.cu sync_collect): fail, grow for the next call
     s->rec_cap_min = std::max<int64_t>(s->rec_cap_min, 2 * s->rec_cap);
     char msg[256];

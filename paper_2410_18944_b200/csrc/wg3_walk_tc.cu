@@ -370,11 +370,20 @@ __global__ void wave_close_kernel(Walk3Args a, Wave3 v) {
   }
 }
 
+// end of a two-iteration body of the device-side loop: continue while the
+// last geometry pass queued slots or walk ids remain; count the kernels
+__global__ void wave_continue_kernel(Wave3 v, unsigned long long total, cudaGraphConditionalHandle cond,
+                                     unsigned long long* launches, unsigned body_kernels) {
+  if (threadIdx.x != 0) return;
+  const bool more = v.qlen[1] != 0u || *v.next_walk < total;
+  cudaGraphSetConditional(cond, more ? 1u : 0u);
+  atomicAdd(launches, static_cast<unsigned long long>(body_kernels));
+}
+
 cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsigned int* h_qlen,
                                int64_t* launches, cudaStream_t st) {
   *launches = 0;
   const unsigned long long total = static_cast<unsigned long long>(a.n_points) * a.n_rounds;
-  unsigned long long handed = 0;
   const int smem = walk3_tc_smem();
   cudaError_t e = cudaFuncSetAttribute(wave_dir_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -395,27 +404,54 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsi
   // persistent direction CTAs, 2 per SM (197 registers; cfg 4 frozen rounds
   // 2.84 s vs 2.91 s at 3 per SM and 3.07 s at 1)
   const int dir_blocks = sms * 2;
-  for (int it = 0;; ++it) {
-    const int par = it & 1;
-    if (sort_period > 0 && it > 0 && it % sort_period == 0) {
+  // The iteration loop runs on the device: a CUDA graph whose while node
+  // repeats a body of two iterations (parities 0 and 1) until a geometry
+  // pass queued nothing and every walk id is out; wave_continue_kernel sets
+  // the condition and counts the body's kernels into counters[5]. No host
+  // polling, no per-iteration launches from the host.
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  auto fail = [&](cudaError_t err) {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    return err;
+  };
+  if ((e = cudaGraphCreate(&graph, 0)) != cudaSuccess) return fail(e);
+  cudaGraphConditionalHandle cond;
+  if ((e = cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault)) != cudaSuccess)
+    return fail(e);
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = cond;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  if ((e = cudaGraphAddNode(&node, graph, nullptr, 0, &cp)) != cudaSuccess) return fail(e);
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  if ((e = cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) !=
+      cudaSuccess)
+    return fail(e);
+  unsigned body_kernels = 0;
+  for (int par = 0; par < 2; ++par) {
+    if (par == 0 || sort_period == 1) {
       cudaMemsetAsync(v.bins, 0, sizeof(unsigned int) * (kSortBins + 1), st);
       sort_count_kernel<<<sms * 2, 256, 0, st>>>(a, v);
       sort_scan_kernel<<<1, 1024, 0, st>>>(a, v);
       sort_scatter_kernel<<<sms * 2, 256, 0, st>>>(a, v);
-      *launches += 3;
+      body_kernels += 3;
     }
     wave_geom_kernel<<<geom_blocks, 128, 0, st>>>(a, v, par);
     wave_dir_kernel<<<dir_blocks, 128, smem, st>>>(a, v, par);
-    *launches += 2;
-    if ((it & 7) == 7) {  // every 8 iterations: stop once a geometry pass queued
-                          // nothing and every walk id has been handed out
-      cudaMemcpyAsync(h_qlen, v.qlen + par, sizeof(unsigned int), cudaMemcpyDeviceToHost, st);
-      cudaMemcpyAsync(&handed, v.next_walk, sizeof(handed), cudaMemcpyDeviceToHost, st);
-      e = cudaStreamSynchronize(st);
-      if (e != cudaSuccess) return e;
-      if (*h_qlen == 0u && handed >= total) break;
-    }
+    body_kernels += 2;
   }
+  wave_continue_kernel<<<1, 32, 0, st>>>(v, total, cond, a.counters + 5, body_kernels + 1);
+  cudaGraph_t captured = nullptr;
+  if ((e = cudaStreamEndCapture(st, &captured)) != cudaSuccess) return fail(e);
+  if ((e = cudaGraphInstantiate(&exec, graph, 0)) != cudaSuccess) return fail(e);
+  if ((e = cudaGraphLaunch(exec, st)) != cudaSuccess) return fail(e);
+  cudaGraphExecDestroy(exec);  // released once the launch completes
+  cudaGraphDestroy(graph);
+  (void)h_qlen;
   if (a.recs) {
     wave_close_kernel<<<geom_blocks, 128, 0, st>>>(a, v);
     *launches += 1;
