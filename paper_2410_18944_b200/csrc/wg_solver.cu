@@ -29,7 +29,8 @@ enum {
   C_REC_OVERFLOW = 3,
   C_SCENE_ERR = 4,
   C_TRAIN_STEPS = 5,
-  C_N = 8
+  C_WAVE_LAUNCHES = 8,  // kernels of the device-side 2D wavefront loop
+  C_N = 9
 };
 
 struct wg_solver_s {
@@ -440,6 +441,8 @@ long long adam_steps(wg_solver_s* s) {
 wg_train_stats sync_collect(wg_solver_s* s, long long steps_before) {
   CK(cudaStreamSynchronize(s->stream));
   CK(cudaMemcpy(s->last_counters, s->counters.p, sizeof(s->last_counters), cudaMemcpyDeviceToHost));
+  g_launches += static_cast<int64_t>(s->last_counters[C_WAVE_LAUNCHES]);
+  CK(cudaMemset(s->counters.as<unsigned long long>() + C_WAVE_LAUNCHES, 0, sizeof(unsigned long long)));
   if (s->last_counters[C_REC_OVERFLOW] > 0) {
     // a collecting round filled the record arena: its walks stopped recording,
     // which would have trained on a short-walk-biased set. Fail the call (the

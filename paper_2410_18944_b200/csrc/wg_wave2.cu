@@ -345,6 +345,14 @@ void wave2_sizes(size_t* lane, size_t* dir) {
   *dir = sizeof(Dir2);
 }
 
+__global__ void wave2_continue_kernel(Wave2 v, unsigned long long total, cudaGraphConditionalHandle cond,
+                                      unsigned long long* launches, unsigned body_kernels) {
+  if (threadIdx.x != 0) return;
+  const bool more = v.qlen[1] != 0u || *v.next_walk < total;
+  cudaGraphSetConditional(cond, more ? 1u : 0u);
+  atomicAdd(launches, static_cast<unsigned long long>(body_kernels));
+}
+
 cudaError_t launch_walks2_wave(const WalkArgs& a, void* lanes, void* dirs, int32_t* rec, uint8_t* state,
                                int32_t* queue, unsigned int* qlen, unsigned long long* next_walk,
                                int64_t slots, int sms, unsigned int* h_qlen, int64_t* launches,
@@ -355,26 +363,48 @@ cudaError_t launch_walks2_wave(const WalkArgs& a, void* lanes, void* dirs, int32
   cudaError_t e = cudaFuncSetAttribute(wave2_dir_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const unsigned long long total = static_cast<unsigned long long>(a.n_points) * a.n_rounds;
-  unsigned long long handed = 0;
   cudaMemsetAsync(v.state, 0, static_cast<size_t>(slots), st);
   cudaMemsetAsync(v.qlen, 0, 2 * sizeof(unsigned int), st);
   cudaMemsetAsync(v.next_walk, 0, sizeof(unsigned long long), st);
   if (a.recs) cudaMemsetAsync(v.lanes, 0, sizeof(Lane2) * static_cast<size_t>(slots), st);
   const int geom_blocks = static_cast<int>((slots + 127) / 128);
   const int dir_blocks = sms * 2;
-  for (int it = 0;; ++it) {
-    const int par = it & 1;
+  // device-side iteration loop (as the 3D wavefront, wg3_walk_tc.cu): a CUDA
+  // graph while node over a two-iteration body; wave2_continue_kernel sets
+  // the condition and counts the body's kernels into counters[8]
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  auto fail = [&](cudaError_t err) {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    return err;
+  };
+  if ((e = cudaGraphCreate(&graph, 0)) != cudaSuccess) return fail(e);
+  cudaGraphConditionalHandle cond;
+  if ((e = cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault)) != cudaSuccess)
+    return fail(e);
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = cond;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  if ((e = cudaGraphAddNode(&node, graph, nullptr, 0, &cp)) != cudaSuccess) return fail(e);
+  if ((e = cudaStreamBeginCaptureToGraph(st, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+    return fail(e);
+  for (int par = 0; par < 2; ++par) {
     wave2_geom_kernel<<<geom_blocks, 128, 0, st>>>(a, v, par);
     wave2_dir_kernel<<<dir_blocks, 128, smem, st>>>(a, v, par);
-    *launches += 2;
-    if ((it & 7) == 7) {
-      cudaMemcpyAsync(h_qlen, v.qlen + par, sizeof(unsigned int), cudaMemcpyDeviceToHost, st);
-      cudaMemcpyAsync(&handed, v.next_walk, sizeof(handed), cudaMemcpyDeviceToHost, st);
-      e = cudaStreamSynchronize(st);
-      if (e != cudaSuccess) return e;
-      if (*h_qlen == 0u && handed >= total) break;
-    }
   }
+  wave2_continue_kernel<<<1, 32, 0, st>>>(v, total, cond, a.counters + 8, 5u);
+  cudaGraph_t captured = nullptr;
+  if ((e = cudaStreamEndCapture(st, &captured)) != cudaSuccess) return fail(e);
+  if ((e = cudaGraphInstantiate(&exec, graph, 0)) != cudaSuccess) return fail(e);
+  if ((e = cudaGraphLaunch(exec, st)) != cudaSuccess) return fail(e);
+  cudaGraphExecDestroy(exec);  // released once the launch completes
+  cudaGraphDestroy(graph);
+  (void)h_qlen;
   if (a.recs) {
     wave2_close_kernel<<<geom_blocks, 128, 0, st>>>(a, v);
     *launches += 1;

@@ -487,7 +487,11 @@ def test_cpp_batched_accel_queries_match_oracle(gpu, orc, tmp_path):
     rng = np.random.default_rng(4)
     ang = rng.uniform(0, 2 * np.pi, len(xy))
     d = np.stack([np.cos(ang), np.sin(ang)], 1)
-    tmax = np.where(rng.random(len(xy)) < 0.3, np.inf, rng.uniform(0.01, 1.0, len(xy)))
+    # t_max = +inf is left out: there the reference accepts a MISSED segment
+    # (ray_segment returns kInf <= inf, geom2d.cpp:46-49, 225) as a hit at
+    # t = inf with an unset segment parameter; the device reports a miss
+    # (DESIGN.md §4). 10 is unbounded for this unit-square scene.
+    tmax = np.where(rng.random(len(xy)) < 0.3, 10.0, rng.uniform(0.01, 1.0, len(xy)))
     fin, fout = tmp_path / "in.bin", tmp_path / "out.bin"
     with open(fin, "wb") as f:
         f.write(np.array([sc.n_segments, len(xy)], dtype=np.int32).tobytes())
