@@ -76,47 +76,50 @@ def test_guided_relmse_and_variance_reduction_within_10_percent(gpu):
     assert abs(vr_ours - vr_ref) / vr_ref < 0.10, (vr_ours, vr_ref)
 
 
-def test_cfg3_seven_seed_relmse_and_vr(gpu):
-    """cfg 3 (const-source-disk: source term f = 4, eps = 1e-6, learnable MIS
-    with online training) at 128^2 x 256 wpp, seeds 1-7, against the
-    reference's own run_solve over the same seeds
-    (tests/golden/ref_cfg3_seeds.json, tests/golden/make_cfg3_seeds.py).
+def _trimmed(v, frac=0.1):
+    """mean of the central 80% (one run in ~20 of the learned estimator has
+    a few high-weight walks that lift its relMSE 2-10x, on the reference and
+    here alike)"""
+    v = np.sort(np.asarray(v, dtype=np.float64))
+    k = int(round(len(v) * frac))
+    return float(v[k:len(v) - k].mean())
 
-    The learned estimator is heavy-tailed over seeds: in ~1 run in 20 a few
-    high-weight walks lift one seed's relMSE 2-10x. The exact CUDA path (fp64
-    mixture, step-for-step parity with the reference) does the same (DESIGN.md
-    §10 "cfg 3 seed spread"), and six-seed means of either path spread over
-    0.00028-0.00043 across repeats. So compare a trimmed mean (each side's
-    worst seed dropped) within 20%; a wrong mixture, loss or MIS term moves
-    relMSE by integer factors (uniform is 7.5x). The uniform estimator uses the
-    same walks as the reference, so its mean matches to 1e-6."""
+
+@pytest.mark.parametrize("walk", ["wave", "lockstep"])
+def test_cfg3_seeds_relmse_and_vr_within_10_percent(gpu, monkeypatch, walk):
+    """cfg 3 (const-source-disk: source term f = 4, eps = 1e-6, learnable MIS
+    trained every round) at 128^2 x 256 wpp over 32 seeds, through the 2D
+    wavefront pair (forced: the pair the configured 512^2 grid selects) and
+    the lockstep kernel (the default at 128^2), against the reference's own
+    run_solve over its seeds (tests/golden/ref_cfg3_seeds.json,
+    tests/golden/make_cfg3_seeds.py): the trimmed-mean relMSE and the
+    variance-reduction factor over uniform within 10% of the reference's.
+    Uniform walks are the reference's walk for walk (seed 1 checked), so
+    both VR factors share the reference's uniform relMSE."""
     with open(os.path.join(G, "ref_cfg3_seeds.json")) as f:
         ref = json.load(f)
+    ref_g = [float(v) for v in ref["learnable_mis"].values()]
+    ref_u = float(np.mean([float(v) for v in ref["uniform"].values()]))
+    assert len(ref_g) >= 15
+    monkeypatch.setenv("WOSTGPU_WALK2", walk)
     pr = make_preset("const-source-disk")
     pts = cell_centers(128, 128, pr.eval_bbox)
     truth = np.array([pr.analytic(x, y) for x, y in pts])
     acc = api.Accel(pr.scene)
-    seeds = range(1, 8)
-    g, u = [], []
-    for seed in seeds:
+    g = []
+    for seed in range(1, 33):
         f = api.GuidingField(abi.field_config(), pr.scene.bbox, seed)
         s = api.Solver(acc, f, abi.solver_config("learnable_mis"), api.MLP_TENSOR)
         s.set_points(pts)
         s.run(seed, 256, 256, abi.train_config(seed=seed))
         g.append(relmse(s.stats()["mean"], truth))
-        us = api.Solver(acc, None, abi.solver_config("uniform"))
-        us.set_points(pts)
-        us.run(seed, 256, 0, None)
-        u.append(relmse(us.stats()["mean"], truth))
-
-    def trimmed(v):
-        return float(np.mean(sorted(v)[:-1]))
-
-    rg = trimmed([ref["learnable_mis"][str(i)] for i in seeds])
-    ru = np.mean([ref["uniform"][str(i)] for i in seeds])
-    assert np.mean(u) == pytest.approx(ru, rel=1e-6)
-    assert abs(trimmed(g) / rg - 1.0) < 0.20, (g, rg)
-    assert abs((np.mean(u) / trimmed(g)) / (ru / rg) - 1.0) < 0.20, (g, rg)
+    us = api.Solver(acc, None, abi.solver_config("uniform"))
+    us.set_points(pts)
+    us.run(1, 256, 0, None)
+    assert relmse(us.stats()["mean"], truth) == pytest.approx(float(ref["uniform"]["1"]), rel=1e-6)
+    ours, theirs = _trimmed(g), _trimmed(ref_g)
+    assert abs(ours / theirs - 1.0) < 0.10, (ours, theirs)
+    assert abs((ref_u / ours) / (ref_u / theirs) - 1.0) < 0.10, (ref_u / ours, ref_u / theirs)
 
 
 def test_cfg3_512_wavefront_per_point_matches_reference(gpu):
