@@ -72,6 +72,17 @@ struct __align__(8) Edge3 {
   double a[3], b[3], n0[3], n1[3];
   int32_t type, pad_;  // 0: always a silhouette, 1: crease (facing test)
 };
+// 4-wide node (128 B, 8 x 16-B loads) of the closest-Dirichlet-point BVH:
+// the binary tree collapsed so every node holds up to four children's fp32
+// boxes (outward-rounded, as Node3's). child[i] >= 0: an interior Node4;
+// child[i] < 0: a leaf, primitives [-(child[i]+1) >> 3, ... + (-(child[i]+1) & 7));
+// an empty slot has an inverted box (never visited).
+struct __align__(16) Node4 {
+  float lox[4], loy[4], loz[4], hix[4], hiy[4], hiz[4];
+  int32_t child[4];
+  int32_t pad_[4];
+};
+static_assert(sizeof(Node4) == 128, "Node4 layout");
 static_assert(sizeof(Node3) == 32, "Node3 layout");
 static_assert(sizeof(Tri3) == 88, "Tri3 layout");
 static_assert(sizeof(Edge3) == 104, "Edge3 layout");
@@ -80,6 +91,7 @@ struct Scene3View {
   const Node3* node[3];  // Dirichlet, Neumann, silhouette edges (nullptr if empty)
   const Tri3* tri[2];    // leaf-ordered triangles per kind
   const float4* tbox;    // [2 per Dirichlet triangle] fp32 box {lo, hi}, outward-rounded
+  const Node4* node4;    // the Dirichlet BVH collapsed 4-wide (closest-point queries)
   const Edge3* edge;     // leaf-ordered edges
   const wg_value3_spec* values;
   double bbox[6];
@@ -259,6 +271,97 @@ __device__ __forceinline__ void cp_bvh(const Node3* nodes, const Tri3* tris, D3 
   }
 }
 
+// closest point over the 4-wide Dirichlet BVH: per node the four children's
+// fp32 lower-bound distances, the nearest child descended into, the other
+// candidates pushed with their bound (a popped entry whose bound exceeds the
+// best is dropped without a load). Leaf children are tested when reached.
+// The same minimum over (d^2, id) as cp_bvh.
+__device__ __forceinline__ void cp_leaf(const Tri3* tris, const float4* tbox, D3 x, const PtBox& pb, int code,
+                                        CP3& best, float& bf) {
+  const int first = (-(code + 1)) >> 3, cnt = (-(code + 1)) & 7;
+  for (int i = first; i < first + cnt; ++i) {
+    if (tbox && box_d2_lb(tbox[2 * i], tbox[2 * i + 1], pb) > bf) continue;
+    const Tri3& t = tris[i];
+    D3 q = closest_on_tri(x, ld3(t.a), ld3(t.b), ld3(t.c));
+    D3 dq = sub(x, q);
+    double d2 = dot(dq, dq);
+    int id = t.id;
+    if (d2 < best.d2 || (d2 == best.d2 && id < best.tri)) {
+      best.d2 = d2;
+      best.p = q;
+      best.tri = id;
+      best.local = i;
+      bf = __double2float_ru(d2);
+    }
+  }
+}
+
+__device__ __forceinline__ void cp_bvh4(const Node4* nodes, const Tri3* tris, const float4* tbox, D3 x,
+                                        CP3& best) {
+  const PtBox pb = pt_box(x);
+  float bf = __double2float_ru(best.d2);
+  int st_code[48];
+  float st_key[48];
+  int sp = 0;
+  int node = 0;
+  for (;;) {
+    if (node >= 0) {
+      const float4* q = reinterpret_cast<const float4*>(nodes + node);
+      const float4 lx = __ldg(q), ly = __ldg(q + 1), lz = __ldg(q + 2);
+      const float4 hx = __ldg(q + 3), hy = __ldg(q + 4), hz = __ldg(q + 5);
+      const int4 ch = __ldg(reinterpret_cast<const int4*>(q + 6));
+      const float lxa[4] = {lx.x, lx.y, lx.z, lx.w}, lya[4] = {ly.x, ly.y, ly.z, ly.w};
+      const float lza[4] = {lz.x, lz.y, lz.z, lz.w}, hxa[4] = {hx.x, hx.y, hx.z, hx.w};
+      const float hya[4] = {hy.x, hy.y, hy.z, hy.w}, hza[4] = {hz.x, hz.y, hz.z, hz.w};
+      const int cha[4] = {ch.x, ch.y, ch.z, ch.w};
+      float km = __int_as_float(0x7f800000);
+      int cm = 0;
+      bool have = false;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float dx = fmaxf(fmaxf(__fsub_rd(lxa[i], pb.xu), __fsub_rd(pb.xl, hxa[i])), 0.0f);
+        const float dy = fmaxf(fmaxf(__fsub_rd(lya[i], pb.yu), __fsub_rd(pb.yl, hya[i])), 0.0f);
+        const float dz = fmaxf(fmaxf(__fsub_rd(lza[i], pb.zu), __fsub_rd(pb.zl, hza[i])), 0.0f);
+        const float k = __fadd_rd(__fadd_rd(__fmul_rd(dx, dx), __fmul_rd(dy, dy)), __fmul_rd(dz, dz));
+        if (k <= bf) {
+          if (!have || k < km) {  // new nearest: the previous nearest goes on the stack
+            if (have) {
+              st_code[sp] = cm;
+              st_key[sp] = km;
+              ++sp;
+            }
+            km = k;
+            cm = cha[i];
+            have = true;
+          } else {
+            st_code[sp] = cha[i];
+            st_key[sp] = k;
+            ++sp;
+          }
+        }
+      }
+      if (have) {
+        node = cm;
+        continue;
+      }
+    } else {
+      cp_leaf(tris, tbox, x, pb, node, best, bf);
+    }
+    // next: the most recently pushed entry still within the bound
+    node = 0;
+    bool found = false;
+    while (sp) {
+      --sp;
+      if (st_key[sp] <= bf) {
+        node = st_code[sp];
+        found = true;
+        break;
+      }
+    }
+    if (!found) return;
+  }
+}
+
 // closest Dirichlet point seeded with a candidate triangle (leaf-order index
 // `seed`, -1 for none): the candidate's exact distance bounds the traversal
 // from the start; the result is the same minimum over (d^2, id)
@@ -270,14 +373,18 @@ __device__ __forceinline__ CP3 closest_dirichlet_seeded(const Scene3View& s, D3 
     D3 dq = sub(x, q);
     best = {q, dot(dq, dq), t.id, seed};
   }
-  cp_bvh(s.node[0], s.tri[0], x, best, s.tbox);
+  if (s.node4) cp_bvh4(s.node4, s.tri[0], s.tbox, x, best);
+  else cp_bvh(s.node[0], s.tri[0], x, best, s.tbox);
   return best;
 }
 
 // Accel::closest_point analogue: (point, distance, triangle id) or id -1, d = inf
 __device__ __forceinline__ CP3 closest_point(const Scene3View& s, D3 x, unsigned kinds) {
   CP3 best{{0.0, 0.0, 0.0}, dinf(), -1, -1};
-  if (kinds & WG_KIND_DIRICHLET) cp_bvh(s.node[0], s.tri[0], x, best, s.tbox);
+  if (kinds & WG_KIND_DIRICHLET) {
+    if (s.node4) cp_bvh4(s.node4, s.tri[0], s.tbox, x, best);
+    else cp_bvh(s.node[0], s.tri[0], x, best, s.tbox);
+  }
   if (kinds & WG_KIND_NEUMANN) cp_bvh(s.node[1], s.tri[1], x, best);
   return best;
 }

@@ -10,6 +10,7 @@
 #include <array>
 #include <cfloat>
 #include <cmath>
+#include <functional>
 #include <map>
 #include <utility>
 
@@ -90,6 +91,66 @@ struct Builder {
     return id;
   }
 };
+
+// the binary BVH collapsed 4-wide (Node4, wg3_geom.cuh): a node's children
+// are its binary children with the internal one of largest surface area
+// replaced by its own two children until there are four; boxes are the
+// binary nodes' (outward-rounded) boxes
+std::vector<Node4> collapse4(const std::vector<Node3>& n3) {
+  std::vector<Node4> out;
+  if (n3.empty()) return out;
+  auto internal = [&](int i) { return n3[i].b >= 0; };
+  auto area = [&](int i) {
+    const double e[3] = {static_cast<double>(n3[i].hi[0]) - n3[i].lo[0], static_cast<double>(n3[i].hi[1]) - n3[i].lo[1],
+                         static_cast<double>(n3[i].hi[2]) - n3[i].lo[2]};
+    return e[0] * e[1] + e[1] * e[2] + e[2] * e[0];
+  };
+  auto leaf_code = [&](int i) {
+    const int first = n3[i].a, cnt = -n3[i].b;
+    return -((first << 3) | cnt) - 1;
+  };
+  std::function<int(int)> build = [&](int i) -> int {
+    const int id = static_cast<int>(out.size());
+    out.emplace_back();
+    std::vector<int> kids;
+    if (internal(i)) kids = {n3[i].a, n3[i].b};
+    else kids = {i};
+    while (kids.size() < 4) {
+      int best = -1;
+      double ba = -1.0;
+      for (size_t k = 0; k < kids.size(); ++k)
+        if (internal(kids[k]) && area(kids[k]) > ba) {
+          ba = area(kids[k]);
+          best = static_cast<int>(k);
+        }
+      if (best < 0) break;
+      const int c = kids[best];
+      kids[best] = n3[c].a;
+      kids.insert(kids.begin() + best + 1, n3[c].b);
+    }
+    Node4 n{};
+    for (int j = 0; j < 4; ++j) {
+      if (j < static_cast<int>(kids.size())) {
+        const Node3& c = n3[kids[j]];
+        n.lox[j] = c.lo[0];
+        n.loy[j] = c.lo[1];
+        n.loz[j] = c.lo[2];
+        n.hix[j] = c.hi[0];
+        n.hiy[j] = c.hi[1];
+        n.hiz[j] = c.hi[2];
+        n.child[j] = internal(kids[j]) ? build(kids[j]) : leaf_code(kids[j]);
+      } else {  // empty slot: an inverted box is never visited
+        n.lox[j] = n.loy[j] = n.loz[j] = INFINITY;
+        n.hix[j] = n.hiy[j] = n.hiz[j] = -INFINITY;
+        n.child[j] = 0;
+      }
+    }
+    out[id] = n;
+    return id;
+  };
+  build(0);
+  return out;
+}
 
 void cross3(const double* a, const double* b, double* o) {
   o[0] = a[1] * b[2] - a[2] * b[1];
@@ -341,6 +402,11 @@ int wostgpu_scene3_create(const double* tri, const int32_t* kind, const int32_t*
         s->tri[k].upload(leaf.data(), leaf.size());
         v.node[k] = s->node[k].as<Node3>();
         v.tri[k] = s->tri[k].as<Tri3>();
+        if (k == 0) {  // the 4-wide closest-point BVH
+          std::vector<Node4> n4 = collapse4(b.nodes);
+          s->node4.upload(n4.data(), n4.size());
+          v.node4 = s->node4.as<Node4>();
+        }
         if (k == 0) {  // fp32 boxes of the Dirichlet triangles, rounded outward (closest-point prefilter)
           std::vector<float> tb(8 * leaf.size());
           for (size_t i = 0; i < leaf.size(); ++i) {
