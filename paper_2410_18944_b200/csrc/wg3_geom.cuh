@@ -92,6 +92,8 @@ struct Scene3View {
   const Tri3* tri[2];    // leaf-ordered triangles per kind
   const float4* tbox;    // [2 per Dirichlet triangle] fp32 box {lo, hi}, outward-rounded
   const Node4* node4;    // the Dirichlet BVH collapsed 4-wide (closest-point queries)
+  const Node4* node4n;   // the Neumann BVH collapsed 4-wide (rays)
+  const Node4* node4e;   // the silhouette-edge BVH collapsed 4-wide
   const Edge3* edge;     // leaf-ordered edges
   const wg_value3_spec* values;
   double bbox[6];
@@ -296,6 +298,31 @@ __device__ __forceinline__ void cp_leaf(const Tri3* tris, const float4* tbox, D3
   }
 }
 
+struct Kids4 {
+  float lx[4], ly[4], lz[4], hx[4], hy[4], hz[4];
+  int c[4];
+};
+__device__ __forceinline__ void load4(const Node4* nodes, int node, Kids4& k) {
+  const float4* q = reinterpret_cast<const float4*>(nodes + node);
+  const float4 lx = __ldg(q), ly = __ldg(q + 1), lz = __ldg(q + 2);
+  const float4 hx = __ldg(q + 3), hy = __ldg(q + 4), hz = __ldg(q + 5);
+  const int4 ch = __ldg(reinterpret_cast<const int4*>(q + 6));
+  k.lx[0] = lx.x; k.lx[1] = lx.y; k.lx[2] = lx.z; k.lx[3] = lx.w;
+  k.ly[0] = ly.x; k.ly[1] = ly.y; k.ly[2] = ly.z; k.ly[3] = ly.w;
+  k.lz[0] = lz.x; k.lz[1] = lz.y; k.lz[2] = lz.z; k.lz[3] = lz.w;
+  k.hx[0] = hx.x; k.hx[1] = hx.y; k.hx[2] = hx.z; k.hx[3] = hx.w;
+  k.hy[0] = hy.x; k.hy[1] = hy.y; k.hy[2] = hy.z; k.hy[3] = hy.w;
+  k.hz[0] = hz.x; k.hz[1] = hz.y; k.hz[2] = hz.z; k.hz[3] = hz.w;
+  k.c[0] = ch.x; k.c[1] = ch.y; k.c[2] = ch.z; k.c[3] = ch.w;
+}
+
+__device__ __forceinline__ float kid_d2_lb(const Kids4& k, int i, const PtBox& pb) {
+  const float dx = fmaxf(fmaxf(__fsub_rd(k.lx[i], pb.xu), __fsub_rd(pb.xl, k.hx[i])), 0.0f);
+  const float dy = fmaxf(fmaxf(__fsub_rd(k.ly[i], pb.yu), __fsub_rd(pb.yl, k.hy[i])), 0.0f);
+  const float dz = fmaxf(fmaxf(__fsub_rd(k.lz[i], pb.zu), __fsub_rd(pb.zl, k.hz[i])), 0.0f);
+  return __fadd_rd(__fadd_rd(__fmul_rd(dx, dx), __fmul_rd(dy, dy)), __fmul_rd(dz, dz));
+}
+
 __device__ __forceinline__ void cp_bvh4(const Node4* nodes, const Tri3* tris, const float4* tbox, D3 x,
                                         CP3& best) {
   const PtBox pb = pt_box(x);
@@ -323,7 +350,7 @@ __device__ __forceinline__ void cp_bvh4(const Node4* nodes, const Tri3* tris, co
         const float dy = fmaxf(fmaxf(__fsub_rd(lya[i], pb.yu), __fsub_rd(pb.yl, hya[i])), 0.0f);
         const float dz = fmaxf(fmaxf(__fsub_rd(lza[i], pb.zu), __fsub_rd(pb.zl, hza[i])), 0.0f);
         const float k = __fadd_rd(__fadd_rd(__fmul_rd(dx, dx), __fmul_rd(dy, dy)), __fmul_rd(dz, dz));
-        if (k <= bf) {
+        if (k <= bf && lxa[i] <= hxa[i]) {  // (an empty slot has an inverted box)
           if (!have || k < km) {  // new nearest: the previous nearest goes on the stack
             if (have) {
               st_code[sp] = cm;
@@ -397,12 +424,76 @@ __device__ __forceinline__ bool is_silhouette(const Edge3& e, D3 x, double tol) 
   return f0 * f1 <= 0.0;
 }
 
+// the silhouette search over the 4-wide edge BVH (strict bound, as below)
+__device__ __forceinline__ double sil_bvh4(const Scene3View& s, D3 x, double bound2) {
+  double best = bound2;
+  const PtBox pb = pt_box(x);
+  float bf = __double2float_ru(best);
+  int st_code[48];
+  float st_key[48];
+  int sp = 0;
+  int node = 0;
+  for (;;) {
+    if (node >= 0) {
+      Kids4 k;
+      load4(s.node4e, node, k);
+      float km = __int_as_float(0x7f800000);
+      int cm = 0;
+      bool have = false;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float d = kid_d2_lb(k, i, pb);
+        if (d < bf && k.lx[i] <= k.hx[i]) {
+          if (!have || d < km) {
+            if (have) {
+              st_code[sp] = cm;
+              st_key[sp] = km;
+              ++sp;
+            }
+            km = d;
+            cm = k.c[i];
+            have = true;
+          } else {
+            st_code[sp] = k.c[i];
+            st_key[sp] = d;
+            ++sp;
+          }
+        }
+      }
+      if (have) {
+        node = cm;
+        continue;
+      }
+    } else {
+      const int first = (-(node + 1)) >> 3, cnt = (-(node + 1)) & 7;
+      for (int i = first; i < first + cnt; ++i) {
+        const Edge3& e = s.edge[i];
+        if (!is_silhouette(e, x, s.sil_tol)) continue;
+        D3 dq = sub(x, closest_on_seg(x, ld3(e.a), ld3(e.b)));
+        best = fmin(best, dot(dq, dq));
+      }
+      bf = __double2float_ru(best);
+    }
+    bool found = false;
+    while (sp) {
+      --sp;
+      if (st_key[sp] < bf) {
+        node = st_code[sp];
+        found = true;
+        break;
+      }
+    }
+    if (!found) return best;
+  }
+}
+
 // squared distance to the nearest silhouette edge (inf if none); with a
 // bound, only edges strictly closer than sqrt(bound2) are searched for and
 // bound2 comes back when there is none
 __device__ __forceinline__ double closest_silhouette_d2(const Scene3View& s, D3 x, double bound2 = dinf()) {
   const Node3* nodes = s.node[2];
   if (!nodes) return dinf();
+  if (s.node4e) return sil_bvh4(s, x, bound2);
   double best = bound2;
   const PtBox pb = pt_box(x);
   float bf = __double2float_ru(best);
@@ -521,6 +612,98 @@ __device__ __forceinline__ void ray_bvh(const Node3* nodes, const Tri3* tris, in
   }
 }
 
+// first hit over a 4-wide BVH: children slab-tested in fp32 (ray_box_f's
+// padded boxes), the nearest entry descended into, the others pushed with
+// their entry t; the same minimum over (t, id) as ray_bvh
+__device__ __forceinline__ void ray_bvh4(const Node4* nodes, const Tri3* tris, int kind, D3 o, D3 d,
+                                         double t_max, double t_eps, int exclude, Hit3& h, float pad) {
+  const bool dz[3] = {d.x == 0.0, d.y == 0.0, d.z == 0.0};
+  const float3 of = make_float3(static_cast<float>(o.x), static_cast<float>(o.y), static_cast<float>(o.z));
+  const float3 invf = make_float3(dz[0] ? 0.0f : static_cast<float>(1.0 / d.x),
+                                  dz[1] ? 0.0f : static_cast<float>(1.0 / d.y),
+                                  dz[2] ? 0.0f : static_cast<float>(1.0 / d.z));
+  float tb_f = __double2float_ru(fmin(t_max, h.t)) * (1.0f + 0x1.0p-20f);
+  int st_code[48];
+  float st_key[48];
+  int sp = 0;
+  int node = 0;
+  for (;;) {
+    if (node >= 0) {
+      Kids4 k;
+      load4(nodes, node, k);
+      float km = __int_as_float(0x7f800000);
+      int cm = 0;
+      bool have = false;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float t0 = 0.0f, t1 = tb_f;
+        bool hit = true;
+        const float lo[3] = {k.lx[i] - pad, k.ly[i] - pad, k.lz[i] - pad};
+        const float hi[3] = {k.hx[i] + pad, k.hy[i] + pad, k.hz[i] + pad};
+        const float oo[3] = {of.x, of.y, of.z}, iv[3] = {invf.x, invf.y, invf.z};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          if (dz[a]) {
+            hit = hit && !(oo[a] < lo[a] || oo[a] > hi[a]);
+          } else {
+            const float ta = (lo[a] - oo[a]) * iv[a], tb = (hi[a] - oo[a]) * iv[a];
+            t0 = fmaxf(t0, fminf(ta, tb));
+            t1 = fminf(t1, fmaxf(ta, tb));
+          }
+        }
+        hit = hit && t0 <= t1 && k.lx[i] <= k.hx[i];
+        if (hit) {
+          if (!have || t0 < km) {
+            if (have) {
+              st_code[sp] = cm;
+              st_key[sp] = km;
+              ++sp;
+            }
+            km = t0;
+            cm = k.c[i];
+            have = true;
+          } else {
+            st_code[sp] = k.c[i];
+            st_key[sp] = t0;
+            ++sp;
+          }
+        }
+      }
+      if (have) {
+        node = cm;
+        continue;
+      }
+    } else {
+      const int first = (-(node + 1)) >> 3, cnt = (-(node + 1)) & 7;
+      for (int i = first; i < first + cnt; ++i) {
+        const Tri3& t = tris[i];
+        const int id = t.id;
+        if (id == exclude) continue;
+        double th;
+        if (!ray_tri(o, d, ld3(t.a), ld3(t.b), ld3(t.c), &th)) continue;
+        if (!(th > t_eps && th <= t_max)) continue;
+        if (th < h.t || (th == h.t && id < h.tri)) {
+          h.t = th;
+          h.tri = id;
+          h.local = i;
+          h.kind = kind;
+          tb_f = __double2float_ru(fmin(t_max, h.t)) * (1.0f + 0x1.0p-20f);
+        }
+      }
+    }
+    bool found = false;
+    while (sp) {
+      --sp;
+      if (st_key[sp] <= tb_f) {
+        node = st_code[sp];
+        found = true;
+        break;
+      }
+    }
+    if (!found) return;
+  }
+}
+
 // box growth of the fp32 slab test: 2^-20 of the scene's coordinate scale
 __device__ __forceinline__ float ray_pad(const Scene3View& s) {
   double m = s.diag;
@@ -532,8 +715,14 @@ __device__ __forceinline__ Hit3 ray_first_hit(const Scene3View& s, D3 o, D3 d, d
                                               unsigned kinds, int exclude) {
   Hit3 h{dinf(), -1, -1, -1};
   const float pad = ray_pad(s);
-  if (kinds & WG_KIND_DIRICHLET) ray_bvh(s.node[0], s.tri[0], 0, o, d, t_max, s.t_eps, exclude, h, pad);
-  if (kinds & WG_KIND_NEUMANN) ray_bvh(s.node[1], s.tri[1], 1, o, d, t_max, s.t_eps, exclude, h, pad);
+  if (kinds & WG_KIND_DIRICHLET) {
+    if (s.node4) ray_bvh4(s.node4, s.tri[0], 0, o, d, t_max, s.t_eps, exclude, h, pad);
+    else ray_bvh(s.node[0], s.tri[0], 0, o, d, t_max, s.t_eps, exclude, h, pad);
+  }
+  if (kinds & WG_KIND_NEUMANN) {
+    if (s.node4n) ray_bvh4(s.node4n, s.tri[1], 1, o, d, t_max, s.t_eps, exclude, h, pad);
+    else ray_bvh(s.node[1], s.tri[1], 1, o, d, t_max, s.t_eps, exclude, h, pad);
+  }
   return h;
 }
 

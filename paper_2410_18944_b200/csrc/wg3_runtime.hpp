@@ -15,7 +15,7 @@ struct wg_scene3_s {
   double eps = 0, t_eps = 0, diag = 0;
   int64_t n_tri = 0, n_always = 0, n_crease = 0;
   int64_t n_node[3] = {0, 0, 0};
-  wgrt::DBuf node[3], tri[2], edge, values, tbox, node4;
+  wgrt::DBuf node[3], tri[2], edge, values, tbox, node4k[3];
   wg3::Scene3View view{};
 };
 

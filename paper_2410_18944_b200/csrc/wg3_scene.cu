@@ -402,10 +402,10 @@ int wostgpu_scene3_create(const double* tri, const int32_t* kind, const int32_t*
         s->tri[k].upload(leaf.data(), leaf.size());
         v.node[k] = s->node[k].as<Node3>();
         v.tri[k] = s->tri[k].as<Tri3>();
-        if (k == 0) {  // the 4-wide closest-point BVH
+        {  // the 4-wide BVHs (closest point / rays)
           std::vector<Node4> n4 = collapse4(b.nodes);
-          s->node4.upload(n4.data(), n4.size());
-          v.node4 = s->node4.as<Node4>();
+          s->node4k[k].upload(n4.data(), n4.size());
+          (k == 0 ? v.node4 : v.node4n) = s->node4k[k].as<Node4>();
         }
         if (k == 0) {  // fp32 boxes of the Dirichlet triangles, rounded outward (closest-point prefilter)
           std::vector<float> tb(8 * leaf.size());
@@ -441,6 +441,9 @@ int wostgpu_scene3_create(const double* tri, const int32_t* kind, const int32_t*
       s->edge.upload(leaf.data(), leaf.size());
       v.node[2] = s->node[2].as<Node3>();
       v.edge = s->edge.as<Edge3>();
+      std::vector<Node4> n4 = collapse4(b.nodes);
+      s->node4k[2].upload(n4.data(), n4.size());
+      v.node4e = s->node4k[2].as<Node4>();
     }
     s->values.upload(values, static_cast<size_t>(n_values));
     v.values = s->values.as<wg_value3_spec>();
