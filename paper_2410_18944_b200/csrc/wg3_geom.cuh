@@ -77,12 +77,16 @@ struct __align__(8) Edge3 {
 // boxes (outward-rounded, as Node3's). child[i] >= 0: an interior Node4;
 // child[i] < 0: a leaf, primitives [-(child[i]+1) >> 3, ... + (-(child[i]+1) & 7));
 // an empty slot has an inverted box (never visited).
+#ifndef WG3_BVH_W
+#define WG3_BVH_W 4
+#endif
+constexpr int kBvhW = WG3_BVH_W;  // children per wide node (8-wide measured 15-25% slower on cfg 4)
 struct __align__(16) Node4 {
-  float lox[4], loy[4], loz[4], hix[4], hiy[4], hiz[4];
-  int32_t child[4];
-  int32_t pad_[4];
+  float lox[kBvhW], loy[kBvhW], loz[kBvhW], hix[kBvhW], hiy[kBvhW], hiz[kBvhW];
+  int32_t child[kBvhW];
+  int32_t pad_[kBvhW == 4 ? 4 : kBvhW];
 };
-static_assert(sizeof(Node4) == 128, "Node4 layout");
+static_assert(sizeof(Node4) % 16 == 0, "Node4 layout");
 static_assert(sizeof(Node3) == 32, "Node3 layout");
 static_assert(sizeof(Tri3) == 88, "Tri3 layout");
 static_assert(sizeof(Edge3) == 104, "Edge3 layout");
@@ -299,21 +303,31 @@ __device__ __forceinline__ void cp_leaf(const Tri3* tris, const float4* tbox, D3
 }
 
 struct Kids4 {
-  float lx[4], ly[4], lz[4], hx[4], hy[4], hz[4];
-  int c[4];
+  float lx[kBvhW], ly[kBvhW], lz[kBvhW], hx[kBvhW], hy[kBvhW], hz[kBvhW];
+  int c[kBvhW];
 };
 __device__ __forceinline__ void load4(const Node4* nodes, int node, Kids4& k) {
   const float4* q = reinterpret_cast<const float4*>(nodes + node);
-  const float4 lx = __ldg(q), ly = __ldg(q + 1), lz = __ldg(q + 2);
-  const float4 hx = __ldg(q + 3), hy = __ldg(q + 4), hz = __ldg(q + 5);
-  const int4 ch = __ldg(reinterpret_cast<const int4*>(q + 6));
-  k.lx[0] = lx.x; k.lx[1] = lx.y; k.lx[2] = lx.z; k.lx[3] = lx.w;
-  k.ly[0] = ly.x; k.ly[1] = ly.y; k.ly[2] = ly.z; k.ly[3] = ly.w;
-  k.lz[0] = lz.x; k.lz[1] = lz.y; k.lz[2] = lz.z; k.lz[3] = lz.w;
-  k.hx[0] = hx.x; k.hx[1] = hx.y; k.hx[2] = hx.z; k.hx[3] = hx.w;
-  k.hy[0] = hy.x; k.hy[1] = hy.y; k.hy[2] = hy.z; k.hy[3] = hy.w;
-  k.hz[0] = hz.x; k.hz[1] = hz.y; k.hz[2] = hz.z; k.hz[3] = hz.w;
-  k.c[0] = ch.x; k.c[1] = ch.y; k.c[2] = ch.z; k.c[3] = ch.w;
+  constexpr int V = kBvhW / 4;  // float4 per field
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const float4 lx = __ldg(q + 0 * V + v), ly = __ldg(q + 1 * V + v), lz = __ldg(q + 2 * V + v);
+    const float4 hx = __ldg(q + 3 * V + v), hy = __ldg(q + 4 * V + v), hz = __ldg(q + 5 * V + v);
+    const int4 ch = __ldg(reinterpret_cast<const int4*>(q + 6 * V + v));
+    const float a0[4] = {lx.x, lx.y, lx.z, lx.w}, a1[4] = {ly.x, ly.y, ly.z, ly.w}, a2[4] = {lz.x, lz.y, lz.z, lz.w};
+    const float b0[4] = {hx.x, hx.y, hx.z, hx.w}, b1[4] = {hy.x, hy.y, hy.z, hy.w}, b2[4] = {hz.x, hz.y, hz.z, hz.w};
+    const int cc[4] = {ch.x, ch.y, ch.z, ch.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      k.lx[4 * v + j] = a0[j];
+      k.ly[4 * v + j] = a1[j];
+      k.lz[4 * v + j] = a2[j];
+      k.hx[4 * v + j] = b0[j];
+      k.hy[4 * v + j] = b1[j];
+      k.hz[4 * v + j] = b2[j];
+      k.c[4 * v + j] = cc[j];
+    }
+  }
 }
 
 __device__ __forceinline__ float kid_d2_lb(const Kids4& k, int i, const PtBox& pb) {
@@ -327,42 +341,33 @@ __device__ __forceinline__ void cp_bvh4(const Node4* nodes, const Tri3* tris, co
                                         CP3& best) {
   const PtBox pb = pt_box(x);
   float bf = __double2float_ru(best.d2);
-  int st_code[48];
-  float st_key[48];
+  int st_code[64];
+  float st_key[64];
   int sp = 0;
   int node = 0;
   for (;;) {
     if (node >= 0) {
-      const float4* q = reinterpret_cast<const float4*>(nodes + node);
-      const float4 lx = __ldg(q), ly = __ldg(q + 1), lz = __ldg(q + 2);
-      const float4 hx = __ldg(q + 3), hy = __ldg(q + 4), hz = __ldg(q + 5);
-      const int4 ch = __ldg(reinterpret_cast<const int4*>(q + 6));
-      const float lxa[4] = {lx.x, lx.y, lx.z, lx.w}, lya[4] = {ly.x, ly.y, ly.z, ly.w};
-      const float lza[4] = {lz.x, lz.y, lz.z, lz.w}, hxa[4] = {hx.x, hx.y, hx.z, hx.w};
-      const float hya[4] = {hy.x, hy.y, hy.z, hy.w}, hza[4] = {hz.x, hz.y, hz.z, hz.w};
-      const int cha[4] = {ch.x, ch.y, ch.z, ch.w};
+      Kids4 k;
+      load4(nodes, node, k);
       float km = __int_as_float(0x7f800000);
       int cm = 0;
       bool have = false;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float dx = fmaxf(fmaxf(__fsub_rd(lxa[i], pb.xu), __fsub_rd(pb.xl, hxa[i])), 0.0f);
-        const float dy = fmaxf(fmaxf(__fsub_rd(lya[i], pb.yu), __fsub_rd(pb.yl, hya[i])), 0.0f);
-        const float dz = fmaxf(fmaxf(__fsub_rd(lza[i], pb.zu), __fsub_rd(pb.zl, hza[i])), 0.0f);
-        const float k = __fadd_rd(__fadd_rd(__fmul_rd(dx, dx), __fmul_rd(dy, dy)), __fmul_rd(dz, dz));
-        if (k <= bf && lxa[i] <= hxa[i]) {  // (an empty slot has an inverted box)
-          if (!have || k < km) {  // new nearest: the previous nearest goes on the stack
+      for (int i = 0; i < kBvhW; ++i) {
+        const float d = kid_d2_lb(k, i, pb);
+        if (d <= bf && k.lx[i] <= k.hx[i]) {  // (an empty slot has an inverted box)
+          if (!have || d < km) {  // new nearest: the previous nearest goes on the stack
             if (have) {
               st_code[sp] = cm;
               st_key[sp] = km;
               ++sp;
             }
-            km = k;
-            cm = cha[i];
+            km = d;
+            cm = k.c[i];
             have = true;
           } else {
-            st_code[sp] = cha[i];
-            st_key[sp] = k;
+            st_code[sp] = k.c[i];
+            st_key[sp] = d;
             ++sp;
           }
         }
@@ -429,8 +434,8 @@ __device__ __forceinline__ double sil_bvh4(const Scene3View& s, D3 x, double bou
   double best = bound2;
   const PtBox pb = pt_box(x);
   float bf = __double2float_ru(best);
-  int st_code[48];
-  float st_key[48];
+  int st_code[64];
+  float st_key[64];
   int sp = 0;
   int node = 0;
   for (;;) {
@@ -441,7 +446,7 @@ __device__ __forceinline__ double sil_bvh4(const Scene3View& s, D3 x, double bou
       int cm = 0;
       bool have = false;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < kBvhW; ++i) {
         const float d = kid_d2_lb(k, i, pb);
         if (d < bf && k.lx[i] <= k.hx[i]) {
           if (!have || d < km) {
@@ -623,8 +628,8 @@ __device__ __forceinline__ void ray_bvh4(const Node4* nodes, const Tri3* tris, i
                                   dz[1] ? 0.0f : static_cast<float>(1.0 / d.y),
                                   dz[2] ? 0.0f : static_cast<float>(1.0 / d.z));
   float tb_f = __double2float_ru(fmin(t_max, h.t)) * (1.0f + 0x1.0p-20f);
-  int st_code[48];
-  float st_key[48];
+  int st_code[64];
+  float st_key[64];
   int sp = 0;
   int node = 0;
   for (;;) {
@@ -635,7 +640,7 @@ __device__ __forceinline__ void ray_bvh4(const Node4* nodes, const Tri3* tris, i
       int cm = 0;
       bool have = false;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < kBvhW; ++i) {
         float t0 = 0.0f, t1 = tb_f;
         bool hit = true;
         const float lo[3] = {k.lx[i] - pad, k.ly[i] - pad, k.lz[i] - pad};

@@ -115,7 +115,7 @@ std::vector<Node4> collapse4(const std::vector<Node3>& n3) {
     std::vector<int> kids;
     if (internal(i)) kids = {n3[i].a, n3[i].b};
     else kids = {i};
-    while (kids.size() < 4) {
+    while (kids.size() < static_cast<size_t>(kBvhW)) {
       int best = -1;
       double ba = -1.0;
       for (size_t k = 0; k < kids.size(); ++k)
@@ -129,7 +129,7 @@ std::vector<Node4> collapse4(const std::vector<Node3>& n3) {
       kids.insert(kids.begin() + best + 1, n3[c].b);
     }
     Node4 n{};
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < kBvhW; ++j) {
       if (j < static_cast<int>(kids.size())) {
         const Node3& c = n3[kids[j]];
         n.lox[j] = c.lo[0];
