@@ -1,3 +1,4 @@
+#include <cstdlib>
 // 3D guided walks with the guiding-field MLP on the 5th-generation tensor
 // cores (the WG_MLP_TENSOR path of the 3D solver; default for the default 3D
 // field shape).
@@ -399,7 +400,7 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsi
   // 512^2 x 256 frozen rounds: 3.25 s (every iteration) / 3.34 s (every
   // second) vs 3.91 s unsorted; 32 training rounds 0.91 / 0.89 / 0.88 s.
   // 4 bits per axis: 5 bits measured no faster (3.27 s; training 0.99 s)
-  const int sort_period = a.recs ? 2 : 1;
+  const int sort_period = a.recs ? 2 : 1;  // (with wide BVHs: frozen rounds equal at 1 and 2)
   const int geom_blocks = static_cast<int>((v.slots + 127) / 128);
   // persistent direction CTAs, 2 per SM (197 registers; cfg 4 frozen rounds
   // 2.84 s vs 2.91 s at 3 per SM and 3.07 s at 1)
@@ -409,6 +410,34 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsi
   // pass queued nothing and every walk id is out; wave_continue_kernel sets
   // the condition and counts the body's kernels into counters[5]. No host
   // polling, no per-iteration launches from the host.
+  // WOSTGPU_PROFILE_LOOP=1 (profiling only): the same iterations launched
+  // from the host, so kernel profilers see every launch (ncu does not
+  // profile the device-launched bodies of a conditional graph node)
+  static const bool host_loop = [] {
+    const char* pe = std::getenv("WOSTGPU_PROFILE_LOOP");
+    return pe && pe[0] == '1';
+  }();
+  if (host_loop) {
+    for (int it = 0;; it += 2) {
+      for (int par = 0; par < 2; ++par) {
+        if (par == 0 || sort_period == 1) {
+          cudaMemsetAsync(v.bins, 0, sizeof(unsigned int) * (kSortBins + 1), st);
+          sort_count_kernel<<<sms * 2, 256, 0, st>>>(a, v);
+          sort_scan_kernel<<<1, 1024, 0, st>>>(a, v);
+          sort_scatter_kernel<<<sms * 2, 256, 0, st>>>(a, v);
+          *launches += 3;
+        }
+        wave_geom_kernel<<<geom_blocks, 128, 0, st>>>(a, v, par);
+        wave_dir_kernel<<<dir_blocks, 128, smem, st>>>(a, v, par);
+        *launches += 2;
+      }
+      unsigned long long h[2] = {0, 0};
+      cudaMemcpyAsync(&h[0], v.qlen + 1, sizeof(unsigned int), cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(&h[1], v.next_walk, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+      if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+      if (static_cast<unsigned int>(h[0]) == 0u && h[1] >= total) break;
+    }
+  } else {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   auto fail = [&](cudaError_t err) {
@@ -451,6 +480,7 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsi
   if ((e = cudaGraphLaunch(exec, st)) != cudaSuccess) return fail(e);
   cudaGraphExecDestroy(exec);  // released once the launch completes
   cudaGraphDestroy(graph);
+  }
   (void)h_qlen;
   if (a.recs) {
     wave_close_kernel<<<geom_blocks, 128, 0, st>>>(a, v);
