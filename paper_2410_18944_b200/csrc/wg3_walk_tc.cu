@@ -163,7 +163,7 @@ enum : uint8_t { SLOT_EMPTY = 0, SLOT_NEED_DIR = 1, SLOT_NEED_MOVE = 2 };
 // at 512^2 x 8 wpp against the unconstrained 132-register build; the
 // tensor-core direction kernel is best left at 2 CTAs/SM (3: 193 ms)
 #ifndef WG3_GEOM_MINB
-#define WG3_GEOM_MINB 5
+#define WG3_GEOM_MINB 6
 #endif
 #ifndef WG3_DIR_MINB
 #define WG3_DIR_MINB 1
@@ -404,7 +404,10 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsi
   const int geom_blocks = static_cast<int>((v.slots + 127) / 128);
   // persistent direction CTAs, 2 per SM (197 registers; cfg 4 frozen rounds
   // 2.84 s vs 2.91 s at 3 per SM and 3.07 s at 1)
-  const int dir_blocks = sms * 2;
+#ifndef WG3_DIR_PER_SM
+#define WG3_DIR_PER_SM 2
+#endif
+  const int dir_blocks = sms * WG3_DIR_PER_SM;
   // The iteration loop runs on the device: a CUDA graph whose while node
   // repeats a body of two iterations (parities 0 and 1) until a geometry
   // pass queued nothing and every walk id is out; wave_continue_kernel sets
