@@ -3,6 +3,7 @@
 // evaluation. The solver (walk rounds, training, Engine loop) is wg_solver.cu.
 #include <dlfcn.h>
 
+#include <functional>
 #include <map>
 
 #include "wg_runtime.hpp"
@@ -369,7 +370,47 @@ int wostgpu_scene_create(const double* seg, const int32_t* kind, const int32_t* 
         normals[vi].push_back(ny);
       }
     }
-    for (size_t v = 0; v < pos.size(); ++v) {
+    // silhouette candidates in index order, or (above 32 vertices) in the leaf
+    // order of a point BVH (median split on the longer axis, leaves <= 4):
+    // closest_silhouette is a minimum over vertices, so any order gives the
+    // reference's value (geom2d.cpp:182-200 scans them linearly)
+    std::vector<int> vorder(pos.size());
+    for (size_t v = 0; v < pos.size(); ++v) vorder[v] = (int)v;
+    if (pos.size() > 32) {
+      std::function<int(int, int)> build = [&](int b0, int e0) -> int {
+        const int id = (int)s->h_sil_nodes.size();
+        s->h_sil_nodes.emplace_back();
+        Node n{};
+        n.lox = n.loy = INFINITY;
+        n.hix = n.hiy = -INFINITY;
+        for (int i = b0; i < e0; ++i) {
+          const auto& p = pos[vorder[i]];
+          n.lox = std::min(n.lox, p.first);
+          n.loy = std::min(n.loy, p.second);
+          n.hix = std::max(n.hix, p.first);
+          n.hiy = std::max(n.hiy, p.second);
+        }
+        if (e0 - b0 <= 4) {
+          n.left = n.right = -1;
+          n.begin = b0;
+          n.end = e0;
+        } else {
+          const bool ax = (n.hix - n.lox) >= (n.hiy - n.loy);
+          const int mid = (b0 + e0) / 2;
+          std::nth_element(vorder.begin() + b0, vorder.begin() + mid, vorder.begin() + e0, [&](int a_, int b_) {
+            const double ka = ax ? pos[a_].first : pos[a_].second, kb = ax ? pos[b_].first : pos[b_].second;
+            return ka < kb || (ka == kb && a_ < b_);
+          });
+          n.begin = n.end = 0;
+          n.left = build(b0, mid);
+          n.right = build(mid, e0);
+        }
+        s->h_sil_nodes[id] = n;
+        return id;
+      };
+      build(0, (int)pos.size());
+    }
+    for (int v : vorder) {
       SilVertex sv;
       sv.px = pos[v].first;
       sv.py = pos[v].second;
@@ -399,6 +440,7 @@ int wostgpu_scene_create(const double* seg, const int32_t* kind, const int32_t* 
     s->segs.upload(order.data(), order.size());
     s->sil.upload(s->h_sil.data(), s->h_sil.size());
     s->sil_n.upload(s->h_sil_n.data(), s->h_sil_n.size());
+    if (!s->h_sil_nodes.empty()) s->sil_nodes.upload(s->h_sil_nodes.data(), s->h_sil_nodes.size());
     s->seg_kind.upload(hk.data(), hk.size());
     s->seg_value.upload(hv.data(), hv.size());
     s->values.upload(dv.data(), dv.size());
@@ -411,6 +453,7 @@ int wostgpu_scene_create(const double* seg, const int32_t* kind, const int32_t* 
     v.n_segs = n_seg;
     v.n_sil = (int32_t)s->h_sil.size();
     v.n_sil_normals = (int32_t)(s->h_sil_n.size() / 2);
+    v.sil_nodes = s->h_sil_nodes.empty() ? nullptr : s->sil_nodes.as<Node>();
     v.seg_kind = s->seg_kind.as<int32_t>();
     v.seg_value = s->seg_value.as<int32_t>();
     v.values = s->values.as<DevValue>();

@@ -116,6 +116,7 @@ struct SceneView {
   int32_t has_flux, source_zero;
   int32_t n_neumann;  // Neumann segments: without any, Neumann-kind rays cannot hit
   int32_t pad_;
+  const Node* sil_nodes;  // point BVH over the silhouette candidates (> 32 of them), else null
 };
 
 WG_D double eval_value(const DevValue& v, double x, double y) {
@@ -209,26 +210,50 @@ WG_D CP closest_point(const SceneView& s, double x, double y, unsigned kinds) {
 // over candidate vertices, so any visiting order gives the same value; the
 // scan compares squared distances and takes one sqrt at the end, which is the
 // same value (a correctly rounded sqrt is monotone, so min and sqrt commute).
+WG_D void sil_vertex(const SceneView& s, int v, double x, double y, double& best) {
+  const SilVertex sv = s.sil[v];
+  double dx = sv.px - x, dy = sv.py - y;
+  double d = dx * dx + dy * dy;
+  if (d >= best) return;
+  bool cand = sv.n_count < 2;
+  if (!cand) {
+    double lo = dinf(), hi = -dinf();
+    for (int k = 0; k < sv.n_count; ++k) {
+      double nx = s.sil_n[2 * (sv.n_begin + k)], ny = s.sil_n[2 * (sv.n_begin + k) + 1];
+      double f = nx * dx + ny * dy;
+      lo = smin(lo, f);
+      hi = smax(hi, f);
+    }
+    cand = lo * hi <= 0.0;
+  }
+  if (cand) best = d;
+}
+
 WG_D double closest_silhouette(const SceneView& s, double x, double y) {
   double best = dinf();
-#pragma unroll 2
-  for (int v = 0; v < s.n_sil; ++v) {
-    const SilVertex sv = s.sil[v];
-    double dx = sv.px - x, dy = sv.py - y;
-    double d = dx * dx + dy * dy;
-    if (d >= best) continue;
-    bool cand = sv.n_count < 2;
-    if (!cand) {
-      double lo = dinf(), hi = -dinf();
-      for (int k = 0; k < sv.n_count; ++k) {
-        double nx = s.sil_n[2 * (sv.n_begin + k)], ny = s.sil_n[2 * (sv.n_begin + k) + 1];
-        double f = nx * dx + ny * dy;
-        lo = smin(lo, f);
-        hi = smax(hi, f);
+  if (s.sil_nodes) {  // indexed: boxes at or beyond the best squared distance are skipped
+    int st[64];
+    int top = 0;
+    st[top++] = 0;
+    while (top > 0) {
+      const Node nd = s.sil_nodes[st[--top]];
+      if (box_d2(nd, x, y) >= best) continue;
+      if (nd.left < 0) {
+        for (int v = nd.begin; v < nd.end; ++v) sil_vertex(s, v, x, y, best);
+      } else {
+        const double dl = box_d2(s.sil_nodes[nd.left], x, y), dr = box_d2(s.sil_nodes[nd.right], x, y);
+        if (dl <= dr) {
+          st[top++] = nd.right;
+          st[top++] = nd.left;
+        } else {
+          st[top++] = nd.left;
+          st[top++] = nd.right;
+        }
       }
-      cand = lo * hi <= 0.0;
     }
-    if (cand) best = d;
+  } else {
+#pragma unroll 2
+    for (int v = 0; v < s.n_sil; ++v) sil_vertex(s, v, x, y, best);
   }
   return best == dinf() ? best : sqrt(best);
 }

@@ -146,7 +146,8 @@ struct wg_scene_s {
   std::vector<wg::Seg> h_segs;
   std::vector<wg::SilVertex> h_sil;
   std::vector<double> h_sil_n;
-  wgrt::DBuf nodes, segs, sil, sil_n, seg_kind, seg_value, values;
+  std::vector<wg::Node> h_sil_nodes;  // point BVH over the silhouette candidates (> 32)
+  wgrt::DBuf nodes, segs, sil, sil_n, seg_kind, seg_value, values, sil_nodes;
   std::vector<std::unique_ptr<wgrt::DBuf>> rasters;
   wg::DevValue source{};
   wg::SceneView view{};
