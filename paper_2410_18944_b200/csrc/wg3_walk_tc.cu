@@ -1,3 +1,5 @@
+#include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 // 3D guided walks with the guiding-field MLP on the 5th-generation tensor
 // cores (the WG_MLP_TENSOR path of the 3D solver; default for the default 3D
@@ -158,6 +160,10 @@ __global__ void __launch_bounds__(128) field3_eval_tc_kernel(Field3View f, int64
 //                     sampling (no BVH work, so no lockstep divergence).
 // The host re-launches the pair until a geometry pass queues nothing.
 enum : uint8_t { SLOT_EMPTY = 0, SLOT_NEED_DIR = 1, SLOT_NEED_MOVE = 2 };
+// walks left at the drain hand-off to wave_tail_kernel: cfg 4 shape, 32 training
+// rounds 408-434 ms at 37,888-131,072 vs 553-563 ms without (and 534-544 ms
+// with every walk in the tail kernel); frozen rounds unchanged
+constexpr long kTailDefault = 65536;
 // occupancy of the latency-bound geometry kernel: 5 CTAs/SM (<= 102
 // registers, a few hundred bytes of spills) measured 144 vs 171 ms walk time
 // at 512^2 x 8 wpp against the unconstrained 132-register build; the
@@ -362,6 +368,79 @@ __global__ void __launch_bounds__(128, WG3_DIR_MINB) wave_dir_kernel(Walk3Args a
   wg::tc_teardown(smem);
 }
 
+// The drain of a call: once every walk id is out and at most tail_n walks
+// remain, the device loop exits and this kernel finishes them in lockstep
+// CTAs like walk3_tc_kernel: pending move, begin_step, gather + MLP on the
+// tensor cores for the rows still walking, MIS draw, repeat. A row whose walk
+// ends takes the next walk of the last queue (qlen[0], zeroed by the last
+// direction pass, counts the hand-out). Same step functions and MLP as the
+// wavefront pair, so every walk's result is unchanged; what goes is the
+// per-iteration cost of the drain (sort, two launches, the direction
+// kernel's weight fetch, a geometry grid over the whole pool) while the
+// round's longest walks finish.
+__global__ void __launch_bounds__(128, 2) wave_tail_kernel(Walk3Args a, Wave3 v) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const unsigned int n = v.qlen[1];
+  // first an even share of the queue per CTA (<= 128 rows), then one at a time
+  const unsigned int per = min(128u, (n + gridDim.x - 1) / gridDim.x);
+  const unsigned int spread = per * gridDim.x;
+  if (static_cast<unsigned int>(blockIdx.x) * per >= n) return;
+  wg::tc_fetch_weights(smem, v.wblob);
+  wg::tc_setup(smem);
+  wg::umma::fence_before();
+  __syncthreads();
+  wg::umma::fence_after();
+  wg::tc_wait_weights(smem);
+  const bool collect = a.recs != nullptr;
+  int32_t slot = -1;
+  Lane3 w;
+  w.alive = false;
+  Dir3 d{};
+  int rec = -1;
+  bool need = false, more = true, first = true;
+  uint32_t phase = 0;
+  for (;;) {
+    if (need) {  // the geometry pass's work for this slot (no walk ids left to claim)
+      step_move(w, a, collect, rec, d, true);
+      need = w.alive && step_begin(w, a, collect, rec);
+    }
+    while (!need && more) {  // next walk of the queue, with its pending move
+      if (slot >= 0) {
+        if (collect) v.lanes[slot] = w;  // record-chunk bookkeeping for wave_close_kernel
+        v.state[slot] = SLOT_EMPTY;
+        slot = -1;
+      }
+      const unsigned int i = first ? blockIdx.x * per + threadIdx.x : spread + claim_queue(v.qlen);
+      first = false;
+      if (i >= n || (i < spread && threadIdx.x >= per)) {
+        more = false;
+        break;
+      }
+      slot = v.queue[i];
+      w = v.lanes[slot];
+      d = v.dirs[slot];
+      rec = v.rec[slot];
+      step_move(w, a, collect, rec, d, true);
+      need = w.alive && step_begin(w, a, collect, rec);
+    }
+    if (__syncthreads_count(need) == 0) break;
+    float in[IN], raw[OD];  // the direction pass's
+    if (need) {
+      gather3_tc(a.f, w.x, in);
+    } else {
+#pragma unroll
+      for (int i = 0; i < IN; ++i) in[i] = 0.0f;
+    }
+    wg::tc_forward<OD>(smem, phase, in, raw);
+    if (need) d = sample_guided_f(w, a, raw);
+  }
+  if (slot >= 0) {
+    if (collect) v.lanes[slot] = w;
+    v.state[slot] = SLOT_EMPTY;
+  }
+  wg::tc_teardown(smem);
+}
+
 // trailing record slots of every lane's last chunk are marked unused
 __global__ void wave_close_kernel(Walk3Args a, Wave3 v) {
   for (int64_t slot = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; slot < v.slots;
@@ -371,12 +450,14 @@ __global__ void wave_close_kernel(Walk3Args a, Wave3 v) {
   }
 }
 
-// end of a two-iteration body of the device-side loop: continue while the
-// last geometry pass queued slots or walk ids remain; count the kernels
-__global__ void wave_continue_kernel(Wave3 v, unsigned long long total, cudaGraphConditionalHandle cond,
-                                     unsigned long long* launches, unsigned body_kernels) {
+// end of a two-iteration body of the device-side loop: continue while walk
+// ids remain or the last geometry pass queued more than tail_n slots (the
+// rest go to wave_tail_kernel); count the kernels
+__global__ void wave_continue_kernel(Wave3 v, unsigned long long total, unsigned int tail_n,
+                                     cudaGraphConditionalHandle cond, unsigned long long* launches,
+                                     unsigned body_kernels) {
   if (threadIdx.x != 0) return;
-  const bool more = v.qlen[1] != 0u || *v.next_walk < total;
+  const bool more = v.qlen[1] > tail_n || *v.next_walk < total;
   cudaGraphSetConditional(cond, more ? 1u : 0u);
   atomicAdd(launches, static_cast<unsigned long long>(body_kernels));
 }
@@ -408,6 +489,18 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsi
 #define WG3_DIR_PER_SM 2
 #endif
   const int dir_blocks = sms * WG3_DIR_PER_SM;
+  // the drain hand-off: 2 tail CTAs per SM of 128 rows
+  // (WOSTGPU_WAVE3_TAIL = walks left when the device loop hands over; 0 = off)
+  const int tail_blocks = sms * 2;
+  const char* tail_pe = std::getenv("WOSTGPU_WAVE3_TAIL");  // read per call (tests switch it)
+  const long tail_env = tail_pe ? std::atol(tail_pe) : -1L;
+  const unsigned int tail_n = static_cast<unsigned int>(
+      tail_env >= 0 ? tail_env : kTailDefault);
+  if (tail_n) {
+    if ((e = cudaFuncSetAttribute(wave_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
+        cudaSuccess)
+      return e;
+  }
   // The iteration loop runs on the device: a CUDA graph whose while node
   // repeats a body of two iterations (parities 0 and 1) until a geometry
   // pass queued nothing and every walk id is out; wave_continue_kernel sets
@@ -416,13 +509,22 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsi
   // WOSTGPU_PROFILE_LOOP=1 (profiling only): the same iterations launched
   // from the host, so kernel profilers see every launch (ncu does not
   // profile the device-launched bodies of a conditional graph node)
-  static const bool host_loop = [] {
+  // WOSTGPU_PROFILE_LOOP=2: also times each pass with events and prints
+  // (iteration, queued walks, sort / geometry / direction microseconds)
+  static const int host_loop = [] {
     const char* pe = std::getenv("WOSTGPU_PROFILE_LOOP");
-    return pe && pe[0] == '1';
+    return pe && (pe[0] == '1' || pe[0] == '2') ? pe[0] - '0' : 0;
   }();
   if (host_loop) {
+    cudaEvent_t ev[4];
+    for (auto& x : ev) cudaEventCreate(&x);
     for (int it = 0;; it += 2) {
       for (int par = 0; par < 2; ++par) {
+        unsigned int q0 = 0;
+        if (host_loop == 2) {
+          cudaMemcpyAsync(&q0, v.qlen + (par ^ 1), sizeof(unsigned int), cudaMemcpyDeviceToHost, st);
+          cudaEventRecord(ev[0], st);
+        }
         if (par == 0 || sort_period == 1) {
           cudaMemsetAsync(v.bins, 0, sizeof(unsigned int) * (kSortBins + 1), st);
           sort_count_kernel<<<sms * 2, 256, 0, st>>>(a, v);
@@ -430,16 +532,27 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsi
           sort_scatter_kernel<<<sms * 2, 256, 0, st>>>(a, v);
           *launches += 3;
         }
+        if (host_loop == 2) cudaEventRecord(ev[1], st);
         wave_geom_kernel<<<geom_blocks, 128, 0, st>>>(a, v, par);
+        if (host_loop == 2) cudaEventRecord(ev[2], st);
         wave_dir_kernel<<<dir_blocks, 128, smem, st>>>(a, v, par);
+        if (host_loop == 2) {
+          cudaEventRecord(ev[3], st);
+          cudaEventSynchronize(ev[3]);
+          float t[3];
+          for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
+          std::fprintf(stderr, "wave3 it %d live %u sort %.1f geom %.1f dir %.1f\n", it + par, q0, t[0] * 1e3f,
+                       t[1] * 1e3f, t[2] * 1e3f);
+        }
         *launches += 2;
       }
       unsigned long long h[2] = {0, 0};
       cudaMemcpyAsync(&h[0], v.qlen + 1, sizeof(unsigned int), cudaMemcpyDeviceToHost, st);
       cudaMemcpyAsync(&h[1], v.next_walk, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
       if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
-      if (static_cast<unsigned int>(h[0]) == 0u && h[1] >= total) break;
+      if (static_cast<unsigned int>(h[0]) <= tail_n && h[1] >= total) break;
     }
+    for (auto& x : ev) cudaEventDestroy(x);
   } else {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -476,7 +589,7 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsi
     wave_dir_kernel<<<dir_blocks, 128, smem, st>>>(a, v, par);
     body_kernels += 2;
   }
-  wave_continue_kernel<<<1, 32, 0, st>>>(v, total, cond, a.counters + 5, body_kernels + 1);
+  wave_continue_kernel<<<1, 32, 0, st>>>(v, total, tail_n, cond, a.counters + 5, body_kernels + 1);
   cudaGraph_t captured = nullptr;
   if ((e = cudaStreamEndCapture(st, &captured)) != cudaSuccess) return fail(e);
   if ((e = cudaGraphInstantiate(&exec, graph, 0)) != cudaSuccess) return fail(e);
@@ -485,6 +598,10 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsi
   cudaGraphDestroy(graph);
   }
   (void)h_qlen;
+  if (tail_n) {
+    wave_tail_kernel<<<tail_blocks, 128, smem, st>>>(a, v);
+    *launches += 1;
+  }
   if (a.recs) {
     wave_close_kernel<<<geom_blocks, 128, 0, st>>>(a, v);
     *launches += 1;

@@ -18,6 +18,9 @@
 // the exact kernel (wg_walk.cu) with fp64 geometry and mixture math; this
 // translation unit may contract FMAs (statistical parity, like the tensor
 // path).
+#include <cooperative_groups.h>
+#include <cstdlib>
+
 #include "wg_kernels.cuh"
 #include "wg_mix32.cuh"
 #include "wg_mlp_tc.cuh"
@@ -39,6 +42,11 @@ struct Dir2 {
 };
 
 enum : uint8_t { SLOT_EMPTY = 0, SLOT_NEED_DIR = 1, SLOT_NEED_MOVE = 2 };
+// walks left at the drain hand-off to wave2_tail_kernel: cfg 3 (512^2), 32
+// training rounds 417-419 ms at 131,072, 427-429 at 65,536, 486 at 16,384,
+// 600 ms without, 485 ms with every walk in the tail kernel; frozen rounds
+// unchanged (200-204 ms)
+constexpr long kTail2Default = 131072;
 
 // greens_ball / sample_greens_radius, d = 2 (wost.cpp:27-65)
 __device__ __forceinline__ double greens_ball_2d(double r, double R) {
@@ -285,6 +293,22 @@ __global__ void __launch_bounds__(128, 4) wave2_geom_kernel(WalkArgs a, Wave2 v,
   if ((threadIdx.x & 31) == 0 && started) atomicAdd(&a.counters[2], started);
 }
 
+// decode + MIS draw of one MLP output row with the tensor path's fp32
+// mixture math (wg_mix32.cuh)
+__device__ __forceinline__ Dir2 draw2(Lane2& w, const WalkArgs& a, const float* raw) {
+  Mix32 m;
+  normalize32(raw, m);
+  // decode_guiding (wost.cpp:111-122); c in fp64 from the logit so that
+  // 1 - c (the defensive uniform weight in p_mis) never rounds to 0
+  double sel = sigmoid(static_cast<double>(raw[32]));
+  if (a.sp.mode == WG_MODE_GUIDING_ONLY) sel = 1.0;
+  else if (a.sp.mode == WG_MODE_FIXED_MIS) sel = a.sp.fixed_c;
+  double dnx, dny;
+  mis_draw32(w.rng, m, sel, w.on_n, w.nx, w.ny, a.sp.reflect != 0, &dnx, &dny);
+  const MisOut o = mis_eval32(m, sel, w.on_n, w.nx, w.ny, a.sp.reflect != 0, dnx, dny);
+  return Dir2{o.nx, o.ny, o.pmis, o.pg, o.pu, sel, o.pu / o.pmis};
+}
+
 __global__ void __launch_bounds__(128) wave2_dir_kernel(WalkArgs a, Wave2 v, int parity) {
   extern __shared__ __align__(128) unsigned char smem[];
   if (blockIdx.x == 0 && threadIdx.x == 0) v.qlen[parity ^ 1] = 0u;
@@ -311,21 +335,84 @@ __global__ void __launch_bounds__(128) wave2_dir_kernel(WalkArgs a, Wave2 v, int
     }
     tc_forward(smem, phase, in, raw);
     if (live) {
-      // decode + MIS with the tensor path's fp32 mixture math (wg_mix32.cuh)
-      Mix32 m;
-      normalize32(raw, m);
-      // decode_guiding (wost.cpp:111-122); c in fp64 from the logit so that
-      // 1 - c (the defensive uniform weight in p_mis) never rounds to 0
-      double sel = sigmoid(static_cast<double>(raw[32]));
-      if (a.sp.mode == WG_MODE_GUIDING_ONLY) sel = 1.0;
-      else if (a.sp.mode == WG_MODE_FIXED_MIS) sel = a.sp.fixed_c;
-      double dnx, dny;
-      mis_draw32(w.rng, m, sel, w.on_n, w.nx, w.ny, a.sp.reflect != 0, &dnx, &dny);
-      const MisOut o = mis_eval32(m, sel, w.on_n, w.nx, w.ny, a.sp.reflect != 0, dnx, dny);
-      v.dirs[slot] = Dir2{o.nx, o.ny, o.pmis, o.pg, o.pu, sel, o.pu / o.pmis};
+      v.dirs[slot] = draw2(w, a, raw);
       v.lanes[slot].rng = w.rng;
       v.state[slot] = SLOT_NEED_MOVE;
     }
+  }
+  tc_teardown(smem);
+}
+
+// the drain hand-off (as wave_tail_kernel, wg3_walk_tc.cu): once every walk
+// id is out and at most tail_n walks remain, lockstep CTAs finish them (move,
+// begin_step, MLP on the tensor cores, draw) with the same step functions,
+// taking the next walk of the last queue as rows free up
+__global__ void __launch_bounds__(128, 2) wave2_tail_kernel(WalkArgs a, Wave2 v) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const unsigned int n = v.qlen[1];
+  const unsigned int per = min(128u, (n + gridDim.x - 1) / gridDim.x);
+  const unsigned int spread = per * gridDim.x;
+  if (static_cast<unsigned int>(blockIdx.x) * per >= n) return;
+  tc_stage_weights(smem, a.field);
+  tc_setup(smem);
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const bool collect = a.recs != nullptr;
+  int32_t slot = -1;
+  Lane2 w;
+  w.alive = false;
+  Dir2 d{};
+  int rec = -1;
+  bool need = false, more = true, first = true;
+  uint32_t phase = 0;
+  for (;;) {
+    if (need) {
+      step2_move(w, a, collect, rec, d);
+      need = w.alive && step2_begin(w, a, collect, rec);
+    }
+    while (!need && more) {
+      if (slot >= 0) {
+        if (collect) v.lanes[slot] = w;  // record-chunk bookkeeping for wave2_close_kernel
+        v.state[slot] = SLOT_EMPTY;
+        slot = -1;
+      }
+      unsigned int i;
+      if (first) {
+        i = blockIdx.x * per + threadIdx.x;
+      } else {
+        namespace cg = cooperative_groups;
+        const cg::coalesced_group g = cg::coalesced_threads();
+        unsigned int base = 0;
+        if (g.thread_rank() == 0) base = atomicAdd(v.qlen, g.size());
+        i = spread + g.shfl(base, 0) + g.thread_rank();
+      }
+      if (i >= n || (first && threadIdx.x >= per)) {
+        more = false;
+        break;
+      }
+      first = false;
+      slot = v.queue[i];
+      w = v.lanes[slot];
+      d = v.dirs[slot];
+      rec = v.rec[slot];
+      step2_move(w, a, collect, rec, d);
+      need = w.alive && step2_begin(w, a, collect, rec);
+    }
+    if (__syncthreads_count(need) == 0) break;
+    float in[16], raw[TcLayout::NO];
+    if (need) {
+      tc_gather(a.field, w.x, w.y, in);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) in[i] = 0.0f;
+    }
+    tc_forward(smem, phase, in, raw);
+    if (need) d = draw2(w, a, raw);
+  }
+  if (slot >= 0) {
+    if (collect) v.lanes[slot] = w;
+    v.state[slot] = SLOT_EMPTY;
   }
   tc_teardown(smem);
 }
@@ -345,10 +432,11 @@ void wave2_sizes(size_t* lane, size_t* dir) {
   *dir = sizeof(Dir2);
 }
 
-__global__ void wave2_continue_kernel(Wave2 v, unsigned long long total, cudaGraphConditionalHandle cond,
-                                      unsigned long long* launches, unsigned body_kernels) {
+__global__ void wave2_continue_kernel(Wave2 v, unsigned long long total, unsigned int tail_n,
+                                      cudaGraphConditionalHandle cond, unsigned long long* launches,
+                                      unsigned body_kernels) {
   if (threadIdx.x != 0) return;
-  const bool more = v.qlen[1] != 0u || *v.next_walk < total;
+  const bool more = v.qlen[1] > tail_n || *v.next_walk < total;
   cudaGraphSetConditional(cond, more ? 1u : 0u);
   atomicAdd(launches, static_cast<unsigned long long>(body_kernels));
 }
@@ -369,6 +457,12 @@ cudaError_t launch_walks2_wave(const WalkArgs& a, void* lanes, void* dirs, int32
   if (a.recs) cudaMemsetAsync(v.lanes, 0, sizeof(Lane2) * static_cast<size_t>(slots), st);
   const int geom_blocks = static_cast<int>((slots + 127) / 128);
   const int dir_blocks = sms * 2;
+  // drain hand-off to wave2_tail_kernel (WOSTGPU_WAVE2_TAIL walks left; 0 = off)
+  const char* tail_pe = std::getenv("WOSTGPU_WAVE2_TAIL");
+  const unsigned int tail_n = static_cast<unsigned int>(tail_pe ? std::atol(tail_pe) : kTail2Default);
+  if (tail_n &&
+      (e = cudaFuncSetAttribute(wave2_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess)
+    return e;
   // device-side iteration loop (as the 3D wavefront, wg3_walk_tc.cu): a CUDA
   // graph while node over a two-iteration body; wave2_continue_kernel sets
   // the condition and counts the body's kernels into counters[8]
@@ -397,7 +491,7 @@ cudaError_t launch_walks2_wave(const WalkArgs& a, void* lanes, void* dirs, int32
     wave2_geom_kernel<<<geom_blocks, 128, 0, st>>>(a, v, par);
     wave2_dir_kernel<<<dir_blocks, 128, smem, st>>>(a, v, par);
   }
-  wave2_continue_kernel<<<1, 32, 0, st>>>(v, total, cond, a.counters + 8, 5u);
+  wave2_continue_kernel<<<1, 32, 0, st>>>(v, total, tail_n, cond, a.counters + 8, 5u);
   cudaGraph_t captured = nullptr;
   if ((e = cudaStreamEndCapture(st, &captured)) != cudaSuccess) return fail(e);
   if ((e = cudaGraphInstantiate(&exec, graph, 0)) != cudaSuccess) return fail(e);
@@ -405,6 +499,10 @@ cudaError_t launch_walks2_wave(const WalkArgs& a, void* lanes, void* dirs, int32
   cudaGraphExecDestroy(exec);  // released once the launch completes
   cudaGraphDestroy(graph);
   (void)h_qlen;
+  if (tail_n) {
+    wave2_tail_kernel<<<sms * 2, 128, smem, st>>>(a, v);
+    *launches += 1;
+  }
   if (a.recs) {
     wave2_close_kernel<<<geom_blocks, 128, 0, st>>>(a, v);
     *launches += 1;

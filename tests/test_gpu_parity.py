@@ -428,6 +428,33 @@ def test_wavefront_2d_matches_lockstep_statistically(gpu, monkeypatch):
     assert abs(z.mean()) < 4.0 / np.sqrt(ok.sum())
 
 
+@pytest.mark.parametrize("collect", [False, True])
+def test_wavefront_2d_drain_handoff_keeps_every_walk(gpu, monkeypatch, collect):
+    """The drain hand-off (wave2_tail_kernel: lockstep CTAs finish the last
+    walks of a call) runs the wavefront pair's own step functions: against
+    the pair alone (hand-off off) every walk's step count and escape flag
+    are equal and its estimate agrees to 1e-9 (FMA contraction may differ
+    between the two kernels); with record collection the record counts match."""
+    p = make_preset("const-source-disk")
+    pts = cell_centers(120, 120, p.eval_bbox)
+    f = api.GuidingField(abi.field_config(), p.scene.bbox, 4)
+    prm = f.params() + np.float32(0.2) * np.random.default_rng(3).standard_normal(f.n_params).astype(np.float32)
+    f.set_params(prm)
+    monkeypatch.setenv("WOSTGPU_WALK2", "wave")
+    out = []
+    for tail in ("0", "2000", "1000000"):
+        monkeypatch.setenv("WOSTGPU_WAVE2_TAIL", tail)
+        s = api.Solver(api.Accel(p.scene), f, abi.solver_config("learnable_mis"), api.MLP_TENSOR)
+        s.set_points(pts)
+        s.solve_rounds(6, 2, 1, collect=collect)
+        out.append(s.walks() + ((len(s.records()),) if collect else (0,)))
+    e0, s0, n0, r0 = out[0]
+    for e, sc, n, r in out[1:]:
+        assert np.array_equal(sc, s0) and np.array_equal(n, n0)
+        assert np.all(np.abs(e - e0) <= 1e-9 * np.maximum(1.0, np.abs(e0)))
+        assert r == r0 and (r > 0) == collect
+
+
 _SPILL_SCRIPT = r"""
 import json, sys
 sys.path.insert(0, sys.argv[1])

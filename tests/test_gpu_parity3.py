@@ -368,12 +368,16 @@ def test_field3_checkpoint_round_trip(gpu, tmp_path):
 
 @pytest.mark.parametrize("name", ["box-strip-vlin-obstacle", "box-strip-vlin"])
 @pytest.mark.parametrize("collect", [False, True])
-def test_wavefront_walks_equal_lockstep_per_walk(gpu, monkeypatch, name, collect):
+@pytest.mark.parametrize("tail", ["0", "3000", "65536"])
+def test_wavefront_walks_equal_lockstep_per_walk(gpu, monkeypatch, name, collect, tail):
     """The wavefront pair (geometry pass + tensor-core direction pass)
     against the lockstep tensor-core kernel: the
     same PCG32 streams, the same tcgen05 MLP rows and the same exact
     geometry minima, so every walk's estimate, escape flag and step count
-    is identical; with record collection the record counts match too."""
+    is identical; with record collection the record counts match too. The
+    drain hand-off (wave_tail_kernel) is off, mid-drain (3,000 walks left)
+    and immediate (all 18k walks)."""
+    monkeypatch.setenv("WOSTGPU_WAVE3_TAIL", tail)
     sc = make_preset3(name, n=24).scene
     f = GuidingField3(abi.field_config3(), BOX, 8)
     p = f.params() + np.float32(0.3) * np.random.default_rng(9).standard_normal(f.n_params).astype(np.float32)
