@@ -378,6 +378,9 @@ __global__ void __launch_bounds__(128, WG3_DIR_MINB) wave_dir_kernel(Walk3Args a
 // per-iteration cost of the drain (sort, two launches, the direction
 // kernel's weight fetch, a geometry grid over the whole pool) while the
 // round's longest walks finish.
+#ifdef WG3_TAIL_PROF
+__device__ unsigned long long g_tail_prof[16];
+#endif
 __global__ void __launch_bounds__(128, 2) wave_tail_kernel(Walk3Args a, Wave3 v) {
   extern __shared__ __align__(128) unsigned char smem[];
   const unsigned int n = v.qlen[1];
@@ -399,7 +402,13 @@ __global__ void __launch_bounds__(128, 2) wave_tail_kernel(Walk3Args a, Wave3 v)
   int rec = -1;
   bool need = false, more = true, first = true;
   uint32_t phase = 0;
+#ifdef WG3_TAIL_PROF
+  long long pc[4][3] = {}, c_g = 0, c_f = 0, c_mma = 0;
+#endif
   for (;;) {
+#ifdef WG3_TAIL_PROF
+    const long long c0 = clock64();
+#endif
     if (need) {  // the geometry pass's work for this slot (no walk ids left to claim)
       step_move(w, a, collect, rec, d, true);
       need = w.alive && step_begin(w, a, collect, rec);
@@ -423,7 +432,11 @@ __global__ void __launch_bounds__(128, 2) wave_tail_kernel(Walk3Args a, Wave3 v)
       step_move(w, a, collect, rec, d, true);
       need = w.alive && step_begin(w, a, collect, rec);
     }
-    if (__syncthreads_count(need) == 0) break;
+    const int live_rows = __syncthreads_count(need);
+    if (live_rows == 0) break;
+#ifdef WG3_TAIL_PROF
+    const long long c1 = clock64();
+#endif
     float in[IN], raw[OD];  // the direction pass's
     if (need) {
       gather3_tc(a.f, w.x, in);
@@ -431,9 +444,42 @@ __global__ void __launch_bounds__(128, 2) wave_tail_kernel(Walk3Args a, Wave3 v)
 #pragma unroll
       for (int i = 0; i < IN; ++i) in[i] = 0.0f;
     }
+#ifdef WG3_TAIL_PROF
+    __syncthreads();
+    const long long c2 = clock64();
+#endif
+#ifdef WG3_TAIL_PROF
+    long long bp[2] = {0, 0};
+    wg::tc_forward<OD>(smem, phase, in, raw, bp);
+    __syncthreads();
+    const long long c3 = clock64();
+#else
     wg::tc_forward<OD>(smem, phase, in, raw);
+#endif
     if (need) d = sample_guided_f(w, a, raw);
+#ifdef WG3_TAIL_PROF
+    __syncthreads();
+    {
+      const int bk = live_rows > 64 ? 0 : live_rows > 16 ? 1 : live_rows > 4 ? 2 : 3;
+      pc[bk][0] += c1 - c0;
+      pc[bk][1] += clock64() - c1;
+      pc[bk][2] += 1;
+      c_g += c2 - c1;
+      c_f += c3 - c2;
+      c_mma += bp[0];
+    }
+#endif
   }
+#ifdef WG3_TAIL_PROF
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < 3; ++j) atomicAdd(&g_tail_prof[3 * i + j], static_cast<unsigned long long>(pc[i][j]));
+    atomicAdd(&g_tail_prof[12], 1ull);
+    atomicAdd(&g_tail_prof[13], static_cast<unsigned long long>(c_g));
+    atomicAdd(&g_tail_prof[14], static_cast<unsigned long long>(c_f));
+    atomicAdd(&g_tail_prof[15], static_cast<unsigned long long>(c_mma));
+  }
+#endif
   if (slot >= 0) {
     if (collect) v.lanes[slot] = w;
     v.state[slot] = SLOT_EMPTY;
@@ -599,7 +645,41 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsi
   }
   (void)h_qlen;
   if (tail_n) {
-    wave_tail_kernel<<<tail_blocks, 128, smem, st>>>(a, v);
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (host_loop == 2) {
+      unsigned int q = 0;
+      cudaMemcpyAsync(&q, v.qlen + 1, sizeof(unsigned int), cudaMemcpyDeviceToHost, st);
+      cudaEventCreate(&t0);
+      cudaEventCreate(&t1);
+      cudaEventRecord(t0, st);
+      wave_tail_kernel<<<tail_blocks, 128, smem, st>>>(a, v);
+      cudaEventRecord(t1, st);
+      cudaEventSynchronize(t1);
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, t0, t1);
+      std::fprintf(stderr, "wave3 tail live %u us %.1f\n", q, ms * 1e3f);
+#ifdef WG3_TAIL_PROF
+      unsigned long long pr[16];
+      cudaMemcpyFromSymbol(pr, g_tail_prof, sizeof(pr));
+      const double ctas = pr[12] ? double(pr[12]) : 1.0;
+      double its = 0;
+      for (int i = 0; i < 4; ++i) {
+        const double n = pr[3 * i + 2] ? double(pr[3 * i + 2]) : 1.0;
+        its += pr[3 * i + 2];
+        std::fprintf(stderr, "wave3 tail prof rows %s: %.1f its/CTA, geo %.0f mlp %.0f cycles/it\n",
+                     i == 0 ? ">64" : i == 1 ? "17-64" : i == 2 ? "5-16" : "<=4", pr[3 * i + 2] / ctas,
+                     pr[3 * i] / n, pr[3 * i + 1] / n);
+      }
+      std::fprintf(stderr, "wave3 tail prof all: gather %.0f forward %.0f mma %.0f cycles/it\n", pr[13] / its,
+                   pr[14] / its, pr[15] / its);
+      const unsigned long long z[16] = {};
+      cudaMemcpyToSymbol(g_tail_prof, z, sizeof(z));
+#endif
+      cudaEventDestroy(t0);
+      cudaEventDestroy(t1);
+    } else {
+      wave_tail_kernel<<<tail_blocks, 128, smem, st>>>(a, v);
+    }
     *launches += 1;
   }
   if (a.recs) {
