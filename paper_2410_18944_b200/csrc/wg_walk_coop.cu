@@ -18,6 +18,8 @@
 // not serialise behind a static slot. The mixture numerics are those of the
 // tensor-core path (wg_mix32.cuh); the MLP is fp32 FMA with a
 // different summation order than the reference (~1e-6 relative).
+#include <cstdio>
+
 #include "wg_kernels.cuh"
 #include "wg_mix32.cuh"
 #include "wg_train.cuh"
@@ -435,6 +437,18 @@ __device__ __forceinline__ void c_mixture_sample(Pcg& rng, const Lobe& L, int la
 // finish the walks the lockstep kernel handed off (WalkArgs::spill), one
 // warp per walk (a standalone warp-per-walk kernel that also started fresh
 // walks measured slower than the lockstep tiles on cfg 2)
+#ifdef WG_COOP_PROF
+__device__ unsigned long long g_coop_prof[7];
+void coop_prof_dump() {
+  unsigned long long p[7];
+  cudaMemcpyFromSymbol(p, g_coop_prof, sizeof(p));
+  const double n = p[6] ? double(p[6]) : 1.0;
+  std::fprintf(stderr, "coop prof steps %llu cycles/step: begin %.0f gather %.0f mlp %.0f decode %.0f sample+pdf %.0f record+ray %.0f\n",
+               p[6], p[0] / n, p[1] / n, p[2] / n, p[3] / n, p[4] / n, p[5] / n);
+  const unsigned long long z[7] = {};
+  cudaMemcpyToSymbol(g_coop_prof, z, sizeof(z));
+}
+#endif
 __device__ __forceinline__ void walk_coop_body(const WalkArgs& a, unsigned char* smem) {
   CoopW& W = *reinterpret_cast<CoopW*>(smem);
   float* hbuf = reinterpret_cast<float*>(smem + al16c(sizeof(CoopW))) + 64 * (threadIdx.x >> 5);
@@ -500,6 +514,9 @@ __device__ __forceinline__ void walk_coop_body(const WalkArgs& a, unsigned char*
   w.rec_base = 0;
   w.rec_left = 0;
   unsigned long long walks_done = 0;
+#ifdef WG_COOP_PROF
+  long long cprof[7] = {};
+#endif
 
   for (;;) {
     unsigned long long idx = 0;
@@ -532,14 +549,36 @@ __device__ __forceinline__ void walk_coop_body(const WalkArgs& a, unsigned char*
     }
 
     // a handed-off walk enters at its direction step (begin_step done)
+#ifdef WG_COOP_PROF
+    long long q0 = clock64(), q1, q2, q3, q4, q5, q6;
+    for (bool go = true; go; go = (q0 = clock64(), c_begin(w, a, s, ss, collect, lane))) {
+      q1 = clock64();
+      cprof[0] += q1 - q0;
+#else
     for (bool go = true; go; go = c_begin(w, a, s, ss, collect, lane)) {
+#endif
       // field evaluation and Table-1 decode
       float xin[16];
       c_gather(f, w.x, w.y, xin);
+#ifdef WG_COOP_PROF
+      __syncwarp();
+      q2 = clock64();
+      cprof[1] += q2 - q1;
+#endif
       float y32;
       const float y = c_mlp(W, hbuf, xin, lane, &y32);
+#ifdef WG_COOP_PROF
+      __syncwarp();
+      q3 = clock64();
+      cprof[2] += q3 - q2;
+#endif
       double cdec;
       const Lobe L = c_decode(y, y32, lane, &cdec);
+#ifdef WG_COOP_PROF
+      __syncwarp();
+      q4 = clock64();
+      cprof[3] += q4 - q3;
+#endif
       double sel = cdec;
       if (a.sp.mode == WG_MODE_GUIDING_ONLY) sel = 1.0;
       else if (a.sp.mode == WG_MODE_FIXED_MIS) sel = a.sp.fixed_c;
@@ -579,6 +618,11 @@ __device__ __forceinline__ void walk_coop_body(const WalkArgs& a, unsigned char*
       const double pu = uniform_pdf(w.on_n, dnx, dny, w.nx, w.ny);
       const double pmis = sel * pg + (1.0 - sel) * pu;
       const double mult = pu / pmis;
+#ifdef WG_COOP_PROF
+      __syncwarp();
+      q5 = clock64();
+      cprof[4] += q5 - q4;
+#endif
       if (w.rec >= 0 && lane == 0) {
         DevRecord r;
         r.x = static_cast<float>(w.x);
@@ -628,12 +672,22 @@ __device__ __forceinline__ void walk_coop_body(const WalkArgs& a, unsigned char*
       }
       w.T *= mult;
       ++w.depth;
+#ifdef WG_COOP_PROF
+      __syncwarp();
+      q6 = clock64();
+      cprof[5] += q6 - q5;
+      cprof[6] += 1;
+#endif
       if (!bbox_contains(s, w.x, w.y, pad)) {
         c_finish(w, a, true, lane);
         break;
       }
     }
   }
+#ifdef WG_COOP_PROF
+  if (lane == 0)
+    for (int i = 0; i < 7; ++i) atomicAdd(&g_coop_prof[i], static_cast<unsigned long long>(cprof[i]));
+#endif
   if (collect && lane == 0)
     for (int i = 0; i < w.rec_left; ++i) a.recs[w.rec_base + (8 - w.rec_left) + i].flags = 0u;
   if (lane == 0 && walks_done) atomicAdd(&a.counters[2], walks_done);
@@ -661,6 +715,13 @@ cudaError_t launch_walks_coop_resume(const WalkArgs& a, int max_walks, int sms, 
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk_kernel_coop_resume, kCoopThreads, smem);
   const int blocks = std::max(1, std::min((max_walks + kCoopWarps - 1) / kCoopWarps, sms * std::max(1, per_sm)));
   walk_kernel_coop_resume<<<blocks, kCoopThreads, smem, st>>>(a);
+#ifdef WG_COOP_PROF
+  static int calls = 0;
+  if (++calls % 256 == 0) {
+    cudaStreamSynchronize(st);
+    coop_prof_dump();
+  }
+#endif
   return cudaGetLastError();
 }
 

@@ -62,6 +62,9 @@ def three_d(name, grid, wpp):
         s = Solver3(acc, f, abi.solver_config(mode), MLP_TENSOR)
         s.set_points(pts)
         tc = abi.train_config(seed=1) if f else None
+        s.run(1, 2, 2 if f else 0, tc)  # warm-up: module load, slot pool, record arena
+        if f:
+            f.set_state(*GuidingField3(abi.field_config3(), (0, 0, 0, 1, 1, 1), 1).state())
         _, ms = s.run(1, wpp, 256 if f else 0, tc)
         pr = s.run_profile()
         out[mode] = {"walks_per_s": len(pts) * wpp / (ms * 1e-3), "steps_per_s": pr["steps"] / (ms * 1e-3),
