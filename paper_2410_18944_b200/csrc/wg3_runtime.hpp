@@ -35,7 +35,7 @@ struct wg_solver3_s {
   int64_t rec_cap_min = 0;  // grown after an arena overflow
   bool have_records = false;
   // wavefront walk pool (WG_MLP_TENSOR guided walks, wg3_walk_tc.cu)
-  wgrt::DBuf w_lanes, w_dirs, w_rec, w_state, w_queue, w_qlen, w_next, w_blob, w_perm, w_bins, g_blob;
+  wgrt::DBuf w_lanes, w_dirs, w_rec, w_state, w_queue, w_qlen, w_next, w_blob, w_perm, w_bins, w_sbin, g_blob;
   int64_t w_slots = 0;
   unsigned int* h_qlen = nullptr;  // pinned
   // training

@@ -545,6 +545,7 @@ void enqueue3_rounds(wg_solver3_s* s, uint64_t seed, uint64_t wpp_first, int32_t
         s->w_state.alloc(slots);
         s->w_queue.alloc(sizeof(int32_t) * slots);
         s->w_perm.alloc(sizeof(int32_t) * slots);
+        s->w_sbin.alloc(sizeof(uint16_t) * slots);
         s->w_slots = slots;
       }
       s->w_qlen.alloc(2 * sizeof(unsigned int));
@@ -558,6 +559,7 @@ void enqueue3_rounds(wg_solver3_s* s, uint64_t seed, uint64_t wpp_first, int32_t
       s->w_bins.alloc(sizeof(unsigned int) * (kSortBins + 3));
       v.perm = s->w_perm.as<int32_t>();
       v.bins = s->w_bins.as<unsigned int>();
+      v.sbin = s->w_sbin.as<uint16_t>();
       int64_t launched = 0;
       CK(launch_walks3_wave(a, v, sms, s->h_qlen, &launched, s->st));
       g_launches += launched;

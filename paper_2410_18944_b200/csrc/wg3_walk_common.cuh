@@ -349,6 +349,7 @@ struct Wave3 {
   unsigned char* wblob;  // [wg::wpack::FWD_BYTES] split-fp16 MLP weights, packed per call
   int32_t* perm;         // [slots] geometry-pass order: slots grouped by spatial cell
   unsigned int* bins;    // [kSortBins + 3] cell histogram / offsets, [+1] entries in perm, [+2] skip
+  uint16_t* sbin;        // [slots] sort cell of the slot's pending move (>= kSortBins: none), set by the geometry pass
 };
 #ifndef WG3_SORT_BITS
 #define WG3_SORT_BITS 4

@@ -175,6 +175,27 @@ constexpr long kTailDefault = 65536;
 #define WG3_DIR_MINB 1
 #endif
 
+// Morton cell (kSortBits per axis) of a position: the sort key of the
+// geometry pass's order
+__device__ __forceinline__ uint32_t spread3(uint32_t v) {  // <= 10 bits -> every third bit
+  v &= 0x3FFu;
+  v = (v | (v << 16)) & 0x030000FFu;
+  v = (v | (v << 8)) & 0x0300F00Fu;
+  v = (v | (v << 4)) & 0x030C30C3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+__device__ __forceinline__ int sort_cell(const Walk3Args& a, const D3& x) {
+  const double* b = a.s.bbox;
+  const double q = static_cast<double>(1 << kSortBits);
+  auto cell = [&](double c, double lo, double hi) {
+    const int i = static_cast<int>((c - lo) / (hi - lo) * q);
+    return static_cast<uint32_t>(i < 0 ? 0 : i > (1 << kSortBits) - 1 ? (1 << kSortBits) - 1 : i);
+  };
+  return static_cast<int>(spread3(cell(x.x, b[0], b[3])) | (spread3(cell(x.y, b[1], b[4])) << 1) |
+                          (spread3(cell(x.z, b[2], b[5])) << 2));
+}
+
 __global__ void __launch_bounds__(128, WG3_GEOM_MINB) wave_geom_kernel(Walk3Args a, Wave3 v, int parity) {
   const bool collect = a.recs != nullptr;
   const unsigned long long total = static_cast<unsigned long long>(a.n_points) * a.n_rounds;
@@ -219,9 +240,11 @@ __global__ void __launch_bounds__(128, WG3_GEOM_MINB) wave_geom_kernel(Walk3Args
       v.rec[slot] = rec;
       v.state[slot] = SLOT_NEED_DIR;
       v.queue[claim_queue(qlen)] = static_cast<int32_t>(slot);
+      v.sbin[slot] = static_cast<uint16_t>(sort_cell(a, w.x));  // where its next move starts
     } else {
       if (collect) v.lanes[slot] = w;  // record-chunk bookkeeping
       v.state[slot] = SLOT_EMPTY;
+      v.sbin[slot] = static_cast<uint16_t>(kSortBins);
     }
   }
   for (int o = 16; o > 0; o >>= 1) started += __shfl_down_sync(0xffffffffu, started, o);
@@ -232,25 +255,9 @@ __global__ void __launch_bounds__(128, WG3_GEOM_MINB) wave_geom_kernel(Walk3Args
 // by the Morton cell (kSortBits per axis) of their walk's position; slots
 // without a pending move go last. The order only changes which lanes run
 // side by side: every slot is visited exactly once either way.
-__device__ __forceinline__ uint32_t spread3(uint32_t v) {  // <= 10 bits -> every third bit
-  v &= 0x3FFu;
-  v = (v | (v << 16)) & 0x030000FFu;
-  v = (v | (v << 8)) & 0x0300F00Fu;
-  v = (v | (v << 4)) & 0x030C30C3u;
-  v = (v | (v << 2)) & 0x09249249u;
-  return v;
-}
-__device__ __forceinline__ int slot_bin(const Walk3Args& a, const Wave3& v, int64_t slot) {
-  if (v.state[slot] != SLOT_NEED_MOVE) return kSortBins;
-  const D3 x = v.lanes[slot].x;
-  const double* b = a.s.bbox;
-  const double q = static_cast<double>(1 << kSortBits);
-  auto cell = [&](double c, double lo, double hi) {
-    const int i = static_cast<int>((c - lo) / (hi - lo) * q);
-    return static_cast<uint32_t>(i < 0 ? 0 : i > (1 << kSortBits) - 1 ? (1 << kSortBits) - 1 : i);
-  };
-  return static_cast<int>(spread3(cell(x.x, b[0], b[3])) | (spread3(cell(x.y, b[1], b[4])) << 1) |
-                          (spread3(cell(x.z, b[2], b[5])) << 2));
+__device__ __forceinline__ int slot_bin(const Wave3& v, int64_t slot) {
+  const int b = v.sbin[slot];
+  return b < kSortBins ? b : kSortBins;
 }
 __device__ __forceinline__ bool walks_exhausted(const Walk3Args& a, const Wave3& v) {
   return *reinterpret_cast<volatile unsigned long long*>(v.next_walk) >=
@@ -268,14 +275,14 @@ __global__ void __launch_bounds__(256) sort_count_kernel(Walk3Args a, Wave3 v) {
     __syncthreads();
     for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < v.slots;
          s += static_cast<int64_t>(gridDim.x) * blockDim.x)
-      atomicAdd(&h[slot_bin(a, v, s)], 1u);
+      atomicAdd(&h[slot_bin(v, s)], 1u);
     __syncthreads();
     for (int i = threadIdx.x; i <= kSortBins; i += blockDim.x)
       if (h[i]) atomicAdd(&v.bins[i], h[i]);
   } else {
     for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < v.slots;
          s += static_cast<int64_t>(gridDim.x) * blockDim.x)
-      atomicAdd(&v.bins[slot_bin(a, v, s)], 1u);
+      atomicAdd(&v.bins[slot_bin(v, s)], 1u);
   }
 }
 __global__ void __launch_bounds__(1024) sort_scan_kernel(Walk3Args a, Wave3 v) {  // exclusive scan, one CTA
@@ -306,15 +313,38 @@ __global__ void __launch_bounds__(1024) sort_scan_kernel(Walk3Args a, Wave3 v) {
     run += loc[j];
   }
 }
+// block-local ranking: each CTA ranks its chunk of slots per cell in shared
+// memory, reserves one range per non-empty cell with a single global atomic,
+// then writes perm (instead of one contended global atomic per slot)
+constexpr int kScatterPer = 16;  // slots per thread
 __global__ void __launch_bounds__(256) sort_scatter_kernel(Walk3Args a, Wave3 v) {
   if (v.bins[kSortBins + 2]) return;
+  __shared__ unsigned int h[kSortBins + 1];
   const bool drop_idle = walks_exhausted(a, v);
-  for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < v.slots;
-       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int b = slot_bin(a, v, s);
-    if (b == kSortBins && drop_idle) continue;
-    v.perm[atomicAdd(&v.bins[b], 1u)] = static_cast<int32_t>(s);
+  for (int i = threadIdx.x; i <= kSortBins; i += blockDim.x) h[i] = 0u;
+  __syncthreads();
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * kScatterPer + threadIdx.x;
+  unsigned int rank[kScatterPer];
+  uint16_t bin[kScatterPer];
+#pragma unroll
+  for (int k = 0; k < kScatterPer; ++k) {
+    const int64_t s = base + static_cast<int64_t>(k) * blockDim.x;
+    int b = kSortBins + 1;  // none
+    if (s < v.slots) {
+      b = slot_bin(v, s);
+      if (b == kSortBins && drop_idle) b = kSortBins + 1;
+    }
+    bin[k] = static_cast<uint16_t>(b);
+    if (b <= kSortBins) rank[k] = atomicAdd(&h[b], 1u);
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= kSortBins; i += blockDim.x)
+    if (h[i]) h[i] = atomicAdd(&v.bins[i], h[i]);
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kScatterPer; ++k)
+    if (bin[k] <= kSortBins)
+      v.perm[h[bin[k]] + rank[k]] = static_cast<int32_t>(base + static_cast<int64_t>(k) * blockDim.x);
 }
 __global__ void perm_identity_kernel(Wave3 v) {
   for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < v.slots;
@@ -529,6 +559,8 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsi
   // 4 bits per axis: 5 bits measured no faster (3.27 s; training 0.99 s)
   const int sort_period = a.recs ? 2 : 1;  // (with wide BVHs: frozen rounds equal at 1 and 2)
   const int geom_blocks = static_cast<int>((v.slots + 127) / 128);
+  const int scatter_blocks = static_cast<int>((v.slots + 256 * kScatterPer - 1) / (256 * kScatterPer));
+  cudaMemsetAsync(v.sbin, 0xFF, sizeof(uint16_t) * static_cast<size_t>(v.slots), st);  // no pending moves
   // persistent direction CTAs, 2 per SM (197 registers; cfg 4 frozen rounds
   // 2.84 s vs 2.91 s at 3 per SM and 3.07 s at 1)
 #ifndef WG3_DIR_PER_SM
@@ -575,7 +607,7 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsi
           cudaMemsetAsync(v.bins, 0, sizeof(unsigned int) * (kSortBins + 1), st);
           sort_count_kernel<<<sms * 2, 256, 0, st>>>(a, v);
           sort_scan_kernel<<<1, 1024, 0, st>>>(a, v);
-          sort_scatter_kernel<<<sms * 2, 256, 0, st>>>(a, v);
+          sort_scatter_kernel<<<scatter_blocks, 256, 0, st>>>(a, v);
           *launches += 3;
         }
         if (host_loop == 2) cudaEventRecord(ev[1], st);
@@ -628,7 +660,7 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsi
       cudaMemsetAsync(v.bins, 0, sizeof(unsigned int) * (kSortBins + 1), st);
       sort_count_kernel<<<sms * 2, 256, 0, st>>>(a, v);
       sort_scan_kernel<<<1, 1024, 0, st>>>(a, v);
-      sort_scatter_kernel<<<sms * 2, 256, 0, st>>>(a, v);
+      sort_scatter_kernel<<<scatter_blocks, 256, 0, st>>>(a, v);
       body_kernels += 3;
     }
     wave_geom_kernel<<<geom_blocks, 128, 0, st>>>(a, v, par);
