@@ -3,13 +3,23 @@
 // (include/wostgpu3.h). Contract: oracle/wost3d.inc (the 3D analogue of
 // proj/src/geom2d.cpp:80-255).
 //
-// BVH: binary, median split of the primitive centroids along the longest
-// axis of their bounds (ties by primitive index), leaves of <= 4, depth-first
-// preorder so a node's first child follows it. Built once per scene on the
-// host (not hot); node boxes are fp32 rounded outward from the fp64 bounds.
+// BVH: binary, binned surface-area-heuristic splits of the primitive
+// centroids (16 bins per axis, the longest-axis median when no bin boundary
+// beats it; ties by primitive index), leaves of <= 2, depth-first preorder so
+// a node's first child follows it, then collapsed 4-wide. Built once per
+// scene on the host (not hot); node boxes are fp32 rounded outward from the
+// fp64 bounds. Every query is an order-independent minimum,
+// so the tree shape changes speed only. cfg 4 shape (512^2, 256 frozen / 32
+// training rounds): median splits with leaves of 4 1547-1549 / 401 ms, SAH
+// leaves of 4 1501-1556 / 395-432, SAH leaves of 2 1464-1526 / 377-381, SAH
+// leaves of 1 / 32 bins / 64 bins no better. WOSTGPU_BVH3 = median | sahN[B]
+// (N = leaf size, B = bins) selects another rule for A/B runs.
+#include <algorithm>
 #include <array>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
+#include <string>
 #include <functional>
 #include <map>
 #include <utility>
@@ -52,7 +62,74 @@ struct Builder {
   std::vector<double> cen;  // 3 per primitive
   std::vector<int> order;
   std::vector<Node3> nodes;
-  Builder(const std::vector<HBox>& b, double pad_) : box(b), pad(pad_), cen(3 * b.size()), order(b.size()) {
+  bool sah;  // binned surface-area split instead of the median
+  int leaf_max = 4;
+  int sah_bins = 16;
+  // binned SAH over the centroid bounds (16 bins per axis): the split minimising
+  // area(left) x count(left) + area(right) x count(right), as a rank `mid` in
+  // the (centroid, index) order along `ax`; the median when no split beats it
+  void sah_split(int lo, int hi, const HBox& cb, int& ax, int& mid) {
+    const int kB = sah_bins;
+    auto area = [](const HBox& b) {
+      if (b.lo[0] > b.hi[0]) return 0.0;
+      const double e0 = b.hi[0] - b.lo[0], e1 = b.hi[1] - b.lo[1], e2 = b.hi[2] - b.lo[2];
+      return e0 * e1 + e1 * e2 + e2 * e0;
+    };
+    double best = INFINITY;
+    int best_ax = ax, best_cnt = (hi - lo) / 2;
+    {  // the median's cost along the longest axis: the baseline to beat
+      std::vector<int> tmp(order.begin() + lo, order.begin() + hi);
+      const int m = (hi - lo) / 2;
+      std::nth_element(tmp.begin(), tmp.begin() + m, tmp.end(), [&](int p, int q) {
+        double kp = cen[3 * p + ax], kq = cen[3 * q + ax];
+        return kp < kq || (kp == kq && p < q);
+      });
+      HBox l, r;
+      for (int i = 0; i < m; ++i) l.grow(box[tmp[i]]);
+      for (int i = m; i < hi - lo; ++i) r.grow(box[tmp[i]]);
+      best = area(l) * m + area(r) * (hi - lo - m);
+    }
+    for (int a = 0; a < 3; ++a) {
+      const double e = cb.hi[a] - cb.lo[a];
+      if (!(e > 0.0)) continue;
+      std::vector<HBox> bb(kB);
+      std::vector<int> cnt(kB, 0);
+      for (int i = lo; i < hi; ++i) {
+        const int p = order[i];
+        int k = static_cast<int>((cen[3 * p + a] - cb.lo[a]) / e * kB);
+        k = k < 0 ? 0 : k >= kB ? kB - 1 : k;
+        ++cnt[k];
+        bb[k].grow(box[p]);
+      }
+      std::vector<double> rarea(kB);
+      std::vector<int> rcnt(kB);
+      HBox acc;
+      int c = 0;
+      for (int k = kB - 1; k >= 1; --k) {
+        acc.grow(bb[k]);
+        c += cnt[k];
+        rarea[k] = area(acc);
+        rcnt[k] = c;
+      }
+      HBox lacc;
+      int lc = 0;
+      for (int k = 0; k < kB - 1; ++k) {
+        lacc.grow(bb[k]);
+        lc += cnt[k];
+        if (lc == 0 || rcnt[k + 1] == 0) continue;
+        const double cost = area(lacc) * lc + rarea[k + 1] * rcnt[k + 1];
+        if (cost < best) {
+          best = cost;
+          best_ax = a;
+          best_cnt = lc;
+        }
+      }
+    }
+    ax = best_ax;
+    mid = lo + best_cnt;
+  }
+  Builder(const std::vector<HBox>& b, double pad_, bool sah_ = false, int leaf_max_ = 4, int bins_ = 16)
+      : box(b), pad(pad_), cen(3 * b.size()), order(b.size()), sah(sah_), leaf_max(leaf_max_), sah_bins(bins_) {
     for (size_t i = 0; i < b.size(); ++i) {
       order[i] = static_cast<int>(i);
       for (int a = 0; a < 3; ++a) cen[3 * i + a] = 0.5 * (b[i].lo[a] + b[i].hi[a]);
@@ -72,15 +149,16 @@ struct Builder {
       n.lo[a] = round_down(bb.lo[a] - pad);
       n.hi[a] = round_up(bb.hi[a] + pad);
     }
-    if (hi - lo <= 4) {
+    if (hi - lo <= leaf_max) {
       n.a = lo;
       n.b = -(hi - lo);
       nodes[id] = n;
       return id;
     }
     double ext[3] = {cb.hi[0] - cb.lo[0], cb.hi[1] - cb.lo[1], cb.hi[2] - cb.lo[2]};
-    const int ax = ext[0] >= ext[1] && ext[0] >= ext[2] ? 0 : (ext[1] >= ext[2] ? 1 : 2);
-    const int mid = (lo + hi) / 2;
+    int ax = ext[0] >= ext[1] && ext[0] >= ext[2] ? 0 : (ext[1] >= ext[2] ? 1 : 2);
+    int mid = (lo + hi) / 2;
+    if (sah) sah_split(lo, hi, cb, ax, mid);
     std::nth_element(order.begin() + lo, order.begin() + mid, order.begin() + hi, [&](int p, int q) {
       double kp = cen[3 * p + ax], kq = cen[3 * q + ax];
       return kp < kq || (kp == kq && p < q);
@@ -392,8 +470,13 @@ int wostgpu_scene3_create(const double* tri, const int32_t* kind, const int32_t*
     s->n_tri = n_tri;
     Scene3View& v = s->view;
     v = Scene3View{};
+    const char* bvh_env = std::getenv("WOSTGPU_BVH3");  // median | sahN[B] (A/B of the split rule)
+    const std::string rule = bvh_env ? bvh_env : "sah2";
+    const bool sah = rule.rfind("sah", 0) == 0;
+    const int leaf_max = sah && rule.size() >= 4 ? std::max(1, std::min(7, rule[3] - '0')) : (sah ? 2 : 4);
+    const int sah_bins = sah && rule.size() > 4 ? std::max(2, std::atoi(rule.c_str() + 4)) : 16;
     for (int k = 0; k < 2; ++k) {
-      Builder b(boxes[k], box_pad);
+      Builder b(boxes[k], box_pad, sah, leaf_max, sah_bins);
       std::vector<Tri3> leaf(b.order.size());
       for (size_t i = 0; i < b.order.size(); ++i) leaf[i] = tris[ids[k][b.order[i]]];
       s->n_node[k] = static_cast<int64_t>(b.nodes.size());
@@ -433,7 +516,7 @@ int wostgpu_scene3_create(const double* tri, const int32_t* kind, const int32_t*
         eb[i].grow(edges[i].a);
         eb[i].grow(edges[i].b);
       }
-      Builder b(eb, box_pad);
+      Builder b(eb, box_pad, sah, leaf_max, sah_bins);
       std::vector<Edge3> leaf(edges.size());
       for (size_t i = 0; i < edges.size(); ++i) leaf[i] = edges[b.order[i]];
       s->n_node[2] = static_cast<int64_t>(b.nodes.size());

