@@ -223,6 +223,19 @@ __device__ __forceinline__ bool ray_box(D3 o, D3 inv, const bool* dz, const floa
   return true;
 }
 
+// traversal stack capacities: a 4-wide descent pushes at most 3 entries per
+// interior node on its path, a binary one at most 1 net; the scene build
+// checks its trees' depths against these (wg3_scene.cu: an SAH tree that is
+// too deep is rebuilt with median splits, and a median tree that is too deep
+// fails the scene). The 4-wide stacks live in local memory: 40 entries
+// (median 4-wide trees to depth 13, > 10^8 triangles) keep the geometry
+// pass's per-thread footprint small (cfg 4 shape, 32 vs 64 entries: frozen
+// rounds -1%, uniform -2%)
+#ifndef WG3_STACK4
+#define WG3_STACK4 40
+#endif
+constexpr int kStack4 = WG3_STACK4, kStack2 = 64;
+
 struct CP3 {
   D3 p;
   double d2;
@@ -235,7 +248,7 @@ __device__ __forceinline__ void cp_bvh(const Node3* nodes, const Tri3* tris, D3 
   if (!nodes) return;
   const PtBox pb = pt_box(x);
   float bf = __double2float_ru(best.d2);
-  int stack[64];
+  int stack[kStack2];
   int sp = 0;
   stack[sp++] = 0;
   while (sp) {
@@ -341,8 +354,8 @@ __device__ __forceinline__ void cp_bvh4(const Node4* nodes, const Tri3* tris, co
                                         CP3& best) {
   const PtBox pb = pt_box(x);
   float bf = __double2float_ru(best.d2);
-  int st_code[64];
-  float st_key[64];
+  int st_code[kStack4];
+  float st_key[kStack4];
   int sp = 0;
   int node = 0;
   for (;;) {
@@ -434,8 +447,8 @@ __device__ __forceinline__ double sil_bvh4(const Scene3View& s, D3 x, double bou
   double best = bound2;
   const PtBox pb = pt_box(x);
   float bf = __double2float_ru(best);
-  int st_code[64];
-  float st_key[64];
+  int st_code[kStack4];
+  float st_key[kStack4];
   int sp = 0;
   int node = 0;
   for (;;) {
@@ -502,7 +515,7 @@ __device__ __forceinline__ double closest_silhouette_d2(const Scene3View& s, D3 
   double best = bound2;
   const PtBox pb = pt_box(x);
   float bf = __double2float_ru(best);
-  int stack[64];
+  int stack[kStack2];
   int sp = 0;
   stack[sp++] = 0;
   while (sp) {
@@ -586,7 +599,7 @@ __device__ __forceinline__ void ray_bvh(const Node3* nodes, const Tri3* tris, in
                                   dz[2] ? 0.0f : static_cast<float>(1.0 / d.z));
   // t bound rounded up, padded like the boxes
   float tb_f = __double2float_ru(fmin(t_max, h.t)) * (1.0f + 0x1.0p-20f);
-  int stack[64];
+  int stack[kStack2];
   int sp = 0;
   stack[sp++] = 0;
   while (sp) {
@@ -628,8 +641,8 @@ __device__ __forceinline__ void ray_bvh4(const Node4* nodes, const Tri3* tris, i
                                   dz[1] ? 0.0f : static_cast<float>(1.0 / d.y),
                                   dz[2] ? 0.0f : static_cast<float>(1.0 / d.z));
   float tb_f = __double2float_ru(fmin(t_max, h.t)) * (1.0f + 0x1.0p-20f);
-  int st_code[64];
-  float st_key[64];
+  int st_code[kStack4];
+  float st_key[kStack4];
   int sp = 0;
   int node = 0;
   for (;;) {

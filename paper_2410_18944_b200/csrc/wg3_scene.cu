@@ -18,6 +18,7 @@
 #include <array>
 #include <cfloat>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <functional>
@@ -174,6 +175,49 @@ struct Builder {
 // are its binary children with the internal one of largest surface area
 // replaced by its own two children until there are four; boxes are the
 // binary nodes' (outward-rounded) boxes
+// interior nodes on the longest root-to-leaf path (binary / 4-wide): the
+// traversal stacks need depth + 1 (binary) and 3 x depth (4-wide) entries
+int depth2(const std::vector<Node3>& n, int i = 0) {
+  if (n.empty() || n[i].b < 0) return 0;
+  return 1 + std::max(depth2(n, n[i].a), depth2(n, n[i].b));
+}
+int depth4(const std::vector<Node4>& n, int i = 0) {
+  if (n.empty()) return 0;
+  int d = 0;
+  for (int j = 0; j < kBvhW; ++j)
+    if (n[i].lox[j] <= n[i].hix[j] && n[i].child[j] >= 0) d = std::max(d, depth4(n, n[i].child[j]));
+  return 1 + d;
+}
+std::vector<Node4> collapse4(const std::vector<Node3>& n3);
+
+bool depths_fit(const std::vector<Node3>& n3, const std::vector<Node4>& n4, const char* what) {
+  const int d2 = depth2(n3), d4 = depth4(n4);
+  if (std::getenv("WOSTGPU_BVH3_STATS"))
+    std::fprintf(stderr, "bvh3 %s: %zu binary nodes depth %d, %zu 4-wide nodes depth %d\n", what, n3.size(), d2,
+                 n4.size(), d4);
+  return d2 + 1 <= kStack2 && 3 * d4 <= kStack4;
+}
+
+// the BVH of one primitive set: the configured split rule, median splits if
+// that tree is too deep for the device stacks, an error if that one is too
+struct Tree {
+  std::vector<int> order;
+  std::vector<Node3> n3;
+  std::vector<Node4> n4;
+};
+Tree build_tree(const std::vector<HBox>& boxes, double pad, bool sah, int leaf_max, int bins, const char* what) {
+  Tree t;
+  {
+    Builder b(boxes, pad, sah, leaf_max, bins);
+    t.order = std::move(b.order);
+    t.n3 = std::move(b.nodes);
+  }
+  t.n4 = collapse4(t.n3);
+  if (depths_fit(t.n3, t.n4, what)) return t;
+  need(sah, WG_ERR_INVALID, std::string("scene BVH too deep for the device traversal stacks: ") + what);
+  return build_tree(boxes, pad, false, 4, bins, what);
+}
+
 std::vector<Node4> collapse4(const std::vector<Node3>& n3) {
   std::vector<Node4> out;
   if (n3.empty()) return out;
@@ -476,18 +520,17 @@ int wostgpu_scene3_create(const double* tri, const int32_t* kind, const int32_t*
     const int leaf_max = sah && rule.size() >= 4 ? std::max(1, std::min(7, rule[3] - '0')) : (sah ? 2 : 4);
     const int sah_bins = sah && rule.size() > 4 ? std::max(2, std::atoi(rule.c_str() + 4)) : 16;
     for (int k = 0; k < 2; ++k) {
-      Builder b(boxes[k], box_pad, sah, leaf_max, sah_bins);
+      Tree b = build_tree(boxes[k], box_pad, sah, leaf_max, sah_bins, k == 0 ? "dirichlet" : "neumann");
       std::vector<Tri3> leaf(b.order.size());
       for (size_t i = 0; i < b.order.size(); ++i) leaf[i] = tris[ids[k][b.order[i]]];
-      s->n_node[k] = static_cast<int64_t>(b.nodes.size());
-      if (!b.nodes.empty()) {
-        s->node[k].upload(b.nodes.data(), b.nodes.size());
+      s->n_node[k] = static_cast<int64_t>(b.n3.size());
+      if (!b.n3.empty()) {
+        s->node[k].upload(b.n3.data(), b.n3.size());
         s->tri[k].upload(leaf.data(), leaf.size());
         v.node[k] = s->node[k].as<Node3>();
         v.tri[k] = s->tri[k].as<Tri3>();
         {  // the 4-wide BVHs (closest point / rays)
-          std::vector<Node4> n4 = collapse4(b.nodes);
-          s->node4k[k].upload(n4.data(), n4.size());
+          s->node4k[k].upload(b.n4.data(), b.n4.size());
           (k == 0 ? v.node4 : v.node4n) = s->node4k[k].as<Node4>();
         }
         if (k == 0) {  // fp32 boxes of the Dirichlet triangles, rounded outward (closest-point prefilter)
@@ -516,16 +559,15 @@ int wostgpu_scene3_create(const double* tri, const int32_t* kind, const int32_t*
         eb[i].grow(edges[i].a);
         eb[i].grow(edges[i].b);
       }
-      Builder b(eb, box_pad, sah, leaf_max, sah_bins);
+      Tree b = build_tree(eb, box_pad, sah, leaf_max, sah_bins, "silhouette edges");
       std::vector<Edge3> leaf(edges.size());
       for (size_t i = 0; i < edges.size(); ++i) leaf[i] = edges[b.order[i]];
-      s->n_node[2] = static_cast<int64_t>(b.nodes.size());
-      s->node[2].upload(b.nodes.data(), b.nodes.size());
+      s->n_node[2] = static_cast<int64_t>(b.n3.size());
+      s->node[2].upload(b.n3.data(), b.n3.size());
       s->edge.upload(leaf.data(), leaf.size());
       v.node[2] = s->node[2].as<Node3>();
       v.edge = s->edge.as<Edge3>();
-      std::vector<Node4> n4 = collapse4(b.nodes);
-      s->node4k[2].upload(n4.data(), n4.size());
+      s->node4k[2].upload(b.n4.data(), b.n4.size());
       v.node4e = s->node4k[2].as<Node4>();
     }
     s->values.upload(values, static_cast<size_t>(n_values));
