@@ -9,9 +9,12 @@
 // compile with -fmad=false (Makefile), so results are bit-identical.
 //
 // HBM layout (per kind: Dirichlet, Neumann; plus the silhouette-edge index):
-//   Node3  32 B  {lo.xyz f32, a i32 | hi.xyz f32, b i32}: one 16-B load per
-//          half; bounds rounded outward from fp64 so pruning is conservative.
-//          Internal: children a, b. Leaf: b = -count, primitives [a, a+count).
+//   Node4 128 B  four children's fp32 boxes (SoA, rounded outward from fp64
+//          so pruning is conservative) + child codes (interior node index, or
+//          a leaf's first primitive and count); every device traversal uses
+//          these 4-wide trees (SAH-built binary trees collapsed, wg3_scene.cu).
+//   Node3  32 B  the binary tree they come from {lo.xyz f32, a i32 | hi.xyz
+//          f32, b i32} (kept on the device as the per-kind presence flag).
 //   Tri3   88 B  vertices (fp64), original id, value index, kind; stored in
 //          leaf order so a leaf's triangles are contiguous.
 //   Edge3 104 B  endpoints, the two incident Neumann normals, type.
@@ -110,11 +113,6 @@ struct Scene3View {
 
 __device__ __forceinline__ D3 ld3(const double* p) { return {p[0], p[1], p[2]}; }
 
-__device__ __forceinline__ void ld_node(const Node3* n, float4& lo, float4& hi) {
-  const float4* q = reinterpret_cast<const float4*>(n);
-  lo = __ldg(q);
-  hi = __ldg(q + 1);
-}
 
 // fp32 lower bound of box_d2 for BVH pruning: the point as an fp32
 // interval [lo, hi] (rounded outward), per-axis gaps and the sum rounded
@@ -198,33 +196,9 @@ __device__ __forceinline__ bool ray_tri(D3 o, D3 d, D3 a, D3 b, D3 c, double* t)
   return true;
 }
 
-// slab test against [0, t_hi] with precomputed inverse direction
-__device__ __forceinline__ bool ray_box(D3 o, D3 inv, const bool* dz, const float4& lo,
-                                        const float4& hi, double t_hi) {
-  double t0 = 0.0, t1 = t_hi;
-  const double oo[3] = {o.x, o.y, o.z}, iv[3] = {inv.x, inv.y, inv.z};
-  const double l[3] = {lo.x, lo.y, lo.z}, h[3] = {hi.x, hi.y, hi.z};
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    if (dz[a]) {
-      if (oo[a] < l[a] || oo[a] > h[a]) return false;
-      continue;
-    }
-    double ta = (l[a] - oo[a]) * iv[a], tb = (h[a] - oo[a]) * iv[a];
-    if (ta > tb) {
-      double s = ta;
-      ta = tb;
-      tb = s;
-    }
-    t0 = fmax(t0, ta);
-    t1 = fmin(t1, tb);
-    if (t0 > t1) return false;
-  }
-  return true;
-}
 
-// traversal stack capacities: a 4-wide descent pushes at most 3 entries per
-// interior node on its path, a binary one at most 1 net; the scene build
+// traversal stack capacity: a 4-wide descent pushes at most 3 entries per
+// interior node on its path; the scene build
 // checks its trees' depths against these (wg3_scene.cu: an SAH tree that is
 // too deep is rebuilt with median splits, and a median tree that is too deep
 // fails the scene). The 4-wide stacks live in local memory: 40 entries
@@ -234,7 +208,7 @@ __device__ __forceinline__ bool ray_box(D3 o, D3 inv, const bool* dz, const floa
 #ifndef WG3_STACK4
 #define WG3_STACK4 40
 #endif
-constexpr int kStack4 = WG3_STACK4, kStack2 = 64;
+constexpr int kStack4 = WG3_STACK4;
 
 struct CP3 {
   D3 p;
@@ -242,53 +216,6 @@ struct CP3 {
   int tri;    // original id, -1 if none
   int local;  // leaf-order index within its kind's triangle array
 };
-
-__device__ __forceinline__ void cp_bvh(const Node3* nodes, const Tri3* tris, D3 x, CP3& best,
-                                       const float4* tbox = nullptr) {
-  if (!nodes) return;
-  const PtBox pb = pt_box(x);
-  float bf = __double2float_ru(best.d2);
-  int stack[kStack2];
-  int sp = 0;
-  stack[sp++] = 0;
-  while (sp) {
-    float4 lo, hi;
-    ld_node(nodes + stack[--sp], lo, hi);
-    if (box_d2_lb(lo, hi, pb) > bf) continue;
-    int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
-    if (b < 0) {
-      for (int i = a; i < a - b; ++i) {
-        // the triangle's own fp32 box bounds its distance from below: skip
-        // the fp64 closest-point test when the box is certainly farther
-        if (tbox && box_d2_lb(tbox[2 * i], tbox[2 * i + 1], pb) > bf) continue;
-        const Tri3& t = tris[i];
-        D3 q = closest_on_tri(x, ld3(t.a), ld3(t.b), ld3(t.c));
-        D3 dq = sub(x, q);
-        double d2 = dot(dq, dq);
-        int id = t.id;
-        if (d2 < best.d2 || (d2 == best.d2 && id < best.tri)) {
-          best.d2 = d2;
-          best.p = q;
-          best.tri = id;
-          best.local = i;
-          bf = __double2float_ru(d2);
-        }
-      }
-      continue;
-    }
-    float4 alo, ahi, blo, bhi;
-    ld_node(nodes + a, alo, ahi);
-    ld_node(nodes + b, blo, bhi);
-    const float da = box_d2_lb(alo, ahi, pb), db = box_d2_lb(blo, bhi, pb);
-    if (da <= db) {  // nearer child on top
-      stack[sp++] = b;
-      stack[sp++] = a;
-    } else {
-      stack[sp++] = a;
-      stack[sp++] = b;
-    }
-  }
-}
 
 // closest point over the 4-wide Dirichlet BVH: per node the four children's
 // fp32 lower-bound distances, the nearest child descended into, the other
@@ -419,18 +346,14 @@ __device__ __forceinline__ CP3 closest_dirichlet_seeded(const Scene3View& s, D3 
     best = {q, dot(dq, dq), t.id, seed};
   }
   if (s.node4) cp_bvh4(s.node4, s.tri[0], s.tbox, x, best);
-  else cp_bvh(s.node[0], s.tri[0], x, best, s.tbox);
   return best;
 }
 
 // Accel::closest_point analogue: (point, distance, triangle id) or id -1, d = inf
 __device__ __forceinline__ CP3 closest_point(const Scene3View& s, D3 x, unsigned kinds) {
   CP3 best{{0.0, 0.0, 0.0}, dinf(), -1, -1};
-  if (kinds & WG_KIND_DIRICHLET) {
-    if (s.node4) cp_bvh4(s.node4, s.tri[0], s.tbox, x, best);
-    else cp_bvh(s.node[0], s.tri[0], x, best, s.tbox);
-  }
-  if (kinds & WG_KIND_NEUMANN) cp_bvh(s.node[1], s.tri[1], x, best);
+  if ((kinds & WG_KIND_DIRICHLET) && s.node4) cp_bvh4(s.node4, s.tri[0], s.tbox, x, best);
+  if ((kinds & WG_KIND_NEUMANN) && s.node4n) cp_bvh4(s.node4n, s.tri[1], nullptr, x, best);
   return best;
 }
 
@@ -509,43 +432,8 @@ __device__ __forceinline__ double sil_bvh4(const Scene3View& s, D3 x, double bou
 // bound, only edges strictly closer than sqrt(bound2) are searched for and
 // bound2 comes back when there is none
 __device__ __forceinline__ double closest_silhouette_d2(const Scene3View& s, D3 x, double bound2 = dinf()) {
-  const Node3* nodes = s.node[2];
-  if (!nodes) return dinf();
-  if (s.node4e) return sil_bvh4(s, x, bound2);
-  double best = bound2;
-  const PtBox pb = pt_box(x);
-  float bf = __double2float_ru(best);
-  int stack[kStack2];
-  int sp = 0;
-  stack[sp++] = 0;
-  while (sp) {
-    float4 lo, hi;
-    ld_node(nodes + stack[--sp], lo, hi);
-    if (box_d2_lb(lo, hi, pb) >= bf) continue;
-    int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
-    if (b < 0) {
-      for (int i = a; i < a - b; ++i) {
-        const Edge3& e = s.edge[i];
-        if (!is_silhouette(e, x, s.sil_tol)) continue;
-        D3 dq = sub(x, closest_on_seg(x, ld3(e.a), ld3(e.b)));
-        best = fmin(best, dot(dq, dq));
-      }
-      bf = __double2float_ru(best);
-      continue;
-    }
-    float4 alo, ahi, blo, bhi;
-    ld_node(nodes + a, alo, ahi);
-    ld_node(nodes + b, blo, bhi);
-    const float da = box_d2_lb(alo, ahi, pb), db = box_d2_lb(blo, bhi, pb);
-    if (da <= db) {
-      stack[sp++] = b;
-      stack[sp++] = a;
-    } else {
-      stack[sp++] = a;
-      stack[sp++] = b;
-    }
-  }
-  return best;
+  if (!s.node4e) return dinf();  // no silhouette edges at all
+  return sil_bvh4(s, x, bound2);
 }
 
 __device__ __forceinline__ double closest_silhouette(const Scene3View& s, D3 x) {
@@ -587,47 +475,6 @@ __device__ __forceinline__ bool ray_box_f(const float3& o, const float3& inv, co
     if (t0 > t1) return false;
   }
   return true;
-}
-
-__device__ __forceinline__ void ray_bvh(const Node3* nodes, const Tri3* tris, int kind, D3 o, D3 d,
-                                        double t_max, double t_eps, int exclude, Hit3& h, float pad) {
-  if (!nodes) return;
-  bool dz[3] = {d.x == 0.0, d.y == 0.0, d.z == 0.0};
-  const float3 of = make_float3(static_cast<float>(o.x), static_cast<float>(o.y), static_cast<float>(o.z));
-  const float3 invf = make_float3(dz[0] ? 0.0f : static_cast<float>(1.0 / d.x),
-                                  dz[1] ? 0.0f : static_cast<float>(1.0 / d.y),
-                                  dz[2] ? 0.0f : static_cast<float>(1.0 / d.z));
-  // t bound rounded up, padded like the boxes
-  float tb_f = __double2float_ru(fmin(t_max, h.t)) * (1.0f + 0x1.0p-20f);
-  int stack[kStack2];
-  int sp = 0;
-  stack[sp++] = 0;
-  while (sp) {
-    float4 lo, hi;
-    ld_node(nodes + stack[--sp], lo, hi);
-    if (!ray_box_f(of, invf, dz, lo, hi, tb_f, pad)) continue;
-    int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
-    if (b < 0) {
-      for (int i = a; i < a - b; ++i) {
-        const Tri3& t = tris[i];
-        int id = t.id;
-        if (id == exclude) continue;
-        double th;
-        if (!ray_tri(o, d, ld3(t.a), ld3(t.b), ld3(t.c), &th)) continue;
-        if (!(th > t_eps && th <= t_max)) continue;
-        if (th < h.t || (th == h.t && id < h.tri)) {
-          h.t = th;
-          h.tri = id;
-          h.local = i;
-          h.kind = kind;
-          tb_f = __double2float_ru(fmin(t_max, h.t)) * (1.0f + 0x1.0p-20f);
-        }
-      }
-      continue;
-    }
-    stack[sp++] = b;
-    stack[sp++] = a;
-  }
 }
 
 // first hit over a 4-wide BVH: children slab-tested in fp32 (ray_box_f's
@@ -733,14 +580,8 @@ __device__ __forceinline__ Hit3 ray_first_hit(const Scene3View& s, D3 o, D3 d, d
                                               unsigned kinds, int exclude) {
   Hit3 h{dinf(), -1, -1, -1};
   const float pad = ray_pad(s);
-  if (kinds & WG_KIND_DIRICHLET) {
-    if (s.node4) ray_bvh4(s.node4, s.tri[0], 0, o, d, t_max, s.t_eps, exclude, h, pad);
-    else ray_bvh(s.node[0], s.tri[0], 0, o, d, t_max, s.t_eps, exclude, h, pad);
-  }
-  if (kinds & WG_KIND_NEUMANN) {
-    if (s.node4n) ray_bvh4(s.node4n, s.tri[1], 1, o, d, t_max, s.t_eps, exclude, h, pad);
-    else ray_bvh(s.node[1], s.tri[1], 1, o, d, t_max, s.t_eps, exclude, h, pad);
-  }
+  if ((kinds & WG_KIND_DIRICHLET) && s.node4) ray_bvh4(s.node4, s.tri[0], 0, o, d, t_max, s.t_eps, exclude, h, pad);
+  if ((kinds & WG_KIND_NEUMANN) && s.node4n) ray_bvh4(s.node4n, s.tri[1], 1, o, d, t_max, s.t_eps, exclude, h, pad);
   return h;
 }
 

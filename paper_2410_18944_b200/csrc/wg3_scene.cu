@@ -176,7 +176,7 @@ struct Builder {
 // replaced by its own two children until there are four; boxes are the
 // binary nodes' (outward-rounded) boxes
 // interior nodes on the longest root-to-leaf path (binary / 4-wide): the
-// traversal stacks need depth + 1 (binary) and 3 x depth (4-wide) entries
+// device's 4-wide traversal stacks need 3 x depth entries
 int depth2(const std::vector<Node3>& n, int i = 0) {
   if (n.empty() || n[i].b < 0) return 0;
   return 1 + std::max(depth2(n, n[i].a), depth2(n, n[i].b));
@@ -195,7 +195,7 @@ bool depths_fit(const std::vector<Node3>& n3, const std::vector<Node4>& n4, cons
   if (std::getenv("WOSTGPU_BVH3_STATS"))
     std::fprintf(stderr, "bvh3 %s: %zu binary nodes depth %d, %zu 4-wide nodes depth %d\n", what, n3.size(), d2,
                  n4.size(), d4);
-  return d2 + 1 <= kStack2 && 3 * d4 <= kStack4;
+  return 3 * d4 <= kStack4;
 }
 
 // the BVH of one primitive set: the configured split rule, median splits if
