@@ -65,6 +65,11 @@ int wostgpu_field3_create(const wg_field_config* cfg, const double bbox[6], uint
 /* mlp = WG_MLP_EXACT: fp32 CUDA cores in the oracle's operation order (bit
  * for bit); WG_MLP_TENSOR: tcgen05 split-fp16 MMAs (~1e-6 relative) */
 int wostgpu_field3_eval_batch(wg_field field, int64_t n, const double* xyz, double* out, int mlp);
+/* diagnostic (the tensor-core 3D direction kernel's fp32 mixture math): decode
+ * raw row i (41 floats, K = 8) and evaluate the d = 3 mixture pdf at the unit
+ * direction nu[i] (normalize_params + mixture_pdf, sphdist.cpp:176-185,
+ * 287-310); out[2i] = pdf, out[2i+1] = c */
+int wostgpu_mixture3f_pdf(int64_t n, const float* raw, const double* nu, double* out);
 
 /* ---- solver ------------------------------------------------------------------
  * solve_batch / Engine analogues over 3D points (include/wostgpu.h for the

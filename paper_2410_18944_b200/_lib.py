@@ -57,6 +57,7 @@ _SIGS = {
     "wostgpu_mixture32_pdf": (C.c_int, [C.c_int64, F32, D, D]),
     "wostgpu_field_check_pack": (C.c_int, [VP, I64]),
     "wostgpu_mixture32_sample": (C.c_int, [F32, C.c_int64, C.c_uint64, D]),
+    "wostgpu_mixture3f_pdf": (C.c_int, [C.c_int64, F32, D, D]),
     "wostgpu_solver_create": (C.c_int, [VP, VP, C.POINTER(abi.SolverConfig), C.POINTER(VP)]),
     "wostgpu_solver_destroy": (C.c_int, [VP]),
     "wostgpu_solver_set_mlp": (C.c_int, [VP, C.c_int]),

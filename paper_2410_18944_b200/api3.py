@@ -31,6 +31,19 @@ def _xyz(x):
     return x
 
 
+def mixture3f_pdf(raw, nu):
+    """The tensor-core 3D direction kernel's fp32 mixture math (diagnostic):
+    decode each raw row (41 floats, K = 8) and evaluate the d = 3 mixture pdf
+    at the unit direction nu[i]; returns (pdf [n], c [n])."""
+    raw = np.ascontiguousarray(raw, dtype=np.float32)
+    nu = _xyz(nu)
+    if raw.ndim != 2 or raw.shape[1] != 41 or len(raw) != len(nu):
+        raise ValueError("raw must be [n, 41] with one direction per row")
+    out = np.zeros((raw.shape[0], 2))
+    check(load().wostgpu_mixture3f_pdf(raw.shape[0], raw.ctypes.data_as(C.POINTER(C.c_float)), _d(nu), _d(out)))
+    return out[:, 0], out[:, 1]
+
+
 class Accel3:
     """Triangle-mesh scene with its per-kind BVHs and silhouette-edge index on
     one GPU (the 3D analogue of Accel, proj/src/geom2d.cpp:80-140)."""

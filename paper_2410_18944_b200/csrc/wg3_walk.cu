@@ -833,6 +833,20 @@ int wostgpu_field3_create(const wg_field_config* cfg, const double bbox[6], uint
   });
 }
 
+int wostgpu_mixture3f_pdf(int64_t n, const float* raw, const double* nu, double* out) {
+  return guarded([&] {
+    need(n >= 0 && (n == 0 || (raw && nu && out)), WG_ERR_INVALID, "mixture3f_pdf: bad arguments");
+    if (n == 0) return;
+    DBuf draw, dnu, dout;
+    draw.upload(raw, static_cast<size_t>(n) * OD);
+    dnu.upload(nu, static_cast<size_t>(n) * 3);
+    dout.alloc(sizeof(double) * 2 * n);
+    CKL(launch_mix3f_pdf(n, draw.as<float>(), dnu.as<double>(), dout.as<double>(), 0));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(out, dout.p, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost));
+  });
+}
+
 int wostgpu_field3_eval_batch(wg_field f, int64_t n, const double* x, double* out, int mlp) {
   return guarded([&] {
     need(f->sdim == 3, WG_ERR_INVALID, "field3_eval_batch: 2D field");

@@ -386,6 +386,7 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& w, int sms, unsi
 int walk3_tc_smem();
 int walk3_tc_blocks_per_sm();
 cudaError_t launch_walks3_tc(const Walk3Args& a, int blocks, cudaStream_t st);
+cudaError_t launch_mix3f_pdf(int64_t n, const float* raw, const double* nu, double* out, cudaStream_t st);
 cudaError_t launch_field3_eval_tc(const Field3View& f, int64_t n, const double* x, double* out,
                                   cudaStream_t st);
 

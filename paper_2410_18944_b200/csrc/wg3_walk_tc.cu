@@ -721,6 +721,24 @@ cudaError_t launch_walks3_wave(const Walk3Args& a, const Wave3& v, int sms, unsi
   return cudaGetLastError();
 }
 
+// diagnostic: the direction kernel's fp32 decode + mixture density of raw
+// rows (41 floats) at unit directions nu (tests compare it with the oracle)
+__global__ void mix3f_pdf_kernel(int64_t n, const float* raw, const double* nu, double* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float r[OD];
+  for (int j = 0; j < OD; ++j) r[j] = raw[i * OD + j];
+  Mix3f m;
+  normalize3f(r, m);
+  out[2 * i] = mixture_pdf3f(m, D3{nu[3 * i], nu[3 * i + 1], nu[3 * i + 2]});
+  out[2 * i + 1] = sigmoid(static_cast<double>(r[40]));  // c as sample_guided_f forms it
+}
+
+cudaError_t launch_mix3f_pdf(int64_t n, const float* raw, const double* nu, double* out, cudaStream_t st) {
+  mix3f_pdf_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(n, raw, nu, out);
+  return cudaGetLastError();
+}
+
 int walk3_tc_smem() { return static_cast<int>((wg::TcLayout::BYTES + 127) / 128 * 128); }
 
 int walk3_tc_blocks_per_sm() {

@@ -95,3 +95,36 @@ def test_mixture32_sampler_distribution(gpu, orc, lobes):
     assert chi2 < stats.chi2.ppf(1.0 - 1e-5, int(ok.sum())), (chi2, int(ok.sum()))
     # mass outside the well-populated bins matches too
     assert abs(counts[~ok].sum() - exp[~ok].sum()) < 6.0 * math.sqrt(max(exp[~ok].sum(), 1.0)) + 5
+
+
+def test_mixture3f_pdf_matches_oracle(gpu, orc):
+    """The 3D direction kernel's fp32 decode + mixture density
+    (wg3_mix32.cuh normalize3f / mixture_pdf3f) against the oracle's fp64
+    d = 3 normalize_params + mixture_pdf: 5e-5 relative wherever the oracle
+    pdf exceeds 1e-30, kappa from the clamp-low to the clamp-high end."""
+    from paper_2410_18944_b200.api3 import mixture3f_pdf
+    rng = np.random.default_rng(12)
+    n = 4000
+    raw = rng.normal(0.0, 1.5, (n, 41))
+    raw[:, 24:32] = rng.uniform(-16.0, 12.0, (n, 8))  # log kappa
+    raw[:8, 0:3] = 0.0  # zero-norm mean -> fallback direction
+    raw = raw.astype(np.float32)
+    # directions: uniform, plus near a random lobe's mean at ~1/sqrt(kappa)
+    u = rng.normal(size=(n, 3))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    lobe = rng.integers(0, 8, n)
+    mu = raw[np.arange(n)[:, None], 3 * lobe[:, None] + np.arange(3)].astype(np.float64)
+    mn = np.linalg.norm(mu, axis=1, keepdims=True)
+    mu = np.where(mn > 1e-12, mu / np.maximum(mn, 1e-300), u)
+    kap = np.exp(np.clip(raw[np.arange(n), 24 + lobe].astype(np.float64), math.log(1e-6), math.log(1e4)))
+    near = mu + rng.normal(size=(n, 3)) / np.sqrt(np.maximum(kap, 1.0))[:, None]
+    near /= np.linalg.norm(near, axis=1, keepdims=True)
+    nu = np.where((np.arange(n) % 2 == 0)[:, None], u, near)
+    pd, cd = mixture3f_pdf(raw, nu)
+    m = orc.normalize(raw.astype(np.float64), 8, dim=3)
+    f = orc.fn("mixture_pdf")
+    po = np.array([f(abi.vptr(m[i:i + 1]), abi.ptr(np.ascontiguousarray(nu[i]))) for i in range(n)])
+    ok = po > 1e-30
+    rel = np.abs(pd[ok] - po[ok]) / po[ok]
+    assert ok.sum() > n // 2 and rel.max() < 5e-5, (rel.max(), np.argmax(rel))
+    np.testing.assert_allclose(cd, m["c"], rtol=1e-6, atol=1e-7)
