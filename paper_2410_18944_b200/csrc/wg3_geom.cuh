@@ -285,6 +285,17 @@ __device__ __forceinline__ void cp_bvh4(const Node4* nodes, const Tri3* tris, co
   float st_key[kStack4];
   int sp = 0;
   int node = 0;
+  // next: the most recently pushed entry still within the bound
+  auto pop = [&]() {
+    while (sp) {
+      --sp;
+      if (st_key[sp] <= bf) {
+        node = st_code[sp];
+        return true;
+      }
+    }
+    return false;
+  };
   for (;;) {
     if (node >= 0) {
       Kids4 k;
@@ -319,18 +330,7 @@ __device__ __forceinline__ void cp_bvh4(const Node4* nodes, const Tri3* tris, co
     } else {
       cp_leaf(tris, tbox, x, pb, node, best, bf);
     }
-    // next: the most recently pushed entry still within the bound
-    node = 0;
-    bool found = false;
-    while (sp) {
-      --sp;
-      if (st_key[sp] <= bf) {
-        node = st_code[sp];
-        found = true;
-        break;
-      }
-    }
-    if (!found) return;
+    if (!pop()) return;
   }
 }
 
