@@ -375,20 +375,28 @@ __global__ void __launch_bounds__(128, WG3_DIR_MINB) wave_dir_kernel(Walk3Args a
   wg::umma::fence_after();
   wg::tc_wait_weights(smem);
   uint32_t phase = 0;
-  for (unsigned int t = blockIdx.x; t * 128u < n; t += gridDim.x) {
-    const unsigned int row = t * 128u + threadIdx.x;
-    const bool live = row < n;
-    int32_t slot = live ? v.queue[row] : 0;
+  // the next tile's slot and position are loaded while this tile works, so a
+  // tile's gather does not wait on the queue -> lane -> grid load chain
+  unsigned int t = blockIdx.x;
+  int32_t nslot = t * 128u + threadIdx.x < n ? v.queue[t * 128u + threadIdx.x] : -1;
+  D3 nx = nslot >= 0 ? v.lanes[nslot].x : D3{0.0, 0.0, 0.0};
+  for (; t * 128u < n; t += gridDim.x) {
+    const int32_t slot = nslot;
+    const bool live = slot >= 0;
+    const D3 x = nx;
+    const unsigned int rn = (t + gridDim.x) * 128u + threadIdx.x;
+    nslot = rn < n ? v.queue[rn] : -1;
     float in[IN], raw[OD];
     Lane3 w;
     if (live) {
+      gather3_tc(a.f, x, in);
       w = v.lanes[slot];
-      gather3_tc(a.f, w.x, in);
     } else {
 #pragma unroll
       for (int i = 0; i < IN; ++i) in[i] = 0.0f;
     }
     wg::tc_forward<OD>(smem, phase, in, raw);
+    nx = nslot >= 0 ? v.lanes[nslot].x : D3{0.0, 0.0, 0.0};
     if (live) {
       v.dirs[slot] = sample_guided_f(w, a, raw);
       v.lanes[slot].rng = w.rng;
