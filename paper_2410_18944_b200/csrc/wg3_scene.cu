@@ -195,7 +195,11 @@ bool depths_fit(const std::vector<Node3>& n3, const std::vector<Node4>& n4, cons
   if (std::getenv("WOSTGPU_BVH3_STATS"))
     std::fprintf(stderr, "bvh3 %s: %zu binary nodes depth %d, %zu 4-wide nodes depth %d\n", what, n3.size(), d2,
                  n4.size(), d4);
-  return 3 * d4 <= kStack4;
+  // test hook: WOSTGPU_BVH3_STACK lowers the capacity the trees are checked
+  // against (it cannot raise it above the device stacks' kStack4)
+  int cap = kStack4;
+  if (const char* e = std::getenv("WOSTGPU_BVH3_STACK")) cap = std::min(cap, std::max(1, std::atoi(e)));
+  return 3 * d4 <= cap;
 }
 
 // the BVH of one primitive set: the configured split rule, median splits if

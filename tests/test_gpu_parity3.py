@@ -59,6 +59,46 @@ def test_geometry_bit_exact(gpu, o3, name):
     o3.scene_destroy(ho)
 
 
+def test_too_deep_tree_falls_back_to_median_splits(gpu, o3, capfd, monkeypatch):
+    """The scene build checks each 4-wide tree against the device traversal
+    stacks (3 x depth entries): a surface-area-split tree that does not fit
+    is rebuilt with median splits (WOSTGPU_BVH3_STATS prints both attempts)
+    and answers every query exactly like the oracle; a scene whose median
+    tree does not fit either is rejected with WG_ERR_INVALID. The capacity
+    is lowered through the WOSTGPU_BVH3_STACK test hook."""
+    sc = soup_scene(13, 3000)
+    sc.kind[:] = abi.DIRICHLET  # one tree (no Neumann / silhouette-edge trees)
+    sc.value_index[:] = 1
+    monkeypatch.setenv("WOSTGPU_BVH3_STATS", "1")
+    capfd.readouterr()
+    Accel3(sc)
+    depths = [int(ln.rsplit("depth", 1)[1]) for ln in capfd.readouterr().err.splitlines()
+              if ln.startswith("bvh3 dirichlet")]
+    assert len(depths) == 1, depths
+    monkeypatch.setenv("WOSTGPU_BVH3_STACK", str(3 * depths[0] - 1))  # the SAH tree no longer fits
+    acc = Accel3(sc)
+    lines = [ln for ln in capfd.readouterr().err.splitlines() if ln.startswith("bvh3 dirichlet")]
+    assert len(lines) == 2, lines  # the SAH attempt, then the median rebuild
+    assert int(lines[1].rsplit("depth", 1)[1]) < depths[0]
+    ho = o3.scene(sc)
+    x = probes3(23, 3000, 0.0, 1.0)
+    for kinds in (abi.KIND_DIRICHLET, abi.KIND_ALL):
+        a, b = o3.closest_point(ho, x, kinds), acc.closest_point(x, kinds)
+        for u, v in zip(a, b):
+            assert np.array_equal(u, v)
+    d = directions3(24, 3000)
+    tmax = np.full(3000, 2.0)
+    ex = np.full(3000, -1, dtype=np.int32)
+    a = o3.ray_first_hit(ho, x, d, tmax, abi.KIND_ALL, ex)
+    b = acc.ray_first_hit(x, d, tmax, abi.KIND_ALL, ex)
+    for u, v in zip(a, b):
+        assert np.array_equal(u, v)
+    o3.scene_destroy(ho)
+    monkeypatch.setenv("WOSTGPU_BVH3_STACK", "3")  # not even a median tree fits
+    with pytest.raises(Exception, match="too deep"):
+        Accel3(sc)
+
+
 def test_field3_init_and_eval_bit_exact(gpu, o3):
     cfg = abi.field_config3()
     fo = o3.field(cfg, BOX, 13)
