@@ -37,6 +37,9 @@ struct wg_solver3_s {
   // wavefront walk pool (WG_MLP_TENSOR guided walks, wg3_walk_tc.cu)
   wgrt::DBuf w_lanes, w_dirs, w_rec, w_state, w_queue, w_qlen, w_next, w_blob, w_perm, w_bins, w_sbin, g_blob;
   int64_t w_slots = 0;
+  // first-step geometry per start point (StartGeo3), valid for the current points
+  wgrt::DBuf start_geo;
+  bool start_ok = false;
   unsigned int* h_qlen = nullptr;  // pinned
   // training
   wgrt::DBuf grad, lists, ctl, totals;

@@ -27,6 +27,19 @@
 
 namespace wg3 {
 
+// begin_step's first-step geometry at every start point (StartGeo3): the
+// same calls, in the same order and arithmetic, as step_begin makes for a
+// walk at depth 0 (so cached and queried answers are bit-identical)
+__global__ void start_geo3_kernel(Scene3View s, const double* points, int64_t n, StartGeo3* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const D3 x{points[3 * i], points[3 * i + 1], points[3 * i + 2]};
+  const CP3 cd = closest_dirichlet_seeded(s, x, -1);
+  const double dd = cd.tri >= 0 ? sqrt(cd.d2) : dinf();
+  const double bound2 = dd == dinf() ? dinf() : dd * dd;
+  out[i] = StartGeo3{cd, closest_silhouette_d2(s, x, bound2)};
+}
+
 template <bool GUIDED>
 __global__ void __launch_bounds__(128) walk3_kernel(Walk3Args a) {
   extern __shared__ __align__(16) float mlp_s[];
@@ -508,6 +521,14 @@ void enqueue3_rounds(wg_solver3_s* s, uint64_t seed, uint64_t wpp_first, int32_t
   a.rec_tail = collect ? s->rec_tail.as<int32_t>() : nullptr;
   a.rec_term = collect ? s->rec_term.as<double>() : nullptr;
   a.rec_dacc = collect ? s->rec_dacc.as<float>() : nullptr;
+  if (!s->start_ok) {  // once per point set (the scene is fixed per solver)
+    s->start_geo.alloc(sizeof(StartGeo3) * s->n_points);
+    start_geo3_kernel<<<static_cast<unsigned>((s->n_points + 127) / 128), 128, 0, s->st>>>(
+        s->scene->view, s->points.as<double>(), s->n_points, s->start_geo.as<StartGeo3>());
+    CKL(cudaGetLastError());
+    s->start_ok = true;
+  }
+  a.start = s->start_geo.as<StartGeo3>();
   const bool tc = guided && s->mlp == WG_MLP_TENSOR;
   const int smem = guided ? static_cast<int>(sizeof(float) * s->field->view3.mlp_count) : 0;
   if (guided && !tc)
@@ -910,6 +931,7 @@ int wostgpu_solver3_set_points(wg_solver3 s, int64_t n, const double* x, int64_t
     s->point_offset = offset;
     s->last_rounds = 0;
     s->have_records = false;
+    s->start_ok = false;
   });
 }
 

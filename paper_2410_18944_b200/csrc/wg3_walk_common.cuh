@@ -56,6 +56,14 @@ inline bool default_shape3(const Field3View& v) {
   return v.levels == 4 && v.F == 4 && v.in == IN && v.hid == HID && v.od == OD && v.k == K8;
 }
 
+// begin_step's geometry at a start point: every walk of a point begins
+// there, so its first closest-point / silhouette queries (the unseeded,
+// costliest ones) are answered once per point (start_geo3_kernel)
+struct StartGeo3 {
+  CP3 cd;      // closest Dirichlet point (closest_dirichlet_seeded, no seed)
+  double ds2;  // closest_silhouette_d2 bounded by cd's distance squared
+};
+
 struct Walk3Args {
   Scene3View s;
   Field3View f;
@@ -76,6 +84,7 @@ struct Walk3Args {
   double* rec_term;
   float* rec_dacc;  // per record slot: accumulator increments since the walk's
                     // previous record (DevRecord::dacc, held aside in 3D)
+  const StartGeo3* start;  // [n_points] cached first-step geometry (nullptr: query)
 };
 
 struct Lane3 {
@@ -159,7 +168,9 @@ __device__ __forceinline__ void finish3(Lane3& w, const Walk3Args& a, bool escap
 __device__ __forceinline__ bool step_begin(Lane3& w, const Walk3Args& a, bool collect, int& rec) {
   const Scene3View& s = a.s;
   rec = -1;
-  CP3 cd = closest_dirichlet_seeded(s, w.x, w.cp_seed);
+  // the start point's answers are the same for every walk of the point
+  const bool at_start = w.depth == 0 && a.start != nullptr;
+  const CP3 cd = at_start ? a.start[w.point].cd : closest_dirichlet_seeded(s, w.x, w.cp_seed);
   w.cp_seed = cd.local;
   const double dd = cd.tri >= 0 ? sqrt(cd.d2) : dinf();
   if (cd.tri >= 0 && dd <= a.sp.eps) {
@@ -184,7 +195,7 @@ __device__ __forceinline__ bool step_begin(Lane3& w, const Walk3Args& a, bool co
   // silhouette search starts bounded by dD^2 and reports inf when nothing
   // is closer, which leaves R = dD exactly as the unbounded query would
   const double bound2 = dd == dinf() ? dinf() : dd * dd;
-  const double ds2 = closest_silhouette_d2(s, w.x, bound2);
+  const double ds2 = at_start ? a.start[w.point].ds2 : closest_silhouette_d2(s, w.x, bound2);
   const double dsil = ds2 < bound2 ? sqrt(ds2) : dinf();
   if (dd == dinf() && dsil == dinf()) {  // SceneError, wost.cpp:184-186
     atomicOr(&a.counters[4], 1ull);
