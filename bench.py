@@ -197,7 +197,12 @@ def cpu_reference_run(rounds, threads, mode=3, preset=PRESET, grid=GRID, train_u
 # cfg 4 CPU sample: the 3D oracle port (the reference has no 3D code) on a
 # G x G slice for R rounds, the first R/4 of them training (the full
 # workload's 256 : 768 split of training to frozen rounds)
-CPU3_GRID, CPU3_ROUNDS = 96, 8
+# 3D oracle-port samples of the cfg 4 workload (same domain, slice and 1:3
+# training : frozen split): the product arm's cpu_baseline is one sample of
+# ~10 s of host work; the reference arm times a smaller sample per step so
+# its whole --steps K --warmup W run stays within a few minutes
+CPU3_GRID, CPU3_ROUNDS = 128, 64
+REF3_GRID, REF3_ROUNDS = 96, 16
 
 
 def cpu_oracle3_run(grid, rounds, train_until, threads):
@@ -217,12 +222,13 @@ def cpu_oracle3_run(grid, rounds, train_until, threads):
     o3.field_destroy(f)
     o3.scene_destroy(h)
     walks = grid * grid * rounds
-    return {"value": walks / sec, "seconds": sec, "walks": walks, "kind": "port"}
+    return {"value": walks / sec, "seconds": sec, "walks": walks, "kind": "port", "grid": grid, "rounds": rounds}
 
 
 def cpu3_sample_text(c):
-    return (f"{CPU3_ROUNDS} wpp rounds ({CPU3_ROUNDS // 4} training, {CPU3_ROUNDS - CPU3_ROUNDS // 4} frozen: "
-            f"the workload's 1:3 split) of a {CPU3_GRID}x{CPU3_GRID} slice of the cfg 4 domain "
+    g, r = c["grid"], c["rounds"]
+    return (f"{r} wpp rounds ({r // 4} training, {r - r // 4} frozen: "
+            f"the workload's 1:3 split) of a {g}x{g} slice of the cfg 4 domain "
             f"({c['walks']} walks, {c['seconds']:.1f} s) through the 3D oracle port "
             f"(oracle/wost3d.inc; the reference has no 3D code)")
 
@@ -270,13 +276,13 @@ def run_reference(args):
         return
     # cfg 4 / 5: the 3D oracle port on a bounded sample
     for _ in range(args.warmup):
-        cpu_oracle3_run(CPU3_GRID, CPU3_ROUNDS, CPU3_ROUNDS // 4, threads)
-    rr = [cpu_oracle3_run(CPU3_GRID, CPU3_ROUNDS, CPU3_ROUNDS // 4, threads) for _ in range(args.steps)]
+        cpu_oracle3_run(REF3_GRID, REF3_ROUNDS, REF3_ROUNDS // 4, threads)
+    rr = [cpu_oracle3_run(REF3_GRID, REF3_ROUNDS, REF3_ROUNDS // 4, threads) for _ in range(args.steps)]
     value = float(np.mean([x["value"] for x in rr]))
     line = dict(base, value=value, ms_per_step=float(np.mean([x["seconds"] for x in rr])) * 1e3,
                 scaling="strong" if args.workload == "cfg5" else "weak",
-                config={"workload": f"{args.workload} oracle-port sample {CPU3_GRID}x{CPU3_GRID} x "
-                                    f"{CPU3_ROUNDS} wpp"},
+                config={"workload": f"{args.workload} oracle-port sample {REF3_GRID}x{REF3_GRID} x "
+                                    f"{REF3_ROUNDS} wpp"},
                 cpu_baseline={"value": value, "unit": "walks/s", "cores": threads, "kind": "port",
                               "sample": cpu3_sample_text(rr[0])},
                 e2e={"value": value, "unit": "walks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
