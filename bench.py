@@ -201,7 +201,7 @@ def cpu_reference_run(rounds, threads, mode=3, preset=PRESET, grid=GRID, train_u
 # training : frozen split): the product arm's cpu_baseline is one sample of
 # ~10 s of host work; the reference arm times a smaller sample per step so
 # its whole --steps K --warmup W run stays within a few minutes
-CPU3_GRID, CPU3_ROUNDS = 128, 64
+CPU3_GRID, CPU3_ROUNDS = 128, 104
 REF3_GRID, REF3_ROUNDS = 96, 16
 
 
