@@ -88,14 +88,18 @@ def _trimmed(v, frac=0.1):
 @pytest.mark.parametrize("walk", ["wave", "lockstep"])
 def test_cfg3_seeds_relmse_and_vr_within_10_percent(gpu, monkeypatch, walk):
     """cfg 3 (const-source-disk: source term f = 4, eps = 1e-6, learnable MIS
-    trained every round) at 128^2 x 256 wpp over 32 seeds, through the 2D
+    trained every round) at 128^2 x 256 wpp over 64 seeds, through the 2D
     wavefront pair (forced: the pair the configured 512^2 grid selects) and
     the lockstep kernel (the default at 128^2), against the reference's own
     run_solve over its seeds (tests/golden/ref_cfg3_seeds.json,
     tests/golden/make_cfg3_seeds.py): the trimmed-mean relMSE and the
     variance-reduction factor over uniform within 10% of the reference's.
     Uniform walks are the reference's walk for walk (seed 1 checked), so
-    both VR factors share the reference's uniform relMSE."""
+    both VR factors share the reference's uniform relMSE. Training sums
+    gradients with fp32 atomics, so our per-seed relMSE varies from run to
+    run: a 32-seed trimmed mean moved by 8% between two runs, 64 seeds bring
+    its spread to ~3-4% (bootstrap over 64-seed runs: ratio 1.01 wave / 1.03
+    lockstep against the reference's seeds).
     with open(os.path.join(G, "ref_cfg3_seeds.json")) as f:
         ref = json.load(f)
     ref_g = [float(v) for v in ref["learnable_mis"].values()]
@@ -107,7 +111,7 @@ def test_cfg3_seeds_relmse_and_vr_within_10_percent(gpu, monkeypatch, walk):
     truth = np.array([pr.analytic(x, y) for x, y in pts])
     acc = api.Accel(pr.scene)
     g = []
-    for seed in range(1, 33):
+    for seed in range(1, 65):
         f = api.GuidingField(abi.field_config(), pr.scene.bbox, seed)
         s = api.Solver(acc, f, abi.solver_config("learnable_mis"), api.MLP_TENSOR)
         s.set_points(pts)
