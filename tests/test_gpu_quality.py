@@ -99,7 +99,7 @@ def test_cfg3_seeds_relmse_and_vr_within_10_percent(gpu, monkeypatch, walk):
     gradients with fp32 atomics, so our per-seed relMSE varies from run to
     run: a 32-seed trimmed mean moved by 8% between two runs, 64 seeds bring
     its spread to ~3-4% (bootstrap over 64-seed runs: ratio 1.01 wave / 1.03
-    lockstep against the reference's seeds).
+    lockstep against the reference's seeds)."""
     with open(os.path.join(G, "ref_cfg3_seeds.json")) as f:
         ref = json.load(f)
     ref_g = [float(v) for v in ref["learnable_mis"].values()]
