@@ -2,7 +2,8 @@
 learnable MIS with train_until 256, and uniform) for seeds 1-8, through the
 reference's own run_solve (oracle/_ref/libwost_ref_fast.so). Writes
 tests/golden/ref_cfg3_seeds.json, the reference side of the cfg-3 quality
-comparison (tools/cfg3_check.py, tests/test_gpu_quality.py).
+comparison (tools/cfg3_check.py, tests/test_gpu_quality.py); the committed
+file holds seeds 1-31.
 
 Runs ~40 min per 8 seeds on 8 cores: python tests/golden/make_cfg3_seeds.py [first last]
 (seeds first..last, merged into the existing file; default 1-8)
